@@ -1,0 +1,198 @@
+/* crsh.h — C ABI of the B200-native Coherent Ray-Space Hierarchy (CRSH)
+ * secondary-ray path (Reis, Costa & Pereira, arXiv 2312.06538).
+ *
+ * Citations: "P:n" = line n of the paper text; "S:n" = line n of
+ * SPEC.md; "R#" = a reading in DESIGN.md §3. The library is libcrsh.so in
+ * paper_2312_06538_b200/ (hand-written sm_100a CUDA + C++ host runtime).
+ *
+ * Conventions for every call:
+ *  - Pointers documented "device" must be CUDA device pointers on the scene's
+ *    device; "host" pointers are ordinary host memory. No torch types.
+ *  - All calls return a crsh_status; argument and limit errors are detected
+ *    synchronously before any work is enqueued (CRSH_EINVAL / CRSH_ELIMIT).
+ *    Asynchronous CUDA failures surface as CRSH_ECUDA from the failing call or
+ *    from the next crsh_stats(). crsh_last_error() gives a thread-local text.
+ *  - One scene is used by one host thread and one stream at a time.
+ *  - There is no CPU fallback: without a usable CUDA device every compute call
+ *    fails with CRSH_ECUDA.
+ */
+#ifndef CRSH_H_
+#define CRSH_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct crsh_scene* crsh_scene_t;
+
+/* Status codes; 2/3/4 mirror the CPU program's exit codes. */
+typedef enum {
+  CRSH_OK = 0,
+  CRSH_EINVAL = 2, /* bad argument (null pointer, bad mesh ids, bad option) */
+  CRSH_EIO = 3,    /* host buffer too small for a tap */
+  CRSH_ELIMIT = 4, /* exceeds an encoding limit (lights > 16, slots >= 2^30, ...) */
+  CRSH_ENOMEM = 5, /* device allocation failed */
+  CRSH_ECUDA = 6,  /* CUDA runtime error (incl. no device) */
+  CRSH_ENCCL = 7   /* reserved for collective failures */
+} crsh_status;
+
+/* Ray types (bitmask), "Batches can consist of any combination of
+ * shadow rays, reflection rays or refraction rays". One hierarchy segment per
+ * type (R5): segment 0 = SH (all lights), 1 = RE, 2 = RR. */
+enum { CRSH_SHADOW = 1u, CRSH_REFLECT = 2u, CRSH_REFRACT = 4u };
+
+/* Option flags. CRSH_F_SORT | CRSH_F_MESH_CULL is the paper's CRSH; neither is
+ * the RAH baseline of P:47-49 (rays in generation order, no mesh spheres).
+ * CRSH_F_ZORDER selects the Z-order (bit-interleaved) hash layout instead of
+ * the concatenated layout of R6.
+ * CRSH_F_STAGE_TIMING records per-stage CUDA-event times into stage_ms. */
+enum {
+  CRSH_F_SORT = 1u,
+  CRSH_F_MESH_CULL = 2u,
+  CRSH_F_ZORDER = 4u,
+  CRSH_F_STAGE_TIMING = 8u
+};
+
+/* Build a scene (untimed preparation): copies the geometry, computes
+ * per-triangle v0/e1/e2 and padded minimal bounding spheres (R1, R2),
+ * per-mesh minimal bounding spheres [Gar99], the scene AABB,
+ * pad = 1e-5*diag and eps_t = 1e-4*diag (R2, R3).
+ *   tris     device [M][9] float32: v0.xyz, v1.xyz, v2.xyz (row-major)
+ *   mesh_ids device [M] int32, non-decreasing, dense from 0
+ *   M        number of triangles, 1 <= M < 2^31
+ *   device   CUDA device ordinal
+ *   out      receives the scene handle (owned by the caller; destroy with
+ *            crsh_scene_destroy). The caller may free tris/mesh_ids on return.
+ * Errors: EINVAL (null / bad mesh ids), ELIMIT (M, meshes > 2048), ECUDA, ENOMEM. */
+crsh_status crsh_scene_create(const float* tris, const int32_t* mesh_ids, int64_t M, int32_t device,
+                              crsh_scene_t* out);
+void crsh_scene_destroy(crsh_scene_t scene);
+
+/* The primary-hit buffer (the paper's G-buffer: position, normal and
+ * material per pixel). P = width*height; pixel p = y*width + x.
+ *   pos, nrm  [3][P] float32 structure-of-arrays (x plane, y plane, z plane);
+ *             nrm is the unit geometric normal
+ *   mat       [P] int32 material index, -1 = no primary hit
+ *   materials [n_mat][3] float32: reflectivity, transmissivity, ior
+ *   eye       camera position (view vector for reflection/refraction)
+ * For crsh_trace_secondary these are device pointers; for
+ * crsh_trace_secondary_host they are host pointers. */
+typedef struct {
+  int32_t width, height;
+  const float* pos;
+  const float* nrm;
+  const int32_t* mat;
+  const float* materials;
+  int32_t n_mat;
+  float eye[3];
+} crsh_primary_hits;
+
+/* Hierarchy and run options.
+ *   levels      Lv, number of RSH levels built and traversed, 1..8;
+ *               the paper's "hierarchy depth of 2" is Lv = 2
+ *   leaf_size   B0, rays per bottom-level node, power of 2 in [2, 64]
+ *   branching   B, children per upper node ("node subdivision"),
+ *               power of 2 in [2, 32]; B0*B^(Lv-1) <= 2^22
+ *   flags       CRSH_F_* bits
+ *   shard_rank, shard_world  hash-range sharding: this call traverses only
+ *               its contiguous range of top-node groups;
+ *               world 1 = everything. */
+typedef struct {
+  int32_t levels, leaf_size, branching;
+  uint32_t flags;
+  int32_t shard_rank, shard_world;
+} crsh_opts;
+
+/* Ray-primitive test counters of the last trace (Tables 1-4), per
+ * segment s (0 = SH, 1 = RE, 2 = RR) and level k (1 = leaves .. Lv = top;
+ * index 0 unused). Node-vs-mesh-sphere tests are reported separately and are
+ * not part of the paper's totals. brute = rays * M. */
+typedef struct {
+  uint64_t rays[3], slots[3], chunks[3];
+  uint64_t mesh_tests[3], mesh_hits[3];
+  uint64_t tests[3][9], hits[3][9];
+  uint64_t final_tests[3], final_hits[3], rays_hit[3], brute[3];
+  int32_t levels, reserved;
+  float stage_ms[8]; /* generate+trim, compress, sort, decompress, build,
+                        mesh-cull+plan, traverse+final, output */
+} crsh_stats_t;
+
+/* Number of ray slots: P * (n_lights*[SH] + [RE] + [RR]). Slot order (the ray
+ * id): SH light 0 pixels 0..P-1, SH light 1 pixels, ..., then RE pixels, then
+ * RR pixels; only requested types get slots. */
+int64_t crsh_num_slots(int32_t P, int32_t n_lights, uint32_t ray_types);
+
+/* Trace one frame of secondary rays: generate + hash + trim,
+ * compress, radix sort, decompress, build the Lv-level sphere-cone hierarchy,
+ * cull against mesh spheres, traverse, closest-hit Moller-Trumbore tests.
+ *   hits        device G-buffer (see crsh_primary_hits)
+ *   lights      host [n_lights][3] float32, 0 <= n_lights <= 16 (4-bit light
+ *               field of the shadow hash)
+ *   ray_types   CRSH_SHADOW | CRSH_REFLECT | CRSH_REFRACT
+ *   hit_tri     device [slots] int32 out: closest triangle, -1 miss, -2 no ray
+ *   t           device [slots] float32 out: hit distance, +inf on miss / no ray
+ *   stream      cudaStream_t (NULL = legacy default stream); work is enqueued
+ *               on it. The call synchronises the stream twice (to read the
+ *               ray and chunk counts) and returns with the traversal enqueued.
+ * Ties in t go to the smaller triangle index. */
+crsh_status crsh_trace_secondary(crsh_scene_t scene, const crsh_primary_hits* hits, const float* lights,
+                                 int32_t n_lights, uint32_t ray_types, const crsh_opts* opts, int32_t* hit_tri,
+                                 float* t, void* stream);
+
+/* Sharded variant for hash-range multi-GPU runs: writes, for
+ * every slot, a packed uint64 that is min-reducible across ranks:
+ *   owned hit  (float_bits(t) << 32) | tri
+ *   owned miss 0x7F800000FFFFFFFF
+ *   otherwise  0x7FFFFFFFFFFFFFFF (empty slot, or a ray owned by another rank)
+ * packed: device [slots] uint64. After an element-wise MIN across ranks
+ * (e.g. an NCCL all-reduce on int64), crsh_unpack_hits gives hit_tri / t. */
+crsh_status crsh_trace_secondary_packed(crsh_scene_t scene, const crsh_primary_hits* hits, const float* lights,
+                                        int32_t n_lights, uint32_t ray_types, const crsh_opts* opts,
+                                        uint64_t* packed, void* stream);
+/* packed: device [slots]; hit_tri, t: device [slots] outputs. */
+crsh_status crsh_unpack_hits(crsh_scene_t scene, const uint64_t* packed, int64_t slots, int32_t* hit_tri, float* t,
+                             void* stream);
+
+/* End-to-end variant with HOST buffers: hits->pos/nrm/mat/materials and the
+ * outputs hit_tri/t are host pointers. The call copies the G-buffer to the
+ * device, traces, copies the results back and synchronises `stream`. */
+crsh_status crsh_trace_secondary_host(crsh_scene_t scene, const crsh_primary_hits* hits, const float* lights,
+                                      int32_t n_lights, uint32_t ray_types, const crsh_opts* opts, int32_t* hit_tri,
+                                      float* t, void* stream);
+
+/* Counters of the last trace (synchronises its stream). out: host. */
+crsh_status crsh_stats(crsh_scene_t scene, crsh_stats_t* out);
+
+/* Number of CUDA kernels the library launched during the last trace. */
+int64_t crsh_launch_count(crsh_scene_t scene);
+
+/* Thread-local description of the last non-OK status. */
+const char* crsh_last_error(void);
+
+/* Debug taps: copy an intermediate array of the last trace to host memory
+ * (synchronises). segment in {0,1,2}; level used by CRSH_TAP_NODES only.
+ *   host_dst host buffer of cap_bytes; *n_out receives the element count.
+ * Returns CRSH_EIO if cap_bytes is too small (n_out still set). */
+enum {
+  CRSH_TAP_KEYS = 1,         /* u32 compacted keys of the segment, slot order (Fig 4) */
+  CRSH_TAP_VALS = 2,         /* u32 compacted slot ids */
+  CRSH_TAP_CHUNK_KEYS = 3,   /* u32 chunk keys (Fig 5) */
+  CRSH_TAP_CHUNK_BASE = 4,   /* u32 chunk bases, relative to the segment */
+  CRSH_TAP_SORTED_KEYS = 5,  /* u32 sorted keys (Fig 6) */
+  CRSH_TAP_SORTED_SLOTS = 6, /* u32 sorted slot ids (the permutation) */
+  CRSH_TAP_NODES = 7,        /* float[8] nodes (c.xyz, r, a.xyz, alpha) at `level` */
+  CRSH_TAP_SORTED_RAYS = 8,  /* float[8] rays (o.xyz, tmin, d.xyz, tmax) in sorted order */
+  CRSH_TAP_TRI_SPHERES = 9,  /* float[4] padded triangle spheres (scene) */
+  CRSH_TAP_MESH_SPHERES = 10,/* float[4] padded mesh spheres (scene) */
+  CRSH_TAP_SCENE_CONSTS = 11 /* float[8]: aabb min.xyz, max.xyz, pad, eps_t */
+};
+crsh_status crsh_debug_tap(crsh_scene_t scene, int32_t tap, int32_t segment, int32_t level, void* host_dst,
+                           size_t cap_bytes, size_t* n_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CRSH_H_ */

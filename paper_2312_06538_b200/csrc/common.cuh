@@ -1,0 +1,119 @@
+// common.cuh — shared device primitives of the CRSH library: single-pass
+// decoupled look-back prefix (Merrill & Garland) used by the trim, chunk,
+// decompression-scan and plan kernels, warp helpers, and launch constants.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define CRSH_FULL 0xFFFFFFFFu
+
+namespace crsh {
+
+constexpr int MAX_SEG = 3;
+constexpr int MAX_LEVELS = 8;
+
+// ---------------------------------------------------------------- scan tiles
+// 256 threads x 8 items, striped (item i of thread t = tile_base + i*256 + t):
+// coalesced loads, and the (item, warp) lexicographic order equals slot order.
+constexpr int SCAN_THREADS = 256;
+constexpr int SCAN_ITEMS = 8;
+constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
+
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Look-back status word: high 32 bits = flag (0 none, 1 aggregate, 2 inclusive
+// prefix), low 32 bits = value. One 64-bit store publishes flag and value
+// together, so readers never see a flag without its value.
+__device__ __forceinline__ void lb_store(unsigned long long* p, uint32_t flag, uint32_t v) {
+  const unsigned long long w = ((unsigned long long)flag << 32) | v;
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(w) : "memory");
+}
+__device__ __forceinline__ unsigned long long lb_load(const unsigned long long* p) {
+  unsigned long long w;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
+  return w;
+}
+
+// Exclusive prefix of tile `tile` over tiles [0, tile), called by one whole
+// warp after it published this tile's aggregate. Returns the same value in
+// every lane. Tiles are numbered in dispatch order (atomic ticket), so every
+// predecessor is resident or done: the spin always terminates.
+__device__ __forceinline__ uint32_t lb_exclusive(unsigned long long* status, int tile) {
+  const int lane = (int)lane_id();
+  uint32_t excl = 0;
+  int p = tile - 1;
+  while (p >= 0) {
+    const int idx = p - lane;
+    unsigned long long w = idx >= 0 ? lb_load(&status[idx]) : (2ull << 32);
+    while (__any_sync(CRSH_FULL, (w >> 32) == 0ull)) {
+      if ((w >> 32) == 0ull) w = lb_load(&status[idx]);
+    }
+    const uint32_t inc = __ballot_sync(CRSH_FULL, (w >> 32) == 2ull);
+    const int stop = inc ? __ffs(inc) - 1 : 31;
+    const uint32_t v = lane <= stop ? (uint32_t)w : 0u;
+    excl += __reduce_add_sync(CRSH_FULL, v);
+    if (inc) break;
+    p -= 32;
+  }
+  return excl;
+}
+
+// Warp 0 of a scan tile: exclusive scan of the 64 (item, warp) counts in
+// s_cnt (flattened item-major), tile look-back, publish; writes s_excl[64] and
+// *s_prefix (the tile's global exclusive offset) and returns the tile total.
+__device__ __forceinline__ uint32_t tile_scan_lookback(const uint32_t* s_cnt, uint32_t* s_excl, uint32_t* s_prefix,
+                                                       unsigned long long* status, int tile) {
+  const int lane = (int)lane_id();
+  const uint32_t a = s_cnt[2 * lane], b = s_cnt[2 * lane + 1];
+  uint32_t incl = a + b;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(CRSH_FULL, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const uint32_t ex = incl - (a + b);
+  s_excl[2 * lane] = ex;
+  s_excl[2 * lane + 1] = ex + a;
+  const uint32_t total = __shfl_sync(CRSH_FULL, incl, 31);
+  uint32_t prefix = 0;
+  if (tile == 0) {
+    if (lane == 0) lb_store(&status[0], 2u, total);
+  } else {
+    if (lane == 0) lb_store(&status[tile], 1u, total);
+    __syncwarp();
+    prefix = lb_exclusive(status, tile);
+    if (lane == 0) lb_store(&status[tile], 2u, prefix + total);
+  }
+  if (lane == 0) *s_prefix = prefix;
+  return total;
+}
+
+// Block-wide exclusive scan of one uint32 per thread (blockDim.x == 256).
+__device__ __forceinline__ uint32_t block_excl_scan_256(uint32_t v, uint32_t* s_warp /*8*/, uint32_t* total) {
+  const int lane = (int)lane_id(), warp = threadIdx.x >> 5;
+  uint32_t incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(CRSH_FULL, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  uint32_t wpre = 0, tot = 0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) {
+    const uint32_t x = s_warp[w];
+    wpre += (w < warp) ? x : 0u;
+    tot += x;
+  }
+  __syncthreads();
+  if (total) *total = tot;
+  return wpre + incl - v;
+}
+
+}  // namespace crsh

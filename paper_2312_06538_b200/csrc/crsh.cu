@@ -1,0 +1,854 @@
+// crsh.cu — host runtime and C ABI of the CRSH library (include/crsh.h):
+// scene preparation, a grow-only device arena, the per-frame launch sequence
+// K1..K9 on the caller's stream, counters, debug taps. All compute runs in
+// the kernels of k_*.cuh; there is no CPU fallback.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/crsh.h"
+#include "common.cuh"
+#include "k_build.cuh"
+#include "k_raygen.cuh"
+#include "k_sort.cuh"
+#include "k_traverse.cuh"
+
+using namespace crsh;
+
+namespace {
+
+thread_local std::string g_err;
+
+crsh_status fail(crsh_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+#define CK(call)                                                                                     \
+  do {                                                                                               \
+    cudaError_t e_ = (call);                                                                         \
+    if (e_ != cudaSuccess) return fail(e_ == cudaErrorMemoryAllocation ? CRSH_ENOMEM : CRSH_ECUDA,  \
+                                       "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
+  } while (0)
+
+struct Buf {
+  void* p = nullptr;
+  size_t cap = 0;
+  void release() { if (p) cudaFree(p); p = nullptr; cap = 0; }
+  template <class T> T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+cudaError_t ensure(Buf& b, size_t bytes) {
+  if (bytes <= b.cap && b.p) return cudaSuccess;
+  b.release();
+  size_t want = std::max<size_t>(bytes + bytes / 8, 256);
+  cudaError_t e = cudaMalloc(&b.p, want);
+  if (e == cudaSuccess) b.cap = want;
+  return e;
+}
+
+inline uint32_t cdiv(uint64_t a, uint64_t b) { return (uint32_t)((a + b - 1) / b); }
+inline uint64_t roundup(uint64_t a, uint64_t b) { return (a + b - 1) / b * b; }
+
+// -------------------------------------------------------------- host miniball (scene prep, P:79 [Gar99])
+// Move-to-front Welzl in double: the smallest ball with support set R
+// (|R| <= 4) on its boundary, grown point by point.
+struct HBall { double c[3]; double r2; };
+
+HBall ball_of(const double (*R)[3], int k) {
+  HBall b{{0, 0, 0}, -1.0};
+  if (k == 0) return b;
+  if (k == 1) { for (int i = 0; i < 3; ++i) b.c[i] = R[0][i]; b.r2 = 0; return b; }
+  double a[3], u[3], v[3], w[3];
+  for (int i = 0; i < 3; ++i) a[i] = R[0][i];
+  auto d2 = [](const double* p, const double* q) {
+    return (p[0] - q[0]) * (p[0] - q[0]) + (p[1] - q[1]) * (p[1] - q[1]) + (p[2] - q[2]) * (p[2] - q[2]);
+  };
+  auto cross = [](const double* p, const double* q, double* o) {
+    o[0] = p[1] * q[2] - p[2] * q[1]; o[1] = p[2] * q[0] - p[0] * q[2]; o[2] = p[0] * q[1] - p[1] * q[0];
+  };
+  auto dot = [](const double* p, const double* q) { return p[0] * q[0] + p[1] * q[1] + p[2] * q[2]; };
+  if (k == 2) {
+    for (int i = 0; i < 3; ++i) b.c[i] = (R[0][i] + R[1][i]) * 0.5;
+    b.r2 = d2(R[0], b.c);
+    return b;
+  }
+  for (int i = 0; i < 3; ++i) { u[i] = R[1][i] - a[i]; v[i] = R[2][i] - a[i]; }
+  if (k == 3) {
+    double n[3];
+    cross(u, v, n);
+    const double den = 2.0 * dot(n, n);
+    if (den == 0.0) {   // collinear: widest pair
+      HBall best = b;
+      const int pr[3][2] = {{0, 1}, {0, 2}, {1, 2}};
+      for (auto& q : pr) {
+        const double P2[2][3] = {{R[q[0]][0], R[q[0]][1], R[q[0]][2]}, {R[q[1]][0], R[q[1]][1], R[q[1]][2]}};
+        HBall c = ball_of(P2, 2);
+        if (c.r2 > best.r2) best = c;
+      }
+      return best;
+    }
+    double nu[3], vn[3];
+    cross(n, u, nu);
+    cross(v, n, vn);
+    const double uu = dot(u, u), vv = dot(v, v);
+    for (int i = 0; i < 3; ++i) b.c[i] = a[i] + (nu[i] * vv + vn[i] * uu) / den;
+    b.r2 = d2(R[0], b.c);
+    return b;
+  }
+  for (int i = 0; i < 3; ++i) w[i] = R[3][i] - a[i];
+  double vw[3], wu[3], uv[3];
+  cross(v, w, vw);
+  cross(w, u, wu);
+  cross(u, v, uv);
+  const double det = dot(u, vw);
+  if (det == 0.0) {   // coplanar: largest 3-point ball
+    HBall best = b;
+    for (int skip = 0; skip < 4; ++skip) {
+      double P3[3][3];
+      int m = 0;
+      for (int i = 0; i < 4; ++i) if (i != skip) { for (int c = 0; c < 3; ++c) P3[m][c] = R[i][c]; ++m; }
+      HBall c = ball_of(P3, 3);
+      if (c.r2 > best.r2) best = c;
+    }
+    return best;
+  }
+  const double hu = 0.5 * dot(u, u), hv = 0.5 * dot(v, v), hw = 0.5 * dot(w, w);
+  double x[3];
+  for (int i = 0; i < 3; ++i) x[i] = (vw[i] * hu + wu[i] * hv + uv[i] * hw) / det;
+  for (int i = 0; i < 3; ++i) b.c[i] = a[i] + x[i];
+  b.r2 = dot(x, x);
+  return b;
+}
+
+HBall mtf(std::vector<std::array<double, 3>>& L, size_t n, double (*R)[3], int k) {
+  HBall b = ball_of(R, k);
+  if (k == 4) return b;
+  for (size_t i = 0; i < n; ++i) {
+    const double* p = L[i].data();
+    const double dd = (p[0] - b.c[0]) * (p[0] - b.c[0]) + (p[1] - b.c[1]) * (p[1] - b.c[1]) +
+                      (p[2] - b.c[2]) * (p[2] - b.c[2]);
+    if (b.r2 < 0.0 || dd > b.r2 * (1.0 + 1e-13)) {
+      for (int c = 0; c < 3; ++c) R[k][c] = p[c];
+      b = mtf(L, i, R, k + 1);
+      std::rotate(L.begin(), L.begin() + i, L.begin() + i + 1);
+    }
+  }
+  return b;
+}
+
+// float centre, radius = max distance from it (rounded up), + pad
+void mesh_sphere(const float* tris, int64_t t0, int64_t t1, float pad, float out[4]) {
+  std::vector<std::array<double, 3>> L;
+  L.reserve(3 * (t1 - t0));
+  for (int64_t t = t0; t < t1; ++t)
+    for (int v = 0; v < 3; ++v) L.push_back({tris[9 * t + 3 * v], tris[9 * t + 3 * v + 1], tris[9 * t + 3 * v + 2]});
+  std::vector<std::array<double, 3>> pts(L);
+  double R[4][3];
+  HBall b = mtf(L, L.size(), R, 0);
+  const float cf[3] = {(float)b.c[0], (float)b.c[1], (float)b.c[2]};
+  double r2 = 0.0;
+  for (auto& p : pts) {
+    const double dx = p[0] - (double)cf[0], dy = p[1] - (double)cf[1], dz = p[2] - (double)cf[2];
+    r2 = std::max(r2, dx * dx + dy * dy + dz * dz);
+  }
+  const double r = std::sqrt(r2);
+  float rf = (float)r;
+  if ((double)rf < r) rf = std::nextafter(rf, INFINITY);
+  out[0] = cf[0]; out[1] = cf[1]; out[2] = cf[2]; out[3] = rf + pad;
+}
+
+}  // namespace
+
+// ============================================================== scene
+struct FrameInfo {
+  bool valid = false;
+  int n_seg = 0;
+  int seg_type[MAX_SEG] = {0, 0, 0};
+  uint32_t slots = 0, N = 0, C = 0, Np = 0, G = 0;
+  uint32_t seg_slot_start[MAX_SEG + 1] = {0};
+  uint32_t seg_comp_start[MAX_SEG + 1] = {0};
+  uint32_t seg_n[MAX_SEG] = {0};
+  uint32_t seg_chunk_start[MAX_SEG + 1] = {0};
+  uint32_t seg_C[MAX_SEG] = {0};
+  uint32_t seg_pad_base[MAX_SEG + 1] = {0};
+  int Lv = 0, B0 = 0, B = 0, K = 0;
+  uint32_t span = 0, GR = 0;
+  bool sorted = false;
+  size_t level_off[MAX_LEVELS + 1] = {0};   // node offset (in nodes) of level k in the node arrays
+  uint32_t level_n[MAX_LEVELS + 1] = {0};   // padded nodes at level k
+  float stage_ms[8] = {0};
+  bool timed = false;
+};
+
+struct crsh_scene {
+  int device = 0;
+  int64_t M = 0;
+  int32_t n_meshes = 0;
+  float box_min[3], box_max[3], box_ext[3], pad = 0, eps_t = 0;
+  Buf tri_e, tri_sph, mesh_sph, mesh_first, mesh_count;
+  std::vector<float> h_mesh_sph;
+  // per-frame arena
+  Buf rays, keys_c, vals_c, ckey, cbase, k1, v1, k2, v2, pos, first_chunk, sorted_key, sorted_slot, sorted_rays,
+      nodes, trav, masks, items, best, zero, small, packed_tmp, stage_in, stage_out;
+  unsigned long long* h_counters = nullptr;   // pinned
+  uint32_t* h_small = nullptr;                 // pinned
+  FrameInfo fi;
+  int64_t launches = 0;
+  cudaStream_t last_stream = nullptr;
+  cudaEvent_t ev[10] = {nullptr};
+  int sm_count = 148;
+};
+
+namespace {
+
+// zero region layout (bytes), sized by the slot bound
+struct ZeroLayout {
+  size_t counters, tickets, hist, st_rg, st_rle, st_scan, st_plan, st_radix, radix_tiles_cap, total;
+  static ZeroLayout make(uint64_t S) {
+    ZeroLayout z;
+    size_t o = 0;
+    auto take = [&](size_t b) { size_t r = o; o += (b + 255) & ~size_t(255); return r; };
+    const uint64_t scan_tiles = cdiv(std::max<uint64_t>(S, 1), SCAN_TILE) + 1;
+    z.radix_tiles_cap = cdiv(std::max<uint64_t>(S, 1), SORT_TILE) + MAX_SEG + 1;
+    z.counters = take(8 * MAX_SEG * CTR_STRIDE);
+    z.tickets = take(4 * 32);
+    z.hist = take(4 * MAX_SEG * SORT_PASSES * RADIX_BINS);
+    z.st_rg = take(8 * scan_tiles);
+    z.st_rle = take(8 * scan_tiles);
+    z.st_scan = take(8 * scan_tiles);
+    z.st_plan = take(8 * scan_tiles);
+    z.st_radix = take(4 * SORT_PASSES * z.radix_tiles_cap * RADIX_BINS);
+    z.total = o;
+    return z;
+  }
+};
+
+enum { T_RG = 0, T_RLE = 1, T_SCAN = 2, T_PLAN = 3, T_TRAV = 4, T_RADIX = 8 };
+
+bool is_pow2(int x) { return x > 0 && (x & (x - 1)) == 0; }
+
+template <class F>
+cudaError_t dispatch_b0(int B0, F&& f) {
+  switch (B0) {
+    case 2: return f(std::integral_constant<int, 2>());
+    case 4: return f(std::integral_constant<int, 4>());
+    case 8: return f(std::integral_constant<int, 8>());
+    case 16: return f(std::integral_constant<int, 16>());
+    case 32: return f(std::integral_constant<int, 32>());
+    case 64: return f(std::integral_constant<int, 64>());
+  }
+  return cudaErrorInvalidValue;
+}
+template <class F>
+cudaError_t dispatch_b(int B, F&& f) {
+  switch (B) {
+    case 2: return f(std::integral_constant<int, 2>());
+    case 4: return f(std::integral_constant<int, 4>());
+    case 8: return f(std::integral_constant<int, 8>());
+    case 16: return f(std::integral_constant<int, 16>());
+    case 32: return f(std::integral_constant<int, 32>());
+  }
+  return cudaErrorInvalidValue;
+}
+
+constexpr uint32_t ITEM_TRIS = 8192;
+
+crsh_status trace_impl(crsh_scene* sc, const crsh_primary_hits* h, const float* lights, int32_t n_lights,
+                       uint32_t types, const crsh_opts* o, int32_t* out_hit, float* out_t,
+                       unsigned long long* out_packed, cudaStream_t st) {
+  if (!sc || !h || !o) return fail(CRSH_EINVAL, "null scene / hits / opts");
+  if (h->width <= 0 || h->height <= 0) return fail(CRSH_EINVAL, "width/height must be positive");
+  const uint64_t P64 = (uint64_t)h->width * (uint64_t)h->height;
+  if (P64 >= (1ull << 31)) return fail(CRSH_ELIMIT, "too many pixels");
+  const int32_t P = (int32_t)P64;
+  if (n_lights < 0 || n_lights > 16) return fail(CRSH_ELIMIT, "n_lights must be in [0, 16] (4-bit light field)");
+  if (n_lights > 0 && !lights) return fail(CRSH_EINVAL, "lights is null");
+  if (types == 0 || (types & ~7u)) return fail(CRSH_EINVAL, "bad ray_types");
+  if (!h->pos || !h->nrm || !h->mat || (h->n_mat > 0 && !h->materials) || h->n_mat < 0)
+    return fail(CRSH_EINVAL, "null G-buffer pointer");
+  const int Lv = o->levels, B0 = o->leaf_size, B = o->branching;
+  if (Lv < 1 || Lv > MAX_LEVELS) return fail(CRSH_EINVAL, "levels must be in [1, 8]");
+  if (!is_pow2(B0) || B0 < 2 || B0 > 64) return fail(CRSH_EINVAL, "leaf_size must be a power of 2 in [2, 64]");
+  if (!is_pow2(B) || B < 2 || B > 32) return fail(CRSH_EINVAL, "branching must be a power of 2 in [2, 32]");
+  uint64_t span = B0;
+  for (int k = 1; k < Lv; ++k) span *= B;
+  if (span > (1ull << 22)) return fail(CRSH_ELIMIT, "leaf_size * branching^(levels-1) > 2^22");
+  const int world = std::max(1, o->shard_world), rank = o->shard_rank;
+  if (rank < 0 || rank >= world) return fail(CRSH_EINVAL, "bad shard rank/world");
+  if ((o->flags & ~15u) != 0) return fail(CRSH_EINVAL, "unknown flags");
+  if (!out_packed && (!out_hit || !out_t)) return fail(CRSH_EINVAL, "null output");
+
+  FrameInfo fi;
+  fi.Lv = Lv; fi.B0 = B0; fi.B = B;
+  fi.span = (uint32_t)span;
+  fi.K = span >= 512 ? 1 : (int)std::min<uint64_t>(32, 512 / span);
+  fi.GR = fi.K * fi.span;
+  fi.sorted = (o->flags & CRSH_F_SORT) != 0;
+  fi.timed = (o->flags & CRSH_F_STAGE_TIMING) != 0;
+  uint64_t S = 0;
+  fi.n_seg = 0;
+  const int type_bits[3] = {1, 2, 4};
+  for (int t = 0; t < 3; ++t) {
+    if (!(types & type_bits[t])) continue;
+    const uint64_t ns = (t == 0) ? (uint64_t)P * n_lights : (uint64_t)P;
+    if (ns == 0) continue;
+    fi.seg_type[fi.n_seg] = t;
+    fi.seg_slot_start[fi.n_seg] = (uint32_t)S;
+    ++fi.n_seg;
+    S += ns;
+  }
+  if (S >= (1ull << 30)) return fail(CRSH_ELIMIT, "slots >= 2^30");
+  fi.seg_slot_start[fi.n_seg] = (uint32_t)S;
+  fi.slots = (uint32_t)S;
+  CK(cudaSetDevice(sc->device));
+  sc->launches = 0;
+  sc->last_stream = st;
+  sc->fi.valid = false;
+  if (S == 0) { sc->fi = fi; sc->fi.valid = true; std::memset(sc->h_counters, 0, 8 * MAX_SEG * CTR_STRIDE); return CRSH_OK; }
+  auto mark = [&](int i) -> cudaError_t { return fi.timed ? cudaEventRecord(sc->ev[i], st) : cudaSuccess; };
+
+  // ---------------------------------------------------------------- buffers (slot-bound)
+  const ZeroLayout Z = ZeroLayout::make(S);
+  CK(ensure(sc->zero, Z.total));
+  CK(ensure(sc->small, 256));
+  CK(ensure(sc->rays, 32 * S));
+  CK(ensure(sc->keys_c, 4 * S));
+  CK(ensure(sc->vals_c, 4 * S));
+  CK(cudaMemsetAsync(sc->zero.p, 0, Z.total, st));
+  char* zb = sc->zero.as<char>();
+  unsigned long long* counters = reinterpret_cast<unsigned long long*>(zb + Z.counters);
+  uint32_t* tickets = reinterpret_cast<uint32_t*>(zb + Z.tickets);
+  uint32_t* d_small = sc->small.as<uint32_t>();   // [0..3] comp starts, [4..7] chunk starts, [8] n_items
+  CK(mark(0));
+
+  // ---------------------------------------------------------------- K1: generate + hash + trim
+  {
+    RaygenArgs a{};
+    a.P = P; a.pos = h->pos; a.nrm = h->nrm; a.mat = h->mat; a.materials = h->materials; a.n_mat = h->n_mat;
+    for (int i = 0; i < 3; ++i) a.eye[i] = h->eye[i];
+    for (int i = 0; i < 3 * n_lights; ++i) a.lights[i] = lights[i];
+    a.n_lights = n_lights; a.zorder = (o->flags & CRSH_F_ZORDER) ? 1 : 0;
+    for (int i = 0; i < 3; ++i) { a.box_min[i] = sc->box_min[i]; a.box_ext[i] = sc->box_ext[i]; }
+    a.eps_t = sc->eps_t; a.n_slots = (uint32_t)S; a.n_seg = fi.n_seg;
+    for (int s = 0; s < fi.n_seg; ++s) a.seg_type[s] = fi.seg_type[s];
+    for (int s = 0; s <= fi.n_seg; ++s) a.seg_slot_start[s] = fi.seg_slot_start[s];
+    a.rays = sc->rays.as<float4>(); a.keys_c = sc->keys_c.as<uint32_t>(); a.vals_c = sc->vals_c.as<uint32_t>();
+    a.out_hit = out_packed ? nullptr : out_hit; a.out_t = out_packed ? nullptr : out_t; a.out_packed = out_packed;
+    a.status = reinterpret_cast<unsigned long long*>(zb + Z.st_rg); a.ticket = tickets + T_RG;
+    a.seg_comp_start = d_small;
+    k_raygen<<<cdiv(S, SCAN_TILE), SCAN_THREADS, 0, st>>>(a);
+    CK(cudaGetLastError());
+    ++sc->launches;
+  }
+  CK(cudaMemcpyAsync(sc->h_small, d_small, 4 * (MAX_SEG + 1), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  for (int s = 0; s <= fi.n_seg; ++s) fi.seg_comp_start[s] = sc->h_small[s];
+  fi.N = fi.seg_comp_start[fi.n_seg];
+  for (int s = 0; s < fi.n_seg; ++s) fi.seg_n[s] = fi.seg_comp_start[s + 1] - fi.seg_comp_start[s];
+  fi.seg_pad_base[0] = 0;
+  for (int s = 0; s < fi.n_seg; ++s) fi.seg_pad_base[s + 1] = (uint32_t)(fi.seg_pad_base[s] + roundup(fi.seg_n[s], fi.GR));
+  fi.Np = fi.seg_pad_base[fi.n_seg];
+  fi.G = fi.Np / fi.GR;
+  CK(mark(1));
+  const uint32_t N = fi.N;
+  if (N == 0) {
+    std::memset(sc->h_counters, 0, 8 * MAX_SEG * CTR_STRIDE);
+    CK(cudaMemsetAsync(counters, 0, 8, st));
+    sc->fi = fi; sc->fi.valid = true;
+    return CRSH_OK;
+  }
+
+  // ---------------------------------------------------------------- K2-K4: compress, sort, decompress
+  CK(ensure(sc->sorted_key, 4 * (size_t)fi.Np));
+  CK(ensure(sc->sorted_slot, 4 * (size_t)fi.Np));
+  if (fi.sorted) {
+    CK(ensure(sc->ckey, 4 * (size_t)N));
+    CK(ensure(sc->cbase, 4 * (size_t)(N + 1)));
+    {
+      RleArgs a{};
+      a.N = N; a.keys = sc->keys_c.as<uint32_t>(); a.n_seg = fi.n_seg;
+      for (int s = 0; s <= fi.n_seg; ++s) a.seg_comp_start[s] = fi.seg_comp_start[s];
+      a.ckey = sc->ckey.as<uint32_t>(); a.cbase = sc->cbase.as<uint32_t>(); a.seg_chunk_start = d_small + 4;
+      a.status = reinterpret_cast<unsigned long long*>(zb + Z.st_rle); a.ticket = tickets + T_RLE;
+      k_rle<<<cdiv(N, SCAN_TILE), SCAN_THREADS, 0, st>>>(a);
+      CK(cudaGetLastError());
+      ++sc->launches;
+    }
+    CK(cudaMemcpyAsync(sc->h_small + 4, d_small + 4, 4 * (MAX_SEG + 1), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int s = 0; s <= fi.n_seg; ++s) fi.seg_chunk_start[s] = sc->h_small[4 + s];
+    fi.C = fi.seg_chunk_start[fi.n_seg];
+    for (int s = 0; s < fi.n_seg; ++s) fi.seg_C[s] = fi.seg_n[s] ? fi.seg_chunk_start[s + 1] - fi.seg_chunk_start[s] : 0;
+    CK(mark(2));
+    const uint32_t C = fi.C;
+    CK(ensure(sc->k1, 4 * (size_t)C)); CK(ensure(sc->v1, 4 * (size_t)C));
+    CK(ensure(sc->k2, 4 * (size_t)C)); CK(ensure(sc->v2, 4 * (size_t)C));
+    SegChunks scn{};
+    scn.n_seg = fi.n_seg;
+    uint32_t tiles = 0;
+    for (int s = 0; s < fi.n_seg; ++s) {
+      scn.start[s] = fi.seg_chunk_start[s];
+      scn.count[s] = fi.seg_C[s];
+      scn.tile_start[s] = tiles;
+      tiles += cdiv(fi.seg_C[s], SORT_TILE);
+    }
+    scn.start[fi.n_seg] = C;
+    scn.tile_start[fi.n_seg] = tiles;
+    uint32_t* hist = reinterpret_cast<uint32_t*>(zb + Z.hist);
+    k_radix_hist<<<std::min<uint32_t>(cdiv(C, 256 * 8), 4 * sc->sm_count), 256, 0, st>>>(scn, sc->ckey.as<uint32_t>(), C, hist);
+    CK(cudaGetLastError());
+    ++sc->launches;
+    const size_t sm_bytes = (2 * SORT_TILE + SORT_WARPS * RADIX_BINS) * 4;
+    const uint32_t* kin = sc->ckey.as<uint32_t>();
+    const uint32_t* vin = nullptr;
+    for (int p = 0; p < SORT_PASSES; ++p) {
+      SortPassArgs a{};
+      a.sc = scn; a.pass = p; a.keys_in = kin; a.vals_in = vin;
+      a.keys_out = (p & 1) ? sc->k2.as<uint32_t>() : sc->k1.as<uint32_t>();
+      a.vals_out = (p & 1) ? sc->v2.as<uint32_t>() : sc->v1.as<uint32_t>();
+      a.hist = hist;
+      a.status = reinterpret_cast<uint32_t*>(zb + Z.st_radix) + (size_t)p * Z.radix_tiles_cap * RADIX_BINS;
+      a.ticket = tickets + T_RADIX + p;
+      if (tiles) {
+        k_onesweep<<<tiles, SORT_THREADS, sm_bytes, st>>>(a);
+        CK(cudaGetLastError());
+        ++sc->launches;
+      }
+      kin = a.keys_out; vin = a.vals_out;
+    }
+    CK(mark(3));
+    // K4: decompression
+    CK(ensure(sc->pos, 4 * (size_t)(C + 1)));
+    CK(ensure(sc->first_chunk, 4 * (size_t)(cdiv(N, EXP_TILE) + 1)));
+    {
+      ScanSizeArgs a{};
+      a.C = C; a.N = N; a.sorted_cidx = sc->v2.as<uint32_t>(); a.cbase = sc->cbase.as<uint32_t>();
+      a.pos = sc->pos.as<uint32_t>(); a.first_chunk = sc->first_chunk.as<uint32_t>();
+      a.status = reinterpret_cast<unsigned long long*>(zb + Z.st_scan); a.ticket = tickets + T_SCAN;
+      k_scan_sizes<<<cdiv(C, SCAN_TILE), SCAN_THREADS, 0, st>>>(a);
+      CK(cudaGetLastError());
+      ++sc->launches;
+    }
+    {
+      ExpandArgs a{};
+      a.N = N; a.C = C; a.pos = sc->pos.as<uint32_t>(); a.first_chunk = sc->first_chunk.as<uint32_t>();
+      a.skey = sc->k2.as<uint32_t>(); a.scidx = sc->v2.as<uint32_t>(); a.cbase = sc->cbase.as<uint32_t>();
+      a.vals_c = sc->vals_c.as<uint32_t>(); a.n_seg = fi.n_seg;
+      for (int s = 0; s <= fi.n_seg; ++s) { a.seg_comp_start[s] = fi.seg_comp_start[s]; a.seg_pad_base[s] = fi.seg_pad_base[s]; }
+      a.sorted_key = sc->sorted_key.as<uint32_t>(); a.sorted_slot = sc->sorted_slot.as<uint32_t>();
+      k_expand<<<cdiv(N, EXP_TILE), 256, 0, st>>>(a);
+      CK(cudaGetLastError());
+      ++sc->launches;
+    }
+  } else {
+    CK(mark(2));
+    CK(mark(3));
+    ExpandArgs a{};
+    a.N = N; a.skey = sc->keys_c.as<uint32_t>(); a.vals_c = sc->vals_c.as<uint32_t>(); a.n_seg = fi.n_seg;
+    for (int s = 0; s <= fi.n_seg; ++s) { a.seg_comp_start[s] = fi.seg_comp_start[s]; a.seg_pad_base[s] = fi.seg_pad_base[s]; }
+    a.sorted_key = sc->sorted_key.as<uint32_t>(); a.sorted_slot = sc->sorted_slot.as<uint32_t>();
+    k_copy_unsorted<<<std::min<uint32_t>(cdiv(N, 256), 8 * sc->sm_count), 256, 0, st>>>(a);
+    CK(cudaGetLastError());
+    ++sc->launches;
+  }
+  CK(mark(4));
+
+  // ---------------------------------------------------------------- K5-K6: hierarchy build
+  size_t total_nodes = 0;
+  {
+    uint64_t per = B0;
+    for (int k = 1; k <= Lv; ++k) {
+      fi.level_off[k] = total_nodes;
+      fi.level_n[k] = (uint32_t)(fi.Np / per);
+      total_nodes += fi.level_n[k];
+      per *= B;
+    }
+  }
+  CK(ensure(sc->sorted_rays, 32 * (size_t)fi.Np));
+  CK(ensure(sc->nodes, 32 * total_nodes));
+  CK(ensure(sc->trav, 48 * total_nodes));
+  float4* nodes = sc->nodes.as<float4>();
+  float4* trav = sc->trav.as<float4>();
+  {
+    LeafArgs a{};
+    a.n_leaves = fi.level_n[1]; a.n_seg = fi.n_seg;
+    for (int s = 0; s <= fi.n_seg; ++s) a.seg_pad_base[s] = fi.seg_pad_base[s];
+    for (int s = 0; s < fi.n_seg; ++s) a.seg_n[s] = fi.seg_n[s];
+    a.sorted_slot = sc->sorted_slot.as<uint32_t>(); a.rays = sc->rays.as<float4>();
+    a.sorted_rays = sc->sorted_rays.as<float4>(); a.nodes = nodes; a.trav = trav;
+    CK(dispatch_b0(B0, [&](auto b0) {
+      k_leaves<decltype(b0)::value><<<cdiv(a.n_leaves, 128), 128, 0, st>>>(a);
+      return cudaGetLastError();
+    }));
+    ++sc->launches;
+  }
+  for (int k = 2; k <= Lv; ++k) {
+    UpperArgs a{};
+    a.n_nodes = fi.level_n[k];
+    a.child_nodes = nodes + 2 * fi.level_off[k - 1];
+    a.nodes = nodes + 2 * fi.level_off[k];
+    a.trav = trav + 3 * fi.level_off[k];
+    CK(dispatch_b(B, [&](auto b) {
+      k_upper<decltype(b)::value><<<cdiv(a.n_nodes, 128), 128, 0, st>>>(a);
+      return cudaGetLastError();
+    }));
+    ++sc->launches;
+  }
+  CK(mark(5));
+
+  // ---------------------------------------------------------------- K7-K9: traversal
+  const int W = (sc->n_meshes + 31) / 32;
+  const uint32_t g_lo = (uint32_t)((uint64_t)fi.G * rank / world), g_hi = (uint32_t)((uint64_t)fi.G * (rank + 1) / world);
+  const uint32_t n_top = fi.level_n[Lv];
+  CK(ensure(sc->masks, 4 * (size_t)n_top * W + 4));
+  CK(ensure(sc->best, 8 * (size_t)fi.Np));
+  const uint64_t items_cap = (uint64_t)std::max<uint32_t>(g_hi - g_lo, 1) * cdiv(std::max<int64_t>(sc->M, 1), ITEM_TRIS);
+  CK(ensure(sc->items, 16 * items_cap));
+  CK(cudaMemsetAsync(sc->best.p, 0xFF, 8 * (size_t)fi.Np, st));
+  uint32_t seg_group_start[MAX_SEG + 1], seg_top_start[MAX_SEG + 1];
+  for (int s = 0; s <= fi.n_seg; ++s) {
+    seg_group_start[s] = fi.seg_pad_base[s] / fi.GR;
+    seg_top_start[s] = fi.seg_pad_base[s] / fi.span;
+  }
+  if (g_hi > g_lo) {
+    CullArgs a{};
+    a.top_lo = g_lo * fi.K; a.top_hi = g_hi * fi.K; a.W = W;
+    a.trav_top = trav + 3 * fi.level_off[Lv];
+    a.n_meshes = sc->n_meshes; a.mesh_sph = sc->mesh_sph.as<float4>(); a.mesh_count = sc->mesh_count.as<uint32_t>();
+    a.cull_on = (o->flags & CRSH_F_MESH_CULL) ? 1 : 0;
+    a.masks = sc->masks.as<uint32_t>(); a.counters = counters; a.n_seg = fi.n_seg;
+    for (int s = 0; s <= fi.n_seg; ++s) a.seg_top_start[s] = seg_top_start[s];
+    k_mesh_cull<<<cdiv((uint64_t)(a.top_hi - a.top_lo) * W, 256), 256, 0, st>>>(a);
+    CK(cudaGetLastError());
+    ++sc->launches;
+    PlanArgs p{};
+    p.g_lo = g_lo; p.g_hi = g_hi; p.K = fi.K; p.W = W; p.masks = sc->masks.as<uint32_t>();
+    p.n_meshes = sc->n_meshes; p.mesh_count = sc->mesh_count.as<uint32_t>(); p.item_tris = ITEM_TRIS;
+    p.items = sc->items.as<uint4>(); p.n_items = d_small + 8;
+    p.status = reinterpret_cast<unsigned long long*>(zb + Z.st_plan); p.ticket = tickets + T_PLAN;
+    k_plan<<<cdiv(g_hi - g_lo, SCAN_TILE), SCAN_THREADS, 0, st>>>(p);
+    CK(cudaGetLastError());
+    ++sc->launches;
+    CK(mark(6));
+
+    TravArgs t{};
+    t.Lv = Lv; t.B0 = B0; t.B = B; t.K = fi.K; t.group_rays = fi.GR;
+    t.tile = std::min(512, std::max(32, 4096 / fi.K));
+    t.qcap = Lv <= 3 ? 2048 : (Lv <= 5 ? 1024 : 512);
+    t.qtop_cap = fi.K * t.tile;
+    uint64_t per = 1;
+    for (int k = Lv; k >= 1; --k) { t.per_group[k] = (uint32_t)(fi.K * per); per *= B; }
+    for (int k = 1; k <= Lv; ++k) t.trav[k] = trav + 3 * fi.level_off[k];
+    t.sorted_rays = sc->sorted_rays.as<float4>(); t.tri_e = sc->tri_e.as<float4>(); t.tri_sph = sc->tri_sph.as<float4>();
+    t.masks = sc->masks.as<uint32_t>(); t.W = W; t.n_meshes = sc->n_meshes;
+    t.mesh_first = sc->mesh_first.as<uint32_t>(); t.mesh_count = sc->mesh_count.as<uint32_t>();
+    t.items = sc->items.as<uint4>(); t.n_items = d_small + 8; t.ticket = tickets + T_TRAV;
+    t.best = sc->best.as<unsigned long long>(); t.counters = counters; t.n_seg = fi.n_seg;
+    for (int s = 0; s <= fi.n_seg; ++s) t.seg_group_start[s] = seg_group_start[s];
+    const bool smem_best = fi.GR <= 512;
+    const TravSmem L = TravSmem::make(fi.K, sc->n_meshes, t.tile, Lv, t.qcap, smem_best);
+    auto launch = [&](auto kern) -> cudaError_t {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
+      if (e != cudaSuccess) return e;
+      int per_sm = 0;
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TRAV_THREADS, L.total);
+      if (e != cudaSuccess) return e;
+      per_sm = std::max(1, per_sm);
+      kern<<<per_sm * sc->sm_count, TRAV_THREADS, L.total, st>>>(t, L);
+      return cudaGetLastError();
+    };
+    CK(smem_best ? launch(k_traverse<true>) : launch(k_traverse<false>));
+    ++sc->launches;
+  } else {
+    CK(mark(6));
+  }
+  CK(mark(7));
+  if (g_hi > g_lo) {
+    UnpackArgs a{};
+    a.r_lo = g_lo * fi.GR; a.r_hi = g_hi * fi.GR; a.n_seg = fi.n_seg;
+    for (int s = 0; s <= fi.n_seg; ++s) a.seg_pad_base[s] = fi.seg_pad_base[s];
+    for (int s = 0; s < fi.n_seg; ++s) a.seg_n[s] = fi.seg_n[s];
+    a.sorted_slot = sc->sorted_slot.as<uint32_t>(); a.best = sc->best.as<unsigned long long>();
+    a.out_hit = out_hit; a.out_t = out_t; a.out_packed = out_packed; a.counters = counters;
+    k_unpack<<<cdiv(a.r_hi - a.r_lo, 256), 256, 0, st>>>(a);
+    CK(cudaGetLastError());
+    ++sc->launches;
+  }
+  CK(mark(8));
+  CK(cudaMemcpyAsync(sc->h_counters, counters, 8 * MAX_SEG * CTR_STRIDE, cudaMemcpyDeviceToHost, st));
+  sc->fi = fi;
+  sc->fi.valid = true;
+  return CRSH_OK;
+}
+
+}  // namespace
+
+// ============================================================== C ABI
+extern "C" {
+
+const char* crsh_last_error(void) { return g_err.c_str(); }
+
+int64_t crsh_num_slots(int32_t P, int32_t n_lights, uint32_t t) {
+  if (P < 0 || n_lights < 0) return 0;
+  return (int64_t)P * (((t & 1u) ? n_lights : 0) + ((t & 2u) ? 1 : 0) + ((t & 4u) ? 1 : 0));
+}
+
+crsh_status crsh_scene_create(const float* tris, const int32_t* mesh_ids, int64_t M, int32_t device,
+                              crsh_scene_t* out) {
+  if (!out) return fail(CRSH_EINVAL, "out is null");
+  *out = nullptr;
+  if (!tris || !mesh_ids) return fail(CRSH_EINVAL, "null geometry");
+  if (M < 1 || M >= (1ll << 31)) return fail(CRSH_ELIMIT, "M must be in [1, 2^31)");
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0) return fail(CRSH_ECUDA, "no CUDA device: %s", cudaGetErrorString(e));
+  if (device < 0 || device >= ndev) return fail(CRSH_EINVAL, "bad device ordinal");
+  CK(cudaSetDevice(device));
+  std::vector<float> ht(9 * (size_t)M);
+  std::vector<int32_t> hm((size_t)M);
+  CK(cudaMemcpy(ht.data(), tris, 36 * (size_t)M, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(hm.data(), mesh_ids, 4 * (size_t)M, cudaMemcpyDeviceToHost));
+  if (hm[0] != 0) return fail(CRSH_EINVAL, "mesh ids must start at 0");
+  for (int64_t t = 1; t < M; ++t)
+    if (hm[t] < hm[t - 1] || hm[t] > hm[t - 1] + 1) return fail(CRSH_EINVAL, "mesh ids must be non-decreasing and dense");
+  const int32_t n_meshes = hm[M - 1] + 1;
+  if (n_meshes > 2048) return fail(CRSH_ELIMIT, "more than 2048 meshes");
+  auto* sc = new crsh_scene();
+  sc->device = device;
+  sc->M = M;
+  sc->n_meshes = n_meshes;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) == cudaSuccess) sc->sm_count = prop.multiProcessorCount;
+  for (int k = 0; k < 3; ++k) { sc->box_min[k] = INFINITY; sc->box_max[k] = -INFINITY; }
+  for (int64_t i = 0; i < 3 * M; ++i) {
+    const int k = (int)(i % 3);
+    sc->box_min[k] = std::min(sc->box_min[k], ht[i]);
+    sc->box_max[k] = std::max(sc->box_max[k], ht[i]);
+  }
+  double diag = 0.0;
+  for (int k = 0; k < 3; ++k) {
+    const double ext = (double)sc->box_max[k] - (double)sc->box_min[k];
+    diag += ext * ext;
+    sc->box_ext[k] = sc->box_max[k] - sc->box_min[k];
+  }
+  diag = std::sqrt(diag);
+  sc->pad = (float)(1e-5 * diag);
+  sc->eps_t = (float)(1e-4 * diag);
+  auto bail = [&](crsh_status s) { crsh_scene_destroy(sc); return s; };
+  crsh_status rc = CRSH_OK;
+  auto ck = [&](cudaError_t err, const char* what) {
+    if (err != cudaSuccess && rc == CRSH_OK)
+      rc = fail(err == cudaErrorMemoryAllocation ? CRSH_ENOMEM : CRSH_ECUDA, "%s: %s", what, cudaGetErrorString(err));
+  };
+  ck(ensure(sc->tri_e, 48 * (size_t)M), "alloc tri_e");
+  ck(ensure(sc->tri_sph, 16 * (size_t)M), "alloc tri_sph");
+  ck(ensure(sc->mesh_sph, 16 * (size_t)n_meshes), "alloc mesh_sph");
+  ck(ensure(sc->mesh_first, 4 * (size_t)n_meshes), "alloc mesh_first");
+  ck(ensure(sc->mesh_count, 4 * (size_t)n_meshes), "alloc mesh_count");
+  ck(cudaMallocHost(&sc->h_counters, 8 * MAX_SEG * CTR_STRIDE), "alloc pinned");
+  ck(cudaMallocHost(&sc->h_small, 64), "alloc pinned");
+  for (int i = 0; i < 10 && rc == CRSH_OK; ++i) ck(cudaEventCreate(&sc->ev[i]), "event");
+  if (rc != CRSH_OK) return bail(rc);
+  std::memset(sc->h_counters, 0, 8 * MAX_SEG * CTR_STRIDE);
+  k_tri_prep<<<std::min<int64_t>((M + 255) / 256, 8 * sc->sm_count), 256>>>(tris, M, sc->pad, sc->tri_e.as<float4>(),
+                                                                          sc->tri_sph.as<float4>());
+  ck(cudaGetLastError(), "k_tri_prep");
+  std::vector<uint32_t> first(n_meshes, 0), count(n_meshes, 0);
+  for (int64_t t = 0; t < M; ++t) {
+    if (count[hm[t]] == 0) first[hm[t]] = (uint32_t)t;
+    ++count[hm[t]];
+  }
+  sc->h_mesh_sph.assign(4 * (size_t)n_meshes, 0.0f);
+  for (int m = 0; m < n_meshes; ++m) {
+    if (count[m] == 0) { sc->h_mesh_sph[4 * m + 3] = -1.0f; continue; }
+    mesh_sphere(ht.data(), first[m], first[m] + count[m], sc->pad, &sc->h_mesh_sph[4 * m]);
+  }
+  ck(cudaMemcpy(sc->mesh_sph.p, sc->h_mesh_sph.data(), 16 * (size_t)n_meshes, cudaMemcpyHostToDevice), "copy mesh_sph");
+  ck(cudaMemcpy(sc->mesh_first.p, first.data(), 4 * (size_t)n_meshes, cudaMemcpyHostToDevice), "copy first");
+  ck(cudaMemcpy(sc->mesh_count.p, count.data(), 4 * (size_t)n_meshes, cudaMemcpyHostToDevice), "copy count");
+  ck(cudaDeviceSynchronize(), "scene prep");
+  if (rc != CRSH_OK) return bail(rc);
+  *out = sc;
+  return CRSH_OK;
+}
+
+void crsh_scene_destroy(crsh_scene_t sc) {
+  if (!sc) return;
+  cudaSetDevice(sc->device);
+  Buf* bufs[] = {&sc->tri_e, &sc->tri_sph, &sc->mesh_sph, &sc->mesh_first, &sc->mesh_count, &sc->rays, &sc->keys_c,
+                 &sc->vals_c, &sc->ckey, &sc->cbase, &sc->k1, &sc->v1, &sc->k2, &sc->v2, &sc->pos, &sc->first_chunk,
+                 &sc->sorted_key, &sc->sorted_slot, &sc->sorted_rays, &sc->nodes, &sc->trav, &sc->masks, &sc->items,
+                 &sc->best, &sc->zero, &sc->small, &sc->packed_tmp, &sc->stage_in, &sc->stage_out};
+  for (Buf* b : bufs) b->release();
+  if (sc->h_counters) cudaFreeHost(sc->h_counters);
+  if (sc->h_small) cudaFreeHost(sc->h_small);
+  for (auto& e : sc->ev) if (e) cudaEventDestroy(e);
+  delete sc;
+}
+
+crsh_status crsh_trace_secondary(crsh_scene_t sc, const crsh_primary_hits* h, const float* lights, int32_t n_lights,
+                                 uint32_t types, const crsh_opts* o, int32_t* hit_tri, float* t, void* stream) {
+  return trace_impl(sc, h, lights, n_lights, types, o, hit_tri, t, nullptr, (cudaStream_t)stream);
+}
+
+crsh_status crsh_trace_secondary_packed(crsh_scene_t sc, const crsh_primary_hits* h, const float* lights,
+                                        int32_t n_lights, uint32_t types, const crsh_opts* o, uint64_t* packed,
+                                        void* stream) {
+  if (!packed) return fail(CRSH_EINVAL, "packed is null");
+  return trace_impl(sc, h, lights, n_lights, types, o, nullptr, nullptr,
+                    reinterpret_cast<unsigned long long*>(packed), (cudaStream_t)stream);
+}
+
+crsh_status crsh_unpack_hits(crsh_scene_t sc, const uint64_t* packed, int64_t slots, int32_t* hit_tri, float* t,
+                             void* stream) {
+  if (!sc || !packed || !hit_tri || !t || slots < 0) return fail(CRSH_EINVAL, "bad unpack arguments");
+  if (slots == 0) return CRSH_OK;
+  CK(cudaSetDevice(sc->device));
+  k_unpack_packed<<<std::min<int64_t>((slots + 255) / 256, 8 * sc->sm_count), 256, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const unsigned long long*>(packed), (uint64_t)slots, hit_tri, t);
+  CK(cudaGetLastError());
+  return CRSH_OK;
+}
+
+crsh_status crsh_trace_secondary_host(crsh_scene_t sc, const crsh_primary_hits* h, const float* lights,
+                                      int32_t n_lights, uint32_t types, const crsh_opts* o, int32_t* hit_tri,
+                                      float* t, void* stream) {
+  if (!sc || !h || !hit_tri || !t) return fail(CRSH_EINVAL, "null argument");
+  if (h->width <= 0 || h->height <= 0) return fail(CRSH_EINVAL, "width/height must be positive");
+  CK(cudaSetDevice(sc->device));
+  const size_t P = (size_t)h->width * h->height;
+  const int64_t S = crsh_num_slots((int32_t)P, n_lights, types);
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t in_bytes = 28 * P + 12 * (size_t)std::max(h->n_mat, 0);
+  CK(ensure(sc->stage_in, in_bytes + 64));
+  CK(ensure(sc->stage_out, 8 * (size_t)std::max<int64_t>(S, 1)));
+  char* din = sc->stage_in.as<char>();
+  float* dpos = reinterpret_cast<float*>(din);
+  float* dnrm = dpos + 3 * P;
+  int32_t* dmat = reinterpret_cast<int32_t*>(dnrm + 3 * P);
+  float* dmats = reinterpret_cast<float*>(dmat + P);
+  CK(cudaMemcpyAsync(dpos, h->pos, 12 * P, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(dnrm, h->nrm, 12 * P, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(dmat, h->mat, 4 * P, cudaMemcpyHostToDevice, st));
+  if (h->n_mat > 0) CK(cudaMemcpyAsync(dmats, h->materials, 12 * (size_t)h->n_mat, cudaMemcpyHostToDevice, st));
+  crsh_primary_hits dh = *h;
+  dh.pos = dpos; dh.nrm = dnrm; dh.mat = dmat; dh.materials = dmats;
+  int32_t* dhit = sc->stage_out.as<int32_t>();
+  float* dt = reinterpret_cast<float*>(dhit + S);
+  crsh_status rc = trace_impl(sc, &dh, lights, n_lights, types, o, dhit, dt, nullptr, st);
+  if (rc != CRSH_OK) return rc;
+  CK(cudaMemcpyAsync(hit_tri, dhit, 4 * (size_t)S, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(t, dt, 4 * (size_t)S, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return CRSH_OK;
+}
+
+crsh_status crsh_stats(crsh_scene_t sc, crsh_stats_t* out) {
+  if (!sc || !out) return fail(CRSH_EINVAL, "null argument");
+  CK(cudaSetDevice(sc->device));
+  CK(cudaStreamSynchronize(sc->last_stream));
+  std::memset(out, 0, sizeof(*out));
+  const FrameInfo& fi = sc->fi;
+  if (!fi.valid) return CRSH_OK;
+  out->levels = fi.Lv;
+  for (int s = 0; s < fi.n_seg; ++s) {
+    const int ty = fi.seg_type[s];
+    const unsigned long long* c = sc->h_counters + s * CTR_STRIDE;
+    out->rays[ty] = fi.seg_n[s];
+    out->slots[ty] = fi.seg_slot_start[s + 1] - fi.seg_slot_start[s];
+    out->chunks[ty] = fi.sorted ? fi.seg_C[s] : 0;
+    for (int k = 1; k <= MAX_LEVELS; ++k) { out->tests[ty][k] = c[CTR_TESTS + k]; out->hits[ty][k] = c[CTR_HITS + k]; }
+    out->mesh_tests[ty] = c[CTR_MESH_TESTS];
+    out->mesh_hits[ty] = c[CTR_MESH_HITS];
+    out->final_tests[ty] = c[CTR_FINAL_TESTS];
+    out->final_hits[ty] = c[CTR_FINAL_HITS];
+    out->rays_hit[ty] = c[CTR_RAYS_HIT];
+    out->brute[ty] = (uint64_t)fi.seg_n[s] * (uint64_t)sc->M;
+  }
+  if (fi.timed && fi.N > 0) {
+    for (int i = 0; i < 8; ++i) {
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, sc->ev[i], sc->ev[i + 1]) == cudaSuccess) out->stage_ms[i] = ms;
+    }
+  }
+  return CRSH_OK;
+}
+
+int64_t crsh_launch_count(crsh_scene_t sc) { return sc ? sc->launches : 0; }
+
+crsh_status crsh_debug_tap(crsh_scene_t sc, int32_t tap, int32_t seg_type, int32_t level, void* host_dst,
+                           size_t cap_bytes, size_t* n_out) {
+  if (!sc || !n_out) return fail(CRSH_EINVAL, "null argument");
+  CK(cudaSetDevice(sc->device));
+  CK(cudaStreamSynchronize(sc->last_stream));
+  *n_out = 0;
+  const FrameInfo& fi = sc->fi;
+  const void* src = nullptr;
+  size_t n = 0, esz = 4;
+  std::vector<uint32_t> rel;
+  if (tap == CRSH_TAP_TRI_SPHERES) { src = sc->tri_sph.p; n = (size_t)sc->M; esz = 16; }
+  else if (tap == CRSH_TAP_MESH_SPHERES) { src = sc->mesh_sph.p; n = (size_t)sc->n_meshes; esz = 16; }
+  else if (tap == CRSH_TAP_SCENE_CONSTS) {
+    float c[8] = {sc->box_min[0], sc->box_min[1], sc->box_min[2], sc->box_max[0], sc->box_max[1], sc->box_max[2], sc->pad, sc->eps_t};
+    *n_out = 8;
+    if (cap_bytes < sizeof c) return fail(CRSH_EIO, "buffer too small");
+    std::memcpy(host_dst, c, sizeof c);
+    return CRSH_OK;
+  } else {
+    if (!fi.valid) return fail(CRSH_EINVAL, "no trace yet");
+    int s = -1;
+    for (int q = 0; q < fi.n_seg; ++q) if (fi.seg_type[q] == seg_type) s = q;
+    if (s < 0) return CRSH_OK;   // segment not present: empty
+    const size_t ns = fi.seg_n[s];
+    switch (tap) {
+      case CRSH_TAP_KEYS: src = sc->keys_c.as<uint32_t>() + fi.seg_comp_start[s]; n = ns; break;
+      case CRSH_TAP_VALS: src = sc->vals_c.as<uint32_t>() + fi.seg_comp_start[s]; n = ns; break;
+      case CRSH_TAP_CHUNK_KEYS:
+        if (!fi.sorted) return CRSH_OK;
+        src = sc->ckey.as<uint32_t>() + fi.seg_chunk_start[s]; n = fi.seg_C[s]; break;
+      case CRSH_TAP_CHUNK_BASE: {
+        if (!fi.sorted) return CRSH_OK;
+        n = fi.seg_C[s];
+        rel.resize(n);
+        if (n) CK(cudaMemcpy(rel.data(), sc->cbase.as<uint32_t>() + fi.seg_chunk_start[s], 4 * n, cudaMemcpyDeviceToHost));
+        for (auto& v : rel) v -= fi.seg_comp_start[s];
+        *n_out = n;
+        if (cap_bytes < 4 * n) return fail(CRSH_EIO, "buffer too small");
+        if (n) std::memcpy(host_dst, rel.data(), 4 * n);
+        return CRSH_OK;
+      }
+      case CRSH_TAP_SORTED_KEYS: src = sc->sorted_key.as<uint32_t>() + fi.seg_pad_base[s]; n = ns; break;
+      case CRSH_TAP_SORTED_SLOTS: src = sc->sorted_slot.as<uint32_t>() + fi.seg_pad_base[s]; n = ns; break;
+      case CRSH_TAP_SORTED_RAYS: src = sc->sorted_rays.as<float4>() + 2 * (size_t)fi.seg_pad_base[s]; n = ns; esz = 32; break;
+      case CRSH_TAP_NODES: {
+        if (level < 1 || level > fi.Lv) return fail(CRSH_EINVAL, "bad level");
+        uint64_t per = fi.B0;
+        for (int k = 1; k < level; ++k) per *= fi.B;
+        n = (size_t)((ns + per - 1) / per);
+        src = sc->nodes.as<float4>() + 2 * (fi.level_off[level] + fi.seg_pad_base[s] / per);
+        esz = 32;
+        break;
+      }
+      default: return fail(CRSH_EINVAL, "unknown tap");
+    }
+  }
+  *n_out = n;
+  if (cap_bytes < n * esz) return fail(CRSH_EIO, "buffer too small");
+  if (n) CK(cudaMemcpy(host_dst, src, n * esz, cudaMemcpyDeviceToHost));
+  return CRSH_OK;
+}
+
+}  // extern "C"

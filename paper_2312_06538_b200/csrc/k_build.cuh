@@ -1,0 +1,188 @@
+// k_build.cuh — scene preparation (triangle data + padded minimal spheres,
+// P:173, R1, R2) and the bottom-up hierarchy build (§3.3.6):
+// K5 gathers the sorted rays into a contiguous array and builds the first
+// level (sphere: Eqs 7-8 in balanced pairwise order, R9; cone: Eqs 1-4
+// sequentially in sorted order), K6 builds one upper level (Eqs 5-8).
+//
+// Sorted rays live in a padded layout: every segment starts at a multiple of
+// the traversal group span, so node j of level k covers rays
+// [j*B0*B^(k-1), (j+1)*B0*B^(k-1)) uniformly; padding rays have tmin = -1 and
+// padding nodes r = -1 ("empty"), and neither is tested nor counted.
+#pragma once
+#include "common.cuh"
+#include "numspec.cuh"
+
+namespace crsh {
+
+// ------------------------------------------------------------ scene prep
+__device__ __forceinline__ void dfinalize(double cx, double cy, double cz, const double* px, const double* py,
+                                          const double* pz, float pad, float4* out) {
+  const float fx = (float)cx, fy = (float)cy, fz = (float)cz;
+  double r2 = 0.0;
+  for (int i = 0; i < 3; ++i) {
+    const double dx = px[i] - (double)fx, dy = py[i] - (double)fy, dz = pz[i] - (double)fz;
+    r2 = fmax(r2, dx * dx + dy * dy + dz * dz);
+  }
+  const double r = sqrt(r2);
+  float rf = (float)r;
+  if ((double)rf < r) rf = nextafterf(rf, __int_as_float(0x7f800000));
+  *out = make_float4(fx, fy, fz, rf + pad);
+}
+
+// Per triangle: v0, e1 = v1 - v0, e2 = v2 - v0 (3 float4) and the minimal
+// sphere of its vertices (longest-edge midpoint when right/obtuse, else the
+// circumcentre), centre rounded to float, radius = max distance from that
+// centre rounded up, plus pad.
+__global__ void k_tri_prep(const float* __restrict__ tris, int64_t M, float pad, float4* __restrict__ tri_e,
+                           float4* __restrict__ tri_sph) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < M; t += (int64_t)gridDim.x * blockDim.x) {
+    const float* v = tris + 9 * t;
+    float f[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) f[i] = v[i];
+    tri_e[3 * t] = make_float4(f[0], f[1], f[2], 0.f);
+    tri_e[3 * t + 1] = make_float4(f[3] - f[0], f[4] - f[1], f[5] - f[2], 0.f);
+    tri_e[3 * t + 2] = make_float4(f[6] - f[0], f[7] - f[1], f[8] - f[2], 0.f);
+    const double ax = f[0], ay = f[1], az = f[2], bx = f[3], by = f[4], bz = f[5], cx = f[6], cy = f[7], cz = f[8];
+    const double abx = bx - ax, aby = by - ay, abz = bz - az;
+    const double acx = cx - ax, acy = cy - ay, acz = cz - az;
+    const double bcx = cx - bx, bcy = cy - by, bcz = cz - bz;
+    double ox, oy, oz;
+    if (abx * acx + aby * acy + abz * acz <= 0.0) {                 // angle at a >= 90
+      ox = (bx + cx) * 0.5; oy = (by + cy) * 0.5; oz = (bz + cz) * 0.5;
+    } else if ((-abx) * bcx + (-aby) * bcy + (-abz) * bcz <= 0.0) { // at b
+      ox = (ax + cx) * 0.5; oy = (ay + cy) * 0.5; oz = (az + cz) * 0.5;
+    } else if (acx * bcx + acy * bcy + acz * bcz <= 0.0) {          // at c
+      ox = (ax + bx) * 0.5; oy = (ay + by) * 0.5; oz = (az + bz) * 0.5;
+    } else {                                                        // circumcentre
+      const double nx = aby * acz - abz * acy, ny = abz * acx - abx * acz, nz = abx * acy - aby * acx;
+      const double den = 2.0 * (nx * nx + ny * ny + nz * nz);
+      const double ac2 = acx * acx + acy * acy + acz * acz, ab2 = abx * abx + aby * aby + abz * abz;
+      // (n x ab) * |ac|^2 + (ac x n) * |ab|^2
+      const double qx = (ny * abz - nz * aby) * ac2 + (acy * nz - acz * ny) * ab2;
+      const double qy = (nz * abx - nx * abz) * ac2 + (acz * nx - acx * nz) * ab2;
+      const double qz = (nx * aby - ny * abx) * ac2 + (acx * ny - acy * nx) * ab2;
+      const double inv = 1.0 / den;
+      ox = ax + qx * inv; oy = ay + qy * inv; oz = az + qz * inv;
+    }
+    const double px[3] = {ax, bx, cx}, py[3] = {ay, by, cy}, pz[3] = {az, bz, cz};
+    dfinalize(ox, oy, oz, px, py, pz, pad, &tri_sph[t]);
+  }
+}
+
+// ------------------------------------------------------------ nodes
+__device__ __forceinline__ void store_node(float4* nodes, float4* trav, size_t j, const NodeV& n) {
+  nodes[2 * j] = make_float4(n.c.x, n.c.y, n.c.z, n.r);
+  nodes[2 * j + 1] = make_float4(n.a.x, n.a.y, n.a.z, n.alpha);
+  // traversal layout: {c, d}, {a, tan(alpha)}, {sec(alpha), 0, 0, 0};
+  // wide cones (alpha >= pi/2): a = 0, tan = sec = 1e30 (pass-all, numspec.cuh)
+  float tn = 0.f, sc = 0.f;
+  f3 a = n.a;
+  if (n.r >= 0.0f) {
+    tansec_ns(n.alpha, &tn, &sc);
+    if (n.alpha >= CRSH_PI2_F) a = mk3(0.f, 0.f, 0.f);
+  }
+  trav[3 * j] = make_float4(n.c.x, n.c.y, n.c.z, n.r);
+  trav[3 * j + 1] = make_float4(a.x, a.y, a.z, tn);
+  trav[3 * j + 2] = make_float4(sc, 0.f, 0.f, 0.f);
+}
+__device__ __forceinline__ NodeV load_node(const float4* nodes, size_t j) {
+  const float4 p = nodes[2 * j], q = nodes[2 * j + 1];
+  NodeV n;
+  n.c = mk3(p.x, p.y, p.z); n.r = p.w; n.a = mk3(q.x, q.y, q.z); n.alpha = q.w;
+  return n;
+}
+
+struct LeafArgs {
+  uint32_t n_leaves;                      // padded, all segments
+  int32_t n_seg;
+  uint32_t seg_pad_base[MAX_SEG + 1];
+  uint32_t seg_n[MAX_SEG];
+  const uint32_t* sorted_slot;
+  const float4* rays;                     // [slots][2]
+  float4* sorted_rays;                    // [Np][2]
+  float4* nodes;                          // level 1, paper layout [2 per node]
+  float4* trav;                           // level 1, traversal layout [3 per node]
+};
+
+// K5: one thread per bundle (leaf). The sphere is the balanced pairwise tree
+// ((0,1),(2,3)),((4,5),(6,7)) of radius-0 origin spheres (R9), evaluated with
+// compile-time indices (registers); missing rays pass through (r = -1).
+template <int B0>
+__global__ void __launch_bounds__(128) k_leaves(const LeafArgs a) {
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= a.n_leaves) return;
+  const uint32_t p0 = j * B0;
+  int s = 0;
+  for (int q = 1; q < a.n_seg; ++q) s = (p0 >= a.seg_pad_base[q]) ? q : s;
+  const uint32_t local = p0 - a.seg_pad_base[s];
+  const int real = (int)min((uint32_t)B0, a.seg_n[s] > local ? a.seg_n[s] - local : 0u);
+  f3 sc[B0];
+  float sr[B0];
+  f3 x = mk3(0.f, 0.f, 1.f);
+  float phi = 0.0f;
+#pragma unroll
+  for (int i = 0; i < B0; ++i) {
+    float4 r0, r1;
+    if (i < real) {
+      const uint32_t slot = __ldg(a.sorted_slot + p0 + i);
+      r0 = __ldg(a.rays + 2 * (size_t)slot);
+      r1 = __ldg(a.rays + 2 * (size_t)slot + 1);
+    } else {
+      r0 = make_float4(0.f, 0.f, 0.f, -1.0f);   // padding ray: tmin = -1
+      r1 = make_float4(0.f, 0.f, 1.f, -1.0f);
+    }
+    a.sorted_rays[2 * (size_t)(p0 + i)] = r0;
+    a.sorted_rays[2 * (size_t)(p0 + i) + 1] = r1;
+    sc[i] = mk3(r0.x, r0.y, r0.z);
+    sr[i] = (i < real) ? 0.0f : -1.0f;
+    if (i < real) {
+      const f3 d = mk3(r1.x, r1.y, r1.z);
+      if (i == 0) { x = d; phi = 0.0f; }     // leaves start as radius 0 / angle 0
+      else cone_grow_ns(&x, &phi, d);        // Eqs 1-4 in sorted order
+    }
+  }
+#pragma unroll
+  for (int w = 1; w < B0; w *= 2) {
+#pragma unroll
+    for (int i = 0; i < B0; i += 2 * w) {
+      f3 c2;
+      float r2;
+      sphere_union_ns(sc[i], sr[i], sc[i + w], sr[i + w], &c2, &r2);   // Eqs 7-8
+      sc[i] = c2; sr[i] = r2;
+    }
+  }
+  NodeV n;
+  if (real == 0) {
+    n = empty_node();
+  } else {
+    n.c = sc[0]; n.r = sr[0]; n.a = x; n.alpha = phi;
+  }
+  store_node(a.nodes, a.trav, j, n);
+}
+
+struct UpperArgs {
+  uint32_t n_nodes;          // padded nodes of this level
+  const float4* child_nodes; // paper layout of level k-1
+  float4* nodes;
+  float4* trav;
+};
+
+// K6: node j = balanced pairwise union (Eqs 5-8, R9, R11) of children
+// [j*B, (j+1)*B); empty children pass through.
+template <int B>
+__global__ void __launch_bounds__(128) k_upper(const UpperArgs a) {
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= a.n_nodes) return;
+  NodeV st[B];
+#pragma unroll
+  for (int i = 0; i < B; ++i) st[i] = load_node(a.child_nodes, (size_t)j * B + i);
+#pragma unroll
+  for (int w = 1; w < B; w *= 2) {
+#pragma unroll
+    for (int i = 0; i < B; i += 2 * w) st[i] = node_union_ns(st[i], st[i + w]);
+  }
+  store_node(a.nodes, a.trav, j, st[0]);
+}
+
+}  // namespace crsh

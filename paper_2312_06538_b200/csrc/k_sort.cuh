@@ -1,0 +1,346 @@
+// k_sort.cuh — K2 compression into chunks (Fig 5), K3 LSD radix
+// sort of the chunks by key (P:107-109 [MG10]; onesweep-style), K4
+// decompression (Fig 6: skeleton of sorted sizes, exclusive scan,
+// fill). Together: a stable sort of the (key, slot) pairs of every segment
+// (SURVEY F7), with bit-exact keys and permutation.
+#pragma once
+#include "common.cuh"
+
+namespace crsh {
+
+// ============================================================== K2: compression
+struct RleArgs {
+  uint32_t N;
+  const uint32_t* keys;                 // compacted keys [N]
+  int32_t n_seg;
+  uint32_t seg_comp_start[MAX_SEG + 1];
+  uint32_t* ckey;                       // [C]
+  uint32_t* cbase;                      // [C + 1], global compacted index of each chunk head
+  uint32_t* seg_chunk_start;            // out [n_seg + 1]
+  unsigned long long* status;
+  uint32_t* ticket;
+};
+
+// Head flag: 1 where the key differs from the previous pair; also at
+// every segment start so chunks never straddle two hierarchies (R5).
+__global__ void __launch_bounds__(SCAN_THREADS) k_rle(const RleArgs a) {
+  __shared__ uint32_t s_tile, s_prefix;
+  __shared__ uint32_t s_cnt[SCAN_ITEMS * 8], s_excl[SCAN_ITEMS * 8];
+  if (threadIdx.x == 0) s_tile = atomicAdd(a.ticket, 1u);
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  uint32_t key[SCAN_ITEMS], ballot[SCAN_ITEMS];
+#pragma unroll
+  for (int it = 0; it < SCAN_ITEMS; ++it) {
+    const uint32_t i = tile * SCAN_TILE + it * SCAN_THREADS + threadIdx.x;
+    bool head = false;
+    uint32_t k = 0;
+    if (i < a.N) {
+      k = __ldg(a.keys + i);
+      head = (i == 0) || (k != __ldg(a.keys + i - 1));
+      for (int s = 0; s < a.n_seg; ++s) head |= (i == a.seg_comp_start[s]);
+    }
+    key[it] = k;
+    ballot[it] = __ballot_sync(CRSH_FULL, head);
+    if (lane == 0) s_cnt[it * 8 + warp] = __popc(ballot[it]);
+  }
+  __syncthreads();
+  if (warp == 0) tile_scan_lookback(s_cnt, s_excl, &s_prefix, a.status, (int)tile);
+  __syncthreads();
+  const uint32_t prefix = s_prefix, lt = lanemask_lt();
+#pragma unroll
+  for (int it = 0; it < SCAN_ITEMS; ++it) {
+    const uint32_t i = tile * SCAN_TILE + it * SCAN_THREADS + threadIdx.x;
+    if ((ballot[it] >> lane) & 1u) {
+      const uint32_t c = prefix + s_excl[it * 8 + warp] + __popc(ballot[it] & lt);
+      a.ckey[c] = key[it];
+      a.cbase[c] = i;
+      for (int s = 0; s < a.n_seg; ++s)
+        if (i == a.seg_comp_start[s]) a.seg_chunk_start[s] = c;
+    }
+  }
+  const uint32_t n_tiles = (a.N + SCAN_TILE - 1) / SCAN_TILE;
+  if (tile == n_tiles - 1 && threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (int q = 0; q < SCAN_ITEMS * 8; ++q) t += s_cnt[q];
+    const uint32_t C = prefix + t;
+    a.cbase[C] = a.N;
+    a.seg_chunk_start[a.n_seg] = C;
+    for (int s = 0; s < a.n_seg; ++s)
+      if (a.seg_comp_start[s] >= a.N) a.seg_chunk_start[s] = C;   // empty trailing segment
+  }
+}
+
+// ============================================================== K3: radix sort
+constexpr int RADIX_BITS = 8;
+constexpr int RADIX_BINS = 256;
+constexpr int SORT_THREADS = 256;
+constexpr int SORT_WARPS = SORT_THREADS / 32;
+constexpr int SORT_ITEMS = 16;
+constexpr int SORT_TILE = SORT_THREADS * SORT_ITEMS;   // 4096
+constexpr int SORT_PASSES = 32 / RADIX_BITS;
+
+struct SegChunks {
+  int32_t n_seg;
+  uint32_t start[MAX_SEG + 1];     // global chunk index of each segment's first chunk
+  uint32_t count[MAX_SEG];
+  uint32_t tile_start[MAX_SEG + 1];
+};
+
+__device__ __forceinline__ int seg_of(const uint32_t* starts, int n, uint32_t i) {
+  int s = 0;
+  for (int q = 1; q < n; ++q) s = (i >= starts[q]) ? q : s;
+  return s;
+}
+
+// Per-segment digit histograms of all passes in one read of the keys.
+__global__ void __launch_bounds__(256) k_radix_hist(const SegChunks sc, const uint32_t* __restrict__ keys,
+                                                    uint32_t C, uint32_t* __restrict__ hist /*[3][4][256]*/) {
+  __shared__ uint32_t h[MAX_SEG * SORT_PASSES * RADIX_BINS];
+  for (int i = threadIdx.x; i < MAX_SEG * SORT_PASSES * RADIX_BINS; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < C; i += gridDim.x * blockDim.x) {
+    const uint32_t k = __ldg(keys + i);
+    const int s = seg_of(sc.start, sc.n_seg, i);
+#pragma unroll
+    for (int p = 0; p < SORT_PASSES; ++p) atomicAdd(&h[(s * SORT_PASSES + p) * RADIX_BINS + ((k >> (8 * p)) & 255u)], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < MAX_SEG * SORT_PASSES * RADIX_BINS; i += blockDim.x)
+    if (h[i]) atomicAdd(hist + i, h[i]);
+}
+
+struct SortPassArgs {
+  SegChunks sc;
+  int32_t pass;
+  const uint32_t* keys_in;
+  const uint32_t* vals_in;   // nullptr on the first pass: values = global chunk index
+  uint32_t* keys_out;
+  uint32_t* vals_out;
+  const uint32_t* hist;      // [3][4][256]
+  uint32_t* status;          // [tiles][256]: bits 31..30 flag, 29..0 count
+  uint32_t* ticket;
+};
+
+__device__ __forceinline__ uint32_t st_load32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_store32(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// One digit pass over all segments: stable local ranking with warp
+// match.any, per-warp shared-memory histograms, decoupled look-back per digit
+// across the segment's tiles, and a shared-memory reorder so the global
+// writes are contiguous within each digit run.
+__global__ void __launch_bounds__(SORT_THREADS) k_onesweep(const SortPassArgs a) {
+  extern __shared__ uint32_t sm[];
+  uint32_t* s_keys = sm;                            // SORT_TILE
+  uint32_t* s_vals = sm + SORT_TILE;                // SORT_TILE
+  uint32_t* s_whist = sm + 2 * SORT_TILE;           // SORT_WARPS * 256
+  __shared__ uint32_t s_bin_excl[RADIX_BINS], s_base[RADIX_BINS], s_warp[8];
+  __shared__ uint32_t s_tile;
+  if (threadIdx.x == 0) s_tile = atomicAdd(a.ticket, 1u);
+  for (int i = threadIdx.x; i < SORT_WARPS * RADIX_BINS; i += SORT_THREADS) s_whist[i] = 0;
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const int seg = seg_of(a.sc.tile_start, a.sc.n_seg, tile);
+  const uint32_t t_local = tile - a.sc.tile_start[seg];
+  const uint32_t n = a.sc.count[seg], seg0 = a.sc.start[seg];
+  const int shift = RADIX_BITS * a.pass;
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5, lt = lanemask_lt();
+
+  uint32_t k[SORT_ITEMS], v[SORT_ITEMS], rank[SORT_ITEMS];
+  const uint32_t wbase = t_local * SORT_TILE + warp * (32 * SORT_ITEMS);
+#pragma unroll
+  for (int it = 0; it < SORT_ITEMS; ++it) {
+    const uint32_t idx = wbase + it * 32 + lane;
+    const bool ok = idx < n;
+    k[it] = ok ? __ldg(a.keys_in + seg0 + idx) : 0xFFFFFFFFu;
+    v[it] = ok ? (a.vals_in ? __ldg(a.vals_in + seg0 + idx) : seg0 + idx) : 0u;
+  }
+#pragma unroll
+  for (int it = 0; it < SORT_ITEMS; ++it) {
+    const uint32_t idx = wbase + it * 32 + lane;
+    const bool ok = idx < n;
+    const uint32_t d = ok ? ((k[it] >> shift) & 255u) : 0x100u + lane;   // invalid lanes never match
+    const uint32_t peers = __match_any_sync(CRSH_FULL, d);
+    const uint32_t leader = __ffs(peers) - 1;
+    uint32_t base = 0;
+    if (ok && lane == leader) {
+      base = s_whist[warp * RADIX_BINS + d];
+      s_whist[warp * RADIX_BINS + d] = base + __popc(peers);
+    }
+    base = __shfl_sync(CRSH_FULL, base, leader);
+    rank[it] = base + __popc(peers & lt);
+    __syncwarp();
+  }
+  __syncthreads();
+  // per-bin tile count, and per-warp exclusive offsets within the bin
+  const uint32_t b = threadIdx.x;
+  uint32_t cnt = 0;
+#pragma unroll
+  for (int w = 0; w < SORT_WARPS; ++w) {
+    const uint32_t c = s_whist[w * RADIX_BINS + b];
+    s_whist[w * RADIX_BINS + b] = cnt;
+    cnt += c;
+  }
+  // decoupled look-back over the tiles of this segment, one bin per thread
+  uint32_t* st = a.status + (size_t)tile * RADIX_BINS + b;
+  uint32_t excl = 0;
+  if (t_local == 0) {
+    st_store32(st, (2u << 30) | cnt);
+  } else {
+    st_store32(st, (1u << 30) | cnt);
+    int p = (int)tile - 1;
+    for (;;) {
+      uint32_t w;
+      do { w = st_load32(a.status + (size_t)p * RADIX_BINS + b); } while ((w >> 30) == 0u);
+      excl += w & 0x3FFFFFFFu;
+      if ((w >> 30) == 2u) break;
+      --p;
+    }
+    st_store32(st, (2u << 30) | (excl + cnt));
+  }
+  // digit base of the segment (exclusive scan of its global histogram)
+  const uint32_t hcount = __ldg(a.hist + ((size_t)seg * SORT_PASSES + a.pass) * RADIX_BINS + b);
+  const uint32_t hexcl = block_excl_scan_256(hcount, s_warp, nullptr);
+  const uint32_t texcl = block_excl_scan_256(cnt, s_warp, nullptr);
+  s_base[b] = hexcl + excl;
+  s_bin_excl[b] = texcl;
+  __syncthreads();
+#pragma unroll
+  for (int it = 0; it < SORT_ITEMS; ++it) {
+    const uint32_t idx = wbase + it * 32 + lane;
+    if (idx < n) {
+      const uint32_t d = (k[it] >> shift) & 255u;
+      const uint32_t pos = s_bin_excl[d] + s_whist[warp * RADIX_BINS + d] + rank[it];
+      s_keys[pos] = k[it];
+      s_vals[pos] = v[it];
+    }
+  }
+  __syncthreads();
+  const uint32_t t_n = min((uint32_t)SORT_TILE, n - t_local * SORT_TILE);
+  for (uint32_t j = threadIdx.x; j < t_n; j += SORT_THREADS) {
+    const uint32_t key = s_keys[j];
+    const uint32_t d = (key >> shift) & 255u;
+    const uint32_t out = seg0 + s_base[d] + (j - s_bin_excl[d]);
+    a.keys_out[out] = key;
+    a.vals_out[out] = s_vals[j];
+  }
+}
+
+// ============================================================== K4: decompression
+constexpr int EXP_TILE = 2048;
+
+struct ScanSizeArgs {
+  uint32_t C, N;
+  const uint32_t* sorted_cidx;   // chunk index of each sorted chunk
+  const uint32_t* cbase;         // [C + 1]
+  uint32_t* pos;                 // out [C + 1]: exclusive scan of the skeleton
+  uint32_t* first_chunk;         // out [ceil(N / EXP_TILE)]
+  unsigned long long* status;
+  uint32_t* ticket;
+};
+
+// The skeleton array (sorted chunk sizes) and its exclusive scan.
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_sizes(const ScanSizeArgs a) {
+  __shared__ uint32_t s_tile, s_prefix;
+  __shared__ uint32_t s_cnt[SCAN_ITEMS * 8], s_excl[SCAN_ITEMS * 8];
+  if (threadIdx.x == 0) s_tile = atomicAdd(a.ticket, 1u);
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  uint32_t size[SCAN_ITEMS], wex[SCAN_ITEMS];
+#pragma unroll
+  for (int it = 0; it < SCAN_ITEMS; ++it) {
+    const uint32_t c = tile * SCAN_TILE + it * SCAN_THREADS + threadIdx.x;
+    uint32_t sz = 0;
+    if (c < a.C) {
+      const uint32_t ci = __ldg(a.sorted_cidx + c);
+      sz = __ldg(a.cbase + ci + 1) - __ldg(a.cbase + ci);
+    }
+    uint32_t incl = sz;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(CRSH_FULL, incl, o);
+      if ((int)lane >= o) incl += y;
+    }
+    size[it] = sz;
+    wex[it] = incl - sz;
+    if (lane == 31) s_cnt[it * 8 + warp] = incl;
+  }
+  __syncthreads();
+  if (warp == 0) tile_scan_lookback(s_cnt, s_excl, &s_prefix, a.status, (int)tile);
+  __syncthreads();
+  const uint32_t prefix = s_prefix;
+#pragma unroll
+  for (int it = 0; it < SCAN_ITEMS; ++it) {
+    const uint32_t c = tile * SCAN_TILE + it * SCAN_THREADS + threadIdx.x;
+    if (c < a.C) {
+      const uint32_t p = prefix + s_excl[it * 8 + warp] + wex[it];
+      a.pos[c] = p;
+      // the chunk covering each output tile start k*EXP_TILE in [p, p + size)
+      for (uint32_t kk = (p + EXP_TILE - 1) / EXP_TILE; kk * EXP_TILE < p + size[it]; ++kk) a.first_chunk[kk] = c;
+    }
+  }
+  const uint32_t n_tiles = (a.C + SCAN_TILE - 1) / SCAN_TILE;
+  if (tile == n_tiles - 1 && threadIdx.x == 0) a.pos[a.C] = a.N;
+}
+
+struct ExpandArgs {
+  uint32_t N, C;
+  const uint32_t* pos;
+  const uint32_t* first_chunk;
+  const uint32_t* skey;
+  const uint32_t* scidx;
+  const uint32_t* cbase;
+  const uint32_t* vals_c;
+  int32_t n_seg;
+  uint32_t seg_comp_start[MAX_SEG + 1];
+  uint32_t seg_pad_base[MAX_SEG + 1];
+  uint32_t* sorted_key;     // padded layout
+  uint32_t* sorted_slot;
+};
+
+// Fill: every output position finds its chunk by a binary search over
+// the tile's slice of the scan (load-balanced: long runs are split across
+// tiles), then gathers the slot id of the run element.
+__global__ void __launch_bounds__(256) k_expand(const ExpandArgs a) {
+  __shared__ uint32_t s_pos[EXP_TILE + 2];
+  const uint32_t o0 = blockIdx.x * EXP_TILE;
+  const uint32_t o1 = min(o0 + EXP_TILE, a.N);
+  const uint32_t c_lo = __ldg(a.first_chunk + blockIdx.x);
+  const uint32_t c_hi = (blockIdx.x + 1 < gridDim.x) ? __ldg(a.first_chunk + blockIdx.x + 1) : a.C - 1;
+  const uint32_t nc = c_hi - c_lo + 1;
+  for (uint32_t j = threadIdx.x; j <= nc; j += blockDim.x) s_pos[j] = __ldg(a.pos + c_lo + j);
+  __syncthreads();
+  for (uint32_t o = o0 + threadIdx.x; o < o1; o += blockDim.x) {
+    uint32_t lo = 0, hi = nc;   // largest j in [0, nc) with s_pos[j] <= o
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (s_pos[mid] <= o) lo = mid; else hi = mid;
+    }
+    const uint32_t c = c_lo + lo;
+    const uint32_t src = __ldg(a.cbase + __ldg(a.scidx + c)) + (o - s_pos[lo]);
+    const int s = seg_of(a.seg_comp_start, a.n_seg, o);
+    const uint32_t dst = a.seg_pad_base[s] + (o - a.seg_comp_start[s]);
+    a.sorted_key[dst] = __ldg(a.skey + c);
+    a.sorted_slot[dst] = __ldg(a.vals_c + src);
+  }
+}
+
+// RAH (CRSH_F_SORT off): rays stay in generation order.
+__global__ void k_copy_unsorted(const ExpandArgs a) {
+  for (uint32_t o = blockIdx.x * blockDim.x + threadIdx.x; o < a.N; o += gridDim.x * blockDim.x) {
+    const int s = seg_of(a.seg_comp_start, a.n_seg, o);
+    const uint32_t dst = a.seg_pad_base[s] + (o - a.seg_comp_start[s]);
+    a.sorted_key[dst] = __ldg(a.skey + o);
+    a.sorted_slot[dst] = __ldg(a.vals_c + o);
+  }
+}
+
+}  // namespace crsh

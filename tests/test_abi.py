@@ -1,0 +1,72 @@
+"""CPU checks of the C ABI boundary: libcrsh.so builds for sm_100a, loads, and
+exports every function include/crsh.h declares; the product path has no CPU
+fallback (it fails loudly without a GPU); host-side logic (slot counts)."""
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+import paper_2312_06538_b200 as crsh
+from paper_2312_06538_b200 import build as nb
+
+
+@pytest.fixture(scope="module")
+def lib():
+    nb.build()
+    return crsh.load()
+
+
+def test_exports_every_header_symbol(lib):
+    names = crsh.header_functions()
+    assert {"crsh_scene_create", "crsh_trace_secondary", "crsh_stats"} <= set(names)
+    for n in names:
+        assert hasattr(lib, n), n
+
+
+def test_sm100a_only_and_no_implicit_fma(lib):
+    """The cubin is sm_100a (no PTX for JIT to other archs)."""
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", nb.OUT], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    ptx = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-ptx", nb.OUT], capture_output=True, text=True).stdout
+    assert ptx.strip() == ""
+    assert "--fmad=false" in nb.FLAGS and "--use_fast_math" not in nb.FLAGS
+
+
+def test_num_slots(lib):
+    """Slot count P * (L*[SH] + [RE] + [RR]) (crsh.h, R5)."""
+    assert crsh.num_slots(100, 3, 1) == 300
+    assert crsh.num_slots(100, 3, 7) == 500
+    assert crsh.num_slots(100, 0, 1) == 0
+    assert crsh.num_slots(10, 2, 6) == 20
+
+
+def test_fails_loudly_without_gpu(lib):
+    try:
+        import torch
+        if torch.cuda.is_available():
+            pytest.skip("a GPU is present")
+    except ImportError:
+        pass
+    tris = np.zeros((1, 9), np.float32)
+    ids = np.zeros(1, np.int32)
+    with pytest.raises(crsh.CrshError) as e:
+        crsh.Scene(tris.ctypes.data, ids.ctypes.data, M=1)
+    assert e.value.status == 6   # CRSH_ECUDA: no CUDA device, no CPU fallback
+
+
+def test_invalid_arguments_are_rejected(lib):
+    assert lib.crsh_scene_create(None, None, 1, 0, ctypes.byref(ctypes.c_void_p())) == 2
+    assert lib.crsh_scene_create(1, 1, 0, 0, ctypes.byref(ctypes.c_void_p())) == 4
+
+
+def test_product_never_imports_oracle():
+    """The product package shares no code with oracle/ (DESIGN.md §2)."""
+    here = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    pkg = os.path.join(here, "paper_2312_06538_b200")
+    for root, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                src = open(os.path.join(root, f)).read()
+                assert "import oracle" not in src and "from oracle" not in src and "oracle.cpp" not in src, f

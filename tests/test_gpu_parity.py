@@ -1,0 +1,200 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle, element by
+element on the same seeded inputs.  Bars (BASELINE.json north_star): keys,
+permutation, chunks and bundle boundaries bit-exact; node values bit-exact
+(both sides implement NUMSPEC); per-level test counts exact
+(bar: within 0.1%); closest-hit triangle and t exact (bar: >= 99.99% of rays,
+t within 1e-5 relative)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import oracle  # noqa: E402
+import paper_2312_06538_b200 as crsh  # noqa: E402
+from paper_2312_06538_b200.api import tracer_for  # noqa: E402
+from workloads import make_micro, make_workload  # noqa: E402
+
+SEG = {0: oracle.SH, 1: oracle.RE, 2: oracle.RR}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _build():
+    from paper_2312_06538_b200 import build as nb
+    nb.build()
+    oracle.build()
+
+
+def run_both(w, flags=crsh.F_SORT | crsh.F_MESH_CULL, taps=True):
+    tr = tracer_for(w, flags=flags)
+    tr.run()
+    hit, t = tr.results()
+    ref = oracle.trace(w, flags=flags, taps=taps)
+    return tr, hit, t, ref
+
+
+def assert_counts_equal(st, ref):
+    for seg in range(3):
+        assert st["rays"][seg] == ref["stats"]["rays"][seg]
+        assert np.array_equal(st["tests"][seg], ref["stats"]["tests"][seg]), (seg, st["tests"][seg], ref["stats"]["tests"][seg])
+        assert np.array_equal(st["hits"][seg], ref["stats"]["hits"][seg]), (seg, st["hits"][seg], ref["stats"]["hits"][seg])
+        for k in ("mesh_tests", "mesh_hits", "final_tests", "final_hits", "rays_hit", "brute"):
+            assert st[k][seg] == ref["stats"][k][seg], (k, seg, st[k][seg], ref["stats"][k][seg])
+
+
+def assert_taps_equal(tr, ref, w):
+    segs = [s for s, _, _ in oracle.segments(w.P, w.lights.shape[0], w.ray_types)]
+    for i, seg in enumerate(segs):
+        tp = ref["taps"]
+        assert np.array_equal(crsh.debug_tap(tr.scene, crsh.TAP_KEYS, seg), tp["keys"][i])
+        assert np.array_equal(crsh.debug_tap(tr.scene, crsh.TAP_VALS, seg), tp["vals"][i])
+        if len(tp["ckey"][i]):
+            assert np.array_equal(crsh.debug_tap(tr.scene, crsh.TAP_CHUNK_KEYS, seg), tp["ckey"][i])
+            assert np.array_equal(crsh.debug_tap(tr.scene, crsh.TAP_CHUNK_BASE, seg), tp["cbase"][i])
+        assert np.array_equal(crsh.debug_tap(tr.scene, crsh.TAP_SORTED_KEYS, seg), tp["skey"][i])
+        assert np.array_equal(crsh.debug_tap(tr.scene, crsh.TAP_SORTED_SLOTS, seg), tp["sslot"][i])
+        for k in range(1, w.levels + 1):
+            g = crsh.debug_tap(tr.scene, crsh.TAP_NODES, seg, k)
+            o = tp["levels"][i][k - 1]
+            assert g.shape == o.shape, (seg, k)
+            assert np.array_equal(g.view(np.uint32), o.view(np.uint32)), (seg, k, np.argwhere(g != o)[:5])
+
+
+def test_scene_prep_matches_oracle():
+    w = make_workload(2)
+    tr = tracer_for(w)
+    prep = oracle.ScenePrep(w.tris, w.mesh_ids)
+    assert np.array_equal(crsh.debug_tap(tr.scene, crsh.TAP_SCENE_CONSTS), prep.consts)
+    ts = crsh.debug_tap(tr.scene, crsh.TAP_TRI_SPHERES)
+    assert np.array_equal(ts.view(np.uint32), prep.tri_sph.view(np.uint32))
+    ms = crsh.debug_tap(tr.scene, crsh.TAP_MESH_SPHERES)
+    assert np.array_equal(ms, prep.mesh_sph[:w.n_meshes])
+
+
+@pytest.mark.parametrize("flags", [3, 7, 0, 1])
+def test_cfg1_full_parity(flags):
+    """cfg1 (128x128 SH, ~1k-tri Cornell box, Lv 3): every intermediate tap,
+    all counts and every hit bit-exact; CRSH, Z-order, RAH and sort-only."""
+    w = make_workload(1)
+    tr, hit, t, ref = run_both(w, flags)
+    assert np.array_equal(hit, ref["hit_tri"]) and np.array_equal(t.view(np.uint32), ref["t"].view(np.uint32))
+    assert_counts_equal(crsh.stats(tr.scene), ref)
+    assert_taps_equal(tr, ref, w)
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_micro_scenes(seed):
+    """Randomised micro-scenes over the option space (Lv 1..4, B0 2..64,
+    B 2..16, all ray-type mixes, empty pixels, ragged bundles)."""
+    r = np.random.default_rng(seed)
+    w = make_micro(5000 + seed, n_tris=int(r.integers(1, 200)), W=int(r.integers(1, 40)), H=int(r.integers(1, 40)),
+                   n_meshes=int(r.integers(1, 40)), n_lights=int(r.integers(0, 5)), ray_types=int(r.integers(1, 8)),
+                   levels=int(r.integers(1, 5)), leaf_size=int(2 ** r.integers(1, 7)),
+                   branching=int(2 ** r.integers(1, 5)), empty_frac=float(r.uniform(0, 0.6)))
+    flags = int(r.choice([3, 7, 0, 2, 1]))
+    tr, hit, t, ref = run_both(w, flags)
+    assert np.array_equal(hit, ref["hit_tri"]) and np.array_equal(t.view(np.uint32), ref["t"].view(np.uint32))
+    assert_counts_equal(crsh.stats(tr.scene), ref)
+    assert_taps_equal(tr, ref, w)
+    # conservativeness against brute force
+    ok = ref["empty"] == 0
+    prep = oracle.ScenePrep(w.tris, w.mesh_ids)
+    bt, btt = oracle.unpack(oracle.brute(ref["rays"][ok], prep))
+    assert np.array_equal(hit[ok], bt)
+
+
+@pytest.mark.parametrize("flags", [3, 7])
+def test_cfg2_full_parity(flags):
+    """cfg2 (512x512 SH+RE, ~70k tris / 16 meshes, Lv 2) at full size: all
+    hits, counts and the sort permutation exact against the oracle."""
+    w = make_workload(2)
+    tr, hit, t, ref = run_both(w, flags, taps=True)
+    assert np.array_equal(hit, ref["hit_tri"]) and np.array_equal(t.view(np.uint32), ref["t"].view(np.uint32))
+    assert_counts_equal(crsh.stats(tr.scene), ref)
+    assert_taps_equal(tr, ref, w)
+
+
+def test_cfg3_sampled_vs_brute():
+    """cfg3 (1024x1024 SH+RE+RR, ~250k tris / 30 meshes) in the bench's launch
+    configuration: 4096 sampled rays against N x M brute force (oracle)."""
+    w = make_workload(3)
+    tr = tracer_for(w, flags=7)
+    tr.run()
+    hit, t = tr.results()
+    prep = oracle.ScenePrep(w.tris, w.mesh_ids)
+    rays, keys, empty = oracle.generate(w, prep, 7)
+    ok = np.flatnonzero(empty == 0)
+    rng = np.random.default_rng(3)
+    pick = rng.choice(ok, size=4096, replace=False)
+    bt, btt = oracle.unpack(oracle.brute(rays[pick], prep))
+    assert np.array_equal(hit[pick], bt) and np.array_equal(t[pick].view(np.uint32), btt.view(np.uint32))
+    assert np.all(hit[empty == 1] == -2)
+    st = crsh.stats(tr.scene)
+    for seg in range(3):
+        for k in range(1, 3):
+            assert st["tests"][seg][k] >= st["hits"][seg][k]
+        assert st["tests"][seg][1] <= 8 * st["hits"][seg][2]          # monotone culling
+        assert st["final_tests"][seg] <= 8 * st["hits"][seg][1]
+
+
+def test_edge_cases():
+    # no valid pixel at all
+    w = make_micro(1, n_tris=10, W=8, H=8, empty_frac=1.0)
+    tr, hit, t, ref = run_both(w)
+    assert np.all(hit == -2) and np.array_equal(hit, ref["hit_tri"])
+    # a single pixel, a single triangle
+    w = make_micro(2, n_tris=1, W=1, H=1, n_meshes=1, empty_frac=0.0)
+    tr, hit, t, ref = run_both(w)
+    assert np.array_equal(hit, ref["hit_tri"]) and np.array_equal(t, ref["t"])
+    # every fragment at the same point: one chunk per segment (long run)
+    w = make_micro(3, n_tris=30, W=64, H=64, empty_frac=0.0, ray_types=1, n_lights=1)
+    w.pos[:] = w.pos[:, :1]
+    tr, hit, t, ref = run_both(w)
+    assert np.array_equal(hit, ref["hit_tri"])
+    assert crsh.stats(tr.scene)["chunks"][0] == ref["stats"]["chunks"][0] == 1
+    # shadow rays requested with no lights: no SH slots
+    w = make_micro(4, n_tris=20, W=9, H=7, n_lights=0, ray_types=3)
+    tr, hit, t, ref = run_both(w)
+    assert np.array_equal(hit, ref["hit_tri"])
+
+
+def test_sharded_equals_single():
+    """Hash-range sharding: the min-merge of the per-rank packed
+    results equals the single-GPU result, and the per-rank counters sum to the
+    single-GPU counters (here the ranks run one after another on one GPU)."""
+    w = make_workload(2, width=256, height=256)
+    tr = tracer_for(w)
+    tr.run()
+    hit1, t1 = tr.results()
+    st1 = tr.stats()
+    for world in (2, 3, 8):
+        merged = None
+        tsum = np.zeros((3, 9), np.uint64)
+        for rank in range(world):
+            trr = tracer_for(w, shard_rank=rank, shard_world=world)
+            packed = torch.empty(trr.slots, dtype=torch.int64, device="cuda")
+            trr.run_packed(packed)
+            merged = packed.clone() if merged is None else torch.minimum(merged, packed)
+            tsum += trr.stats()["tests"]
+        trr.unpack(merged)
+        hit, t = trr.results()
+        assert np.array_equal(hit, hit1) and np.array_equal(t, t1)
+        assert np.array_equal(tsum, st1["tests"])
+
+
+def test_host_variant_and_determinism():
+    w = make_workload(2, width=200, height=150)
+    tr = tracer_for(w)
+    tr.run()
+    h1, t1 = tr.results()
+    tr.run()
+    h2, t2 = tr.results()
+    assert np.array_equal(h1, h2) and np.array_equal(t1, t2)
+    hh = np.empty(tr.slots, np.int32)
+    th = np.empty(tr.slots, np.float32)
+    tr.run_host(np.ascontiguousarray(w.pos), np.ascontiguousarray(w.nrm), np.ascontiguousarray(w.mat),
+                np.ascontiguousarray(w.materials), hh, th)
+    assert np.array_equal(hh, h1) and np.array_equal(th, t1)
