@@ -633,7 +633,7 @@ crsh_status crsh_scene_create(const float* tris, const int32_t* mesh_ids, int64_
   cudaDeviceProp prop;
   if (cudaGetDeviceProperties(&prop, device) == cudaSuccess) sc->sm_count = prop.multiProcessorCount;
   for (int k = 0; k < 3; ++k) { sc->box_min[k] = INFINITY; sc->box_max[k] = -INFINITY; }
-  for (int64_t i = 0; i < 3 * M; ++i) {
+  for (int64_t i = 0; i < 9 * M; ++i) {   // every vertex coordinate
     const int k = (int)(i % 3);
     sc->box_min[k] = std::min(sc->box_min[k], ht[i]);
     sc->box_max[k] = std::max(sc->box_max[k], ht[i]);

@@ -96,12 +96,14 @@ def test_micro_scenes(seed):
                    branching=int(2 ** r.integers(1, 5)), empty_frac=float(r.uniform(0, 0.6)))
     flags = int(r.choice([3, 7, 0, 2, 1]))
     tr, hit, t, ref = run_both(w, flags)
+    prep = oracle.ScenePrep(w.tris, w.mesh_ids)
+    assert np.array_equal(crsh.debug_tap(tr.scene, crsh.TAP_SCENE_CONSTS), prep.consts)
+    assert np.array_equal(crsh.debug_tap(tr.scene, crsh.TAP_MESH_SPHERES), prep.mesh_sph[:w.n_meshes])
     assert np.array_equal(hit, ref["hit_tri"]) and np.array_equal(t.view(np.uint32), ref["t"].view(np.uint32))
     assert_counts_equal(crsh.stats(tr.scene), ref)
     assert_taps_equal(tr, ref, w)
     # conservativeness against brute force
     ok = ref["empty"] == 0
-    prep = oracle.ScenePrep(w.tris, w.mesh_ids)
     bt, btt = oracle.unpack(oracle.brute(ref["rays"][ok], prep))
     assert np.array_equal(hit[ok], bt)
 
