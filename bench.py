@@ -1,0 +1,332 @@
+#!/usr/bin/env python
+"""bench.py -- secondary Mrays/s of the CRSH path (BASELINE.json metric).
+
+One step = one frame of the whole hot path through the C
+ABI call crsh_trace_secondary: generate + hash + trim, compress, radix sort,
+decompress, build, mesh cull, traversal, final tests, per-slot output (plus,
+at N > 1, the NCCL min-merge of the per-rank packed results).
+
+Default workload: BASELINE.json configs[1] ("512x512 shadow+reflection rays,
+~70k-triangle multi-mesh procedural scene, 1 B200"), seeded synthetic scene +
+rasterised G-buffer (workloads/).  Timing: W untimed warm-up frames, then K
+frames, each bracketed by CUDA events on the launching stream after an L2
+flush (a 512 MiB write outside the bracket); barrier + synchronize on both
+sides; max over ranks.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl crsh|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...    (hash-range sharding)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "secondary Mrays/s at 1/2/4/8 B200; ray-primitive tests/ray vs naive N×M"
+EQ9_FLOPS = 24      # Eq 9 test as evaluated: 3 sub, dot(5), 3 fma(6), dot(5), add, mul+fma(3), mul
+MT_FLOPS = 46       # Moller-Trumbore as evaluated, reciprocal counted once
+SM_COUNT, FP32_LANES, FMA_FLOPS = 148, 128, 2
+
+
+def env_rank():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+# ----------------------------------------------------------------------------- clocks
+REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+           0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+           0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+
+class ClockSampler:
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 3:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+                bits = int(parts[2], 16)
+            except ValueError:
+                continue
+            for b, name in REASONS.items():
+                if bits & b and name != "gpu_idle":
+                    reasons.add(name)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- helpers
+def frame_flops(st):
+    tests = int(np.asarray(st["tests"]).sum()) + int(sum(st["mesh_tests"]))
+    return tests * EQ9_FLOPS + int(sum(st["final_tests"])) * MT_FLOPS
+
+
+def trav_flops(st):
+    return int(np.asarray(st["tests"]).sum()) * EQ9_FLOPS + int(sum(st["final_tests"])) * MT_FLOPS
+
+
+def load_traffic(kernel="k_traverse"):
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        d = json.load(open(p))
+        return d.get("kernels", {}).get(kernel, {}).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        return {}
+
+
+def oracle_sample(w, flags, target_s=12.0, max_rows=None):
+    """Time the oracle (as it stands) on a band of image rows sized to about
+    target_s seconds of host CPU work; returns (rays, seconds, rows, cores)."""
+    import oracle
+    from workloads.scenes import Workload
+    prep = oracle.ScenePrep(w.tris, w.mesh_ids)
+    rows = max(1, w.height // 64)
+    while True:
+        r0 = (w.height - rows) // 2
+        P = w.width
+        sub = Workload(w.name, w.tris, w.mesh_ids, w.tri_mat, w.materials, w.lights, w.eye, w.width, rows,
+                       np.ascontiguousarray(w.pos.reshape(3, w.height, P)[:, r0:r0 + rows].reshape(3, -1)),
+                       np.ascontiguousarray(w.nrm.reshape(3, w.height, P)[:, r0:r0 + rows].reshape(3, -1)),
+                       np.ascontiguousarray(w.mat.reshape(w.height, P)[r0:r0 + rows].reshape(-1)), w.ray_types,
+                       w.levels, w.leaf_size, w.branching)
+        t0 = time.perf_counter()
+        out = oracle.trace(sub, prep, flags=flags)
+        dt = time.perf_counter() - t0
+        rays = int(sum(out["stats"]["rays"]))
+        if dt >= target_s / 4 or rows >= w.height or (max_rows and rows >= max_rows):
+            return rays, dt, rows, oracle.default_threads()
+        rows = min(w.height, max(rows + 1, int(rows * min(8.0, target_s / max(dt, 1e-3)))))
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def run_crsh(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2312_06538_b200 as crsh
+    from paper_2312_06538_b200.api import tracer_for
+    from workloads import make_workload
+
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    flags = crsh.F_SORT | crsh.F_MESH_CULL | (crsh.F_ZORDER if args.zorder else 0)
+    w = make_workload(args.config)
+    tr = tracer_for(w, device=local, flags=flags | crsh.F_STAGE_TIMING, shard_rank=rank, shard_world=world)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+    packed = torch.empty(max(tr.slots, 1), dtype=torch.int64, device="cuda") if world > 1 else None
+
+    def step():
+        if world == 1:
+            tr.run(stream)
+        else:
+            tr.run_packed(packed, stream)
+            dist.all_reduce(packed, op=dist.ReduceOp.MIN)   # per-slot min-merge over NVLink
+            tr.unpack(packed, stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    st0 = tr.stats()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    stage = np.zeros(8)
+    launches = 0
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+            st = tr.stats()          # synchronises; outside the event bracket
+            stage += np.asarray(st["stage_ms"])
+            launches += tr.launches() + (1 if world > 1 else 0)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ms = np.array([a.elapsed_time(b) for a, b in ev])
+    total_ms = float(ms.sum())
+    trav_ms = stage[6] / args.steps
+    st = tr.stats()
+    # counters: traversal counters are per rank (sum); ray counts are global
+    vec = torch.tensor([total_ms, trav_ms], dtype=torch.float64, device="cuda")
+    cnt = torch.tensor([int(np.asarray(st["tests"]).sum()), int(sum(st["final_tests"])), int(sum(st["mesh_tests"]))],
+                       dtype=torch.int64, device="cuda")
+    if world > 1:
+        dist.all_reduce(vec, op=dist.ReduceOp.MAX)
+        dist.all_reduce(cnt, op=dist.ReduceOp.SUM)
+    total_ms, trav_ms_max = float(vec[0]), float(vec[1])
+    tests_all, final_all, mesh_all = (int(x) for x in cnt.tolist())
+    rays = int(sum(st["rays"]))
+    mrays = rays * args.steps / (total_ms * 1e-3) / 1e6
+    # end to end through the public API with HOST buffers (crsh_trace_secondary_host), N = 1 path
+    e2e = None
+    if world == 1:
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+        hpos, hnrm, hmat, hmats = pin(w.pos), pin(w.nrm), pin(w.mat), pin(w.materials)
+        hh = torch.empty(tr.slots, dtype=torch.int32).pin_memory()
+        ht = torch.empty(tr.slots, dtype=torch.float32).pin_memory()
+        for _ in range(2):
+            tr.run_host(hpos.numpy(), hnrm.numpy(), hmat.numpy(), hmats.numpy(), hh.numpy(), ht.numpy(), stream)
+        e_ms = []
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            tr.run_host(hpos.numpy(), hnrm.numpy(), hmat.numpy(), hmats.numpy(), hh.numpy(), ht.numpy(), stream)
+            b.record(stream)
+            torch.cuda.synchronize()
+            e_ms.append(a.elapsed_time(b))
+        P = w.width * w.height
+        e2e = {"value": round(rays * len(e_ms) / (sum(e_ms) * 1e-3) / 1e6, 3), "unit": "Mrays/s",
+               "h2d_bytes_per_step": 28 * P + 12 * int(w.materials.shape[0]), "d2h_bytes_per_step": 8 * tr.slots,
+               "api": "crsh_trace_secondary_host"}
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    peaks = measured_peaks()
+    clocks = clk.summary()
+    sm_max = (clocks or {}).get("sm_max_mhz") or peaks.get("sm_max_mhz", 1965.0)
+    peak_tflops = SM_COUNT * FP32_LANES * FMA_FLOPS * sm_max * 1e6 / 1e12
+    tflops = trav_flops(st) / (trav_ms * 1e-3) / 1e12 if trav_ms > 0 else 0.0
+    traffic = load_traffic()
+    brute = rays * tr.M
+    stage_names = ["generate+trim", "compress", "sort", "decompress", "build", "mesh-cull+plan", "traverse+final",
+                   "output"]
+    out = {
+        "metric": METRIC, "value": round(mrays, 3), "unit": "Mrays/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded procedural scene + rasterised G-buffer, workloads/)",
+        "config": {"workload": w.name, "pixels": w.width * w.height, "triangles": tr.M, "meshes": int(w.n_meshes),
+                   "ray_types": w.ray_types, "lights": int(w.lights.shape[0]), "levels": w.levels,
+                   "leaf_size": w.leaf_size, "branching": w.branching, "hash": "zorder" if args.zorder else "R6 (SPEC layout)",
+                   "parallelism": f"hash-range shard x{world}" if world > 1 else "single GPU",
+                   "l2": "flushed before every timed step (512 MiB write outside the event bracket)"},
+        "rays_per_step": rays,
+        "tests_per_ray": round((tests_all + final_all) / max(rays, 1), 2),
+        "naive_tests_per_ray": tr.M,
+        "relative_pct_of_brute": round(100.0 * (tests_all + final_all) / max(brute, 1), 4),
+        "stage_ms": {n: round(v / args.steps, 4) for n, v in zip(stage_names, stage)},
+        "roofline": {"bound": "alu", "kernel": "k_traverse", "achieved": round(tflops, 3), "peak": round(peak_tflops, 2),
+                     "unit": "TFLOP/s", "frac": round(tflops / peak_tflops, 4), "traffic": traffic,
+                     "note": f"FP32: {EQ9_FLOPS} flops per Eq 9 test, {MT_FLOPS} per MT test; peak = 148 SM x 128 "
+                             f"FP32 lanes x 2 x {sm_max:.0f} MHz; kernel time from CUDA events around k_traverse"},
+        "gpu_launches": launches,
+        "e2e": e2e,
+        "clocks": clocks,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        cr, cs, rows, cores = oracle_sample(w, flags & 7)
+        out["cpu_baseline"] = {"value": round(cr / cs / 1e6, 5), "unit": "Mrays/s", "cores": cores, "kind": "oracle",
+                               "sample": f"{rows} of {w.height} image rows (centre band), {cr} rays, {cs:.1f} s"}
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ----------------------------------------------------------------------------- reference arm (the oracle)
+def run_reference(args):
+    rank, world, local = env_rank()
+    if rank != 0:
+        return
+    import oracle
+    from workloads import make_workload
+    oracle.build()
+    w = make_workload(args.config)
+    flags = 3 | (4 if args.zorder else 0)
+    budget = 150.0 / max(1, args.steps + args.warmup)      # whole run within a few minutes
+    rows_probe = oracle_sample(w, flags, target_s=min(budget, 8.0))[2]
+    times, rays = [], 0
+    for i in range(args.warmup + args.steps):
+        r, dt, rows, cores = oracle_sample(w, flags, target_s=0.0, max_rows=rows_probe)
+        if i >= args.warmup:
+            times.append(dt)
+            rays += r
+    v = rays / sum(times) / 1e6
+    out = {"metric": METRIC, "value": round(v, 5), "unit": "Mrays/s", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": round(1e3 * sum(times) / len(times), 2), "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
+           "config": {"workload": w.name},
+           "cpu_baseline": {"value": round(v, 5), "unit": "Mrays/s", "cores": oracle.default_threads(),
+                            "kind": "oracle", "sample": f"{rows_probe} of {w.height} image rows per step"},
+           "e2e": {"value": round(v, 5), "unit": "Mrays/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--impl", default="crsh", choices=["crsh", "reference"])
+    ap.add_argument("--zorder", action="store_true", help="Z-order hash layout (SURVEY §8(f) NEXT-4)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_crsh(args)
+
+
+if __name__ == "__main__":
+    main()
