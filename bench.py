@@ -261,6 +261,9 @@ def run_crsh(args):
                    "l2": "flushed before every timed step (512 MiB write outside the event bracket)"},
         "rays_per_step": rays,
         "tests_per_ray": round((tests_all + final_all) / max(rays, 1), 2),
+        "tests_by_level": {f"L{k}": int(np.asarray(st["tests"])[:, k].sum()) for k in range(w.levels, 0, -1)},
+        "hits_by_level": {f"L{k}": int(np.asarray(st["hits"])[:, k].sum()) for k in range(w.levels, 0, -1)},
+        "final_tests": final_all, "mesh_tests": mesh_all,
         "naive_tests_per_ray": tr.M,
         "relative_pct_of_brute": round(100.0 * (tests_all + final_all) / max(brute, 1), 4),
         "stage_ms": {n: round(v / args.steps, 4) for n, v in zip(stage_names, stage)},

@@ -546,9 +546,7 @@ crsh_status trace_impl(crsh_scene* sc, const crsh_primary_hits* h, const float* 
 
     TravArgs t{};
     t.Lv = Lv; t.B0 = B0; t.B = B; t.K = fi.K; t.group_rays = fi.GR;
-    t.tile = std::min(512, std::max(32, 4096 / fi.K));
-    t.qcap = Lv <= 3 ? 2048 : (Lv <= 5 ? 1024 : 512);
-    t.qtop_cap = fi.K * t.tile;
+    t.logB0 = __builtin_ctz((unsigned)B0); t.logB = __builtin_ctz((unsigned)B);
     uint64_t per = 1;
     for (int k = Lv; k >= 1; --k) { t.per_group[k] = (uint32_t)(fi.K * per); per *= B; }
     for (int k = 1; k <= Lv; ++k) t.trav[k] = trav + 3 * fi.level_off[k];
@@ -558,8 +556,8 @@ crsh_status trace_impl(crsh_scene* sc, const crsh_primary_hits* h, const float* 
     t.items = sc->items.as<uint4>(); t.n_items = d_small + 8; t.ticket = tickets + T_TRAV;
     t.best = sc->best.as<unsigned long long>(); t.counters = counters; t.n_seg = fi.n_seg;
     for (int s = 0; s <= fi.n_seg; ++s) t.seg_group_start[s] = seg_group_start[s];
-    const bool smem_best = fi.GR <= 512;
-    const TravSmem L = TravSmem::make(fi.K, sc->n_meshes, t.tile, Lv, t.qcap, smem_best);
+    const bool small = fi.GR <= SMALL_GROUP_RAYS;
+    const TravSmem L = TravSmem::make(fi.K, B, sc->n_meshes, Lv, small, t.per_group, fi.GR);
     auto launch = [&](auto kern) -> cudaError_t {
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
       if (e != cudaSuccess) return e;
@@ -570,7 +568,8 @@ crsh_status trace_impl(crsh_scene* sc, const crsh_primary_hits* h, const float* 
       kern<<<per_sm * sc->sm_count, TRAV_THREADS, L.total, st>>>(t, L);
       return cudaGetLastError();
     };
-    CK(smem_best ? launch(k_traverse<true>) : launch(k_traverse<false>));
+    if (B == 8) CK(small ? launch(k_traverse<true, 8>) : launch(k_traverse<false, 8>));
+    else CK(small ? launch(k_traverse<true, 0>) : launch(k_traverse<false, 0>));
     ++sc->launches;
   } else {
     CK(mark(6));

@@ -169,16 +169,27 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_plan(const PlanArgs a) {
 }
 
 // ============================================================== K8
+// Warp-synchronous traversal. Each warp streams 32-triangle slices of the
+// item's virtual triangle range; lane i owns triangle i of the slice.
+//  * top level: K top nodes x 32 triangles (Eq 9), node data broadcast from
+//    shared memory;
+//  * level Lv-1: every (top node j, triangle) that passed is tested at once
+//    against the B children of j (all lanes iterate the same j and child, so
+//    the node reads are broadcasts; B = 8 is fully unrolled);
+//  * child survivors go to the warp's queue; deeper levels (Lv >= 3) are
+//    expanded by 32-lane steps, and each 32-lane step of the bundle level runs
+//    Moller-Trumbore for B0 rays of 32/B0 (bundle, triangle) entries. A step
+//    is taken from the LOWEST level that has a full step, so the queues stay
+//    bounded and persist across slices; the rest is drained at the item end.
+// No block barrier is executed inside the hot loop.
 constexpr int TRAV_THREADS = 256;
-constexpr int TRI_BITS = 9;           // tile-local triangle index bits in queue entries
-constexpr int MAX_TILE = 1 << TRI_BITS;
+constexpr int TRAV_WARPS = TRAV_THREADS / 32;
+constexpr uint32_t SMALL_GROUP_RAYS = 512;   // groups up to this size live in shared memory
+constexpr int LOWQ = 64;                     // capacity of a warp queue below level Lv-1
 
 struct TravArgs {
-  int32_t Lv, B0, B, K;
+  int32_t Lv, B0, B, K, logB0, logB;
   uint32_t group_rays;
-  int32_t tile;                       // triangles per tile (<= 512)
-  int32_t qcap;                       // capacity of the lower-level queues
-  int32_t qtop_cap;                   // K * tile
   const float4* trav[MAX_LEVELS + 1]; // level k (1..Lv), traversal layout
   uint32_t per_group[MAX_LEVELS + 1]; // nodes per group at level k
   const float4* sorted_rays;
@@ -199,67 +210,83 @@ struct TravArgs {
 
 // dynamic shared-memory layout (bytes), shared by host and device
 struct TravSmem {
-  uint32_t off_top, off_act_mesh, off_act_nmask, off_act_prefix, off_act_first, off_tri_sph, off_tri_id,
-      off_tri_nmask, off_q[MAX_LEVELS + 1], off_best, total;
-  __host__ __device__ static TravSmem make(int K, int n_meshes, int tile, int Lv, int qcap, bool smem_best) {
+  uint32_t off_top, off_act_nmask, off_act_prefix, off_act_first, off_q, off_best, off_nodes, off_rays,
+      node_off[MAX_LEVELS + 1], q_off[MAX_LEVELS + 1], q_warp, total;
+  __host__ __device__ static TravSmem make(int K, int B, int n_meshes, int Lv, bool small, const uint32_t* per_group,
+                                           uint32_t group_rays) {
     TravSmem s;
     uint32_t o = 0;
     auto take = [&](uint32_t bytes) { const uint32_t r = o; o += (bytes + 15u) & ~15u; return r; };
     s.off_top = take(K * 48u);
-    s.off_act_mesh = take(4u * n_meshes);
     s.off_act_nmask = take(4u * n_meshes);
     s.off_act_prefix = take(4u * (n_meshes + 1));
     s.off_act_first = take(4u * n_meshes);
-    s.off_tri_sph = take(16u * tile);
-    s.off_tri_id = take(4u * tile);
-    s.off_tri_nmask = take(4u * tile);
-    for (int k = 0; k <= MAX_LEVELS; ++k) s.off_q[k] = 0;
-    for (int k = 1; k <= Lv; ++k) s.off_q[k] = take(4u * (k == Lv ? (uint32_t)(K * tile) : (uint32_t)qcap));
-    s.off_best = smem_best ? take(8u * 512u) : 0u;
+    // per-warp queues of uint2 (node_local, triangle): Lv == 1: the top (=
+    // bundle) level holds one slice (32 K) plus a partial step; Lv >= 2:
+    // level Lv-1 receives the dense child tests of one top node (32 B) plus
+    // a partial step; deeper levels LOWQ (they receive <= 32 per step)
+    uint32_t qw = 0;
+    for (int k = 0; k <= MAX_LEVELS; ++k) { s.q_off[k] = 0; s.node_off[k] = 0; }
+    for (int k = 1; k <= Lv; ++k) {
+      s.q_off[k] = qw;
+      if (Lv == 1) qw += 32u * K + 32u;
+      else if (k == Lv - 1) qw += 32u * B + 32u;
+      else if (k < Lv - 1) qw += (uint32_t)LOWQ;
+    }
+    s.q_warp = qw;
+    s.off_q = take(8u * qw * TRAV_WARPS);
+    s.off_best = s.off_nodes = s.off_rays = 0;
+    if (small) {
+      uint32_t n4 = 0;   // float4 slots of the group's nodes below the top level
+      for (int k = 1; k < Lv; ++k) { s.node_off[k] = n4; n4 += 3u * per_group[k]; }
+      s.off_nodes = take(16u * (n4 ? n4 : 1u));
+      s.off_rays = take(32u * group_rays);
+      s.off_best = take(8u * group_rays);
+    }
     s.total = o;
     return s;
   }
 };
 
-// warp-aggregated append of `val` where pred; every lane of the warp calls.
-__device__ __forceinline__ void push_warp(bool pred, uint32_t val, uint32_t* q, uint32_t* qlen) {
-  const uint32_t b = __ballot_sync(CRSH_FULL, pred);
-  if (b == 0u) return;
-  const uint32_t lane = lane_id();
-  const int leader = __ffs(b) - 1;
-  uint32_t base = 0;
-  if ((int)lane == leader) base = atomicAdd(qlen, (uint32_t)__popc(b));
-  base = __shfl_sync(CRSH_FULL, base, leader);
-  if (pred) q[base + __popc(b & lanemask_lt())] = val;
-}
-
-__device__ __forceinline__ void warp_count(unsigned long long* dst, uint32_t v) {
-  const uint32_t s = __reduce_add_sync(CRSH_FULL, v);
-  if (lane_id() == 0 && s) atomicAdd(dst, (unsigned long long)s);
-}
-
-template <bool SMEM_BEST>
+// BT: compile-time branching factor (0 = runtime a.B)
+template <bool SMALL, int BT>
 __global__ void __launch_bounds__(TRAV_THREADS) k_traverse(const TravArgs a, const TravSmem L) {
   extern __shared__ __align__(16) unsigned char smraw[];
   float4* s_top = reinterpret_cast<float4*>(smraw + L.off_top);
-  uint32_t* s_act_mesh = reinterpret_cast<uint32_t*>(smraw + L.off_act_mesh);
   uint32_t* s_act_nmask = reinterpret_cast<uint32_t*>(smraw + L.off_act_nmask);
   uint32_t* s_act_prefix = reinterpret_cast<uint32_t*>(smraw + L.off_act_prefix);
   uint32_t* s_act_first = reinterpret_cast<uint32_t*>(smraw + L.off_act_first);
-  float4* s_tri_sph = reinterpret_cast<float4*>(smraw + L.off_tri_sph);
-  uint32_t* s_tri_id = reinterpret_cast<uint32_t*>(smraw + L.off_tri_id);
-  uint32_t* s_tri_nmask = reinterpret_cast<uint32_t*>(smraw + L.off_tri_nmask);
   unsigned long long* s_best = reinterpret_cast<unsigned long long*>(smraw + L.off_best);
-  __shared__ uint32_t s_qlen[MAX_LEVELS + 1];
+  const float4* s_nodes = reinterpret_cast<const float4*>(smraw + L.off_nodes);
+  const float4* s_rays = reinterpret_cast<const float4*>(smraw + L.off_rays);
   __shared__ uint32_t s_item, s_cur_g, s_n_act, s_carry, s_carry_c;
   __shared__ uint32_t s_warp[8];
   __shared__ unsigned long long s_ctr[MAX_SEG * CTR_STRIDE];
+  __shared__ uint32_t s_qlen[TRAV_WARPS][MAX_LEVELS + 1];
+  // per-level tables copied out of the kernel parameters: a runtime index into
+  // a parameter array compiles to a select chain, into shared memory to one LDS
+  __shared__ uint32_t s_qoff[MAX_LEVELS + 1], s_noff[MAX_LEVELS + 1], s_pg[MAX_LEVELS + 1];
+  __shared__ const float4* s_trav[MAX_LEVELS + 1];
+  if (threadIdx.x <= MAX_LEVELS) {
+    s_qoff[threadIdx.x] = L.q_off[threadIdx.x];
+    s_noff[threadIdx.x] = L.node_off[threadIdx.x];
+    s_pg[threadIdx.x] = a.per_group[threadIdx.x];
+    s_trav[threadIdx.x] = a.trav[threadIdx.x];
+  }
 
-  const int Lv = a.Lv, B = a.B, B0 = a.B0, K = a.K;
-  const uint32_t tid = threadIdx.x, lane = lane_id();
+  const int Lv = a.Lv, K = a.K, logB0 = a.logB0;
+  const int B = BT ? BT : a.B;
+  const int logB = BT ? __builtin_ctz(BT) : a.logB;
+  const uint32_t Bm = (uint32_t)B - 1u, B0m = (uint32_t)a.B0 - 1u;
+  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+  const uint32_t lt = lanemask_lt();
+  uint2* q = reinterpret_cast<uint2*>(smraw + L.off_q) + warp * L.q_warp;
+  uint32_t* qlen = s_qlen[warp];
+  const uint32_t step_exp = (32u >> logB) ? (32u >> logB) : 1u;   // entries per expansion step
+  const uint32_t step_mt = (32u >> logB0) ? (32u >> logB0) : 1u;  // entries per final-test step
   for (uint32_t i = tid; i < MAX_SEG * CTR_STRIDE; i += TRAV_THREADS) s_ctr[i] = 0ull;
+  if (lane <= MAX_LEVELS) qlen[lane] = 0u;
   if (tid == 0) s_cur_g = 0xFFFFFFFFu;
-  if (tid <= MAX_LEVELS) s_qlen[tid] = 0u;
   const uint32_t n_items = *a.n_items;
 
   for (;;) {
@@ -271,11 +298,22 @@ __global__ void __launch_bounds__(TRAV_THREADS) k_traverse(const TravArgs a, con
     const uint4 item = __ldg(a.items + it);
     const uint32_t g = item.x;
     int seg = 0;
-    for (int q = 1; q < a.n_seg; ++q) seg = (g >= a.seg_group_start[q]) ? q : seg;
+    for (int qq = 1; qq < a.n_seg; ++qq) seg = (g >= a.seg_group_start[qq]) ? qq : seg;
     unsigned long long* ctr = s_ctr + seg * CTR_STRIDE;
 
-    if (g != s_cur_g) {   // uniform: group setup (top nodes, surviving meshes)
-      for (int j = tid; j < 3 * K; j += TRAV_THREADS) s_top[j] = __ldg(a.trav[Lv] + (size_t)g * K * 3 + j);
+    if (g != s_cur_g) {   // uniform: group setup (top nodes, surviving meshes, group data)
+      for (int j = tid; j < 3 * K; j += TRAV_THREADS) s_top[j] = __ldg(s_trav[Lv] + (size_t)g * K * 3 + j);
+      if (SMALL) {
+        float4* sn = reinterpret_cast<float4*>(smraw + L.off_nodes);
+        for (int k = 1; k < Lv; ++k) {
+          const uint32_t n4 = 3u * s_pg[k];
+          const float4* src = s_trav[k] + (size_t)g * n4;
+          for (uint32_t j = tid; j < n4; j += TRAV_THREADS) sn[s_noff[k] + j] = __ldg(src + j);
+        }
+        float4* sr = reinterpret_cast<float4*>(smraw + L.off_rays);
+        const float4* rs = a.sorted_rays + 2 * (size_t)g * a.group_rays;
+        for (uint32_t j = tid; j < 2 * a.group_rays; j += TRAV_THREADS) sr[j] = __ldg(rs + j);
+      }
       if (tid == 0) { s_carry = 0u; s_carry_c = 0u; }
       __syncthreads();
       // compact the meshes any of the K nodes kept, in mesh order, with the
@@ -295,7 +333,6 @@ __global__ void __launch_bounds__(TRAV_THREADS) k_traverse(const TravArgs a, con
         const uint32_t ec = block_excl_scan_256(cnt, s_warp, &tot_c);
         const uint32_t base_a = s_carry, base_c = s_carry_c;
         if (act) {
-          s_act_mesh[base_a + ea] = (uint32_t)m;
           s_act_nmask[base_a + ea] = nm;
           s_act_prefix[base_a + ea] = base_c + ec;
           s_act_first[base_a + ea] = __ldg(a.mesh_first + m);
@@ -306,137 +343,171 @@ __global__ void __launch_bounds__(TRAV_THREADS) k_traverse(const TravArgs a, con
       }
       if (tid == 0) s_act_prefix[s_carry] = s_carry_c;
       if (tid == 0) { s_n_act = s_carry; s_cur_g = g; }
-      __syncthreads();
     }
-    const uint32_t n_act = s_n_act;
-    if (SMEM_BEST) {
+    if (SMALL) {
       for (uint32_t r = tid; r < a.group_rays; r += TRAV_THREADS) s_best[r] = BEST_NONE;
     }
     __syncthreads();
+    const uint32_t n_act = s_n_act;
+    const size_t rbase = (size_t)g * a.group_rays;
+    uint32_t c_top_t = 0, c_top_h = 0, c_ch_t = 0, c_ch_h = 0, c_mt_t = 0, c_mt_h = 0;   // item counters
 
-    for (uint32_t tb = item.y; tb < item.z; tb += a.tile) {
-      const uint32_t n_t = min((uint32_t)a.tile, item.z - tb);
-      // ---- stage the tile's triangle spheres (contiguous per mesh, coalesced)
-      for (uint32_t i = tid; i < (uint32_t)a.tile; i += TRAV_THREADS) {
-        uint32_t nm = 0;
-        if (i < n_t) {
-          const uint32_t v = tb + i;
-          uint32_t lo = 0, hi = n_act;   // largest q with prefix[q] <= v
-          while (hi - lo > 1) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if (s_act_prefix[mid] <= v) lo = mid; else hi = mid;
-          }
-          const uint32_t tri = s_act_first[lo] + (v - s_act_prefix[lo]);
-          s_tri_sph[i] = __ldg(a.tri_sph + tri);
-          s_tri_id[i] = tri;
-          nm = s_act_nmask[lo];
+    // final tests: one 32-lane step of Moller-Trumbore, B0 rays of up
+    // to step_mt (bundle, triangle) entries taken from the end of Q[1]
+    auto step_mt_fn = [&]() {
+      const uint32_t qk = qlen[1];
+      const uint32_t n = min(qk, step_mt);
+      const uint2* qin = q + s_qoff[1] + (qk - n);
+      const uint32_t n_work = n << logB0;
+      for (uint32_t w = lane; w < n_work; w += 32) {
+        const uint2 e = qin[w >> logB0];
+        const uint32_t rl = (e.x << logB0) | (w & B0m);
+        const float4 r0 = SMALL ? s_rays[2 * rl] : __ldg(a.sorted_rays + 2 * (rbase + rl));
+        if (r0.w < 0.0f) continue;   // padding ray
+        const float4 r1 = SMALL ? s_rays[2 * rl + 1] : __ldg(a.sorted_rays + 2 * (rbase + rl) + 1);
+        const float4* te = a.tri_e + 3 * (size_t)e.y;
+        const float4 v0 = __ldg(te), e1 = __ldg(te + 1), e2 = __ldg(te + 2);
+        ++c_mt_t;
+        float th;
+        if (mt_ns(mk3(r0.x, r0.y, r0.z), mk3(r1.x, r1.y, r1.z), r0.w, r1.w, mk3(v0.x, v0.y, v0.z),
+                  mk3(e1.x, e1.y, e1.z), mk3(e2.x, e2.y, e2.z), &th)) {
+          ++c_mt_h;
+          const unsigned long long pk = pack_hit(th, e.y);
+          if (SMALL) atomicMin(s_best + rl, pk);
+          else atomicMin(a.best + rbase + rl, pk);
         }
-        s_tri_nmask[i] = nm;
       }
-      __syncthreads();
-      // ---- top level: dense (top node x triangle) Eq 9 tests
-      {
-        uint32_t* q = reinterpret_cast<uint32_t*>(smraw + L.off_q[Lv]);
-        uint32_t tests = 0, hits = 0;
-        for (uint32_t i0 = 0; i0 < (uint32_t)a.tile; i0 += TRAV_THREADS) {
-          const uint32_t i = i0 + tid;
-          const bool in = i < n_t;
-          const float4 tgt = in ? s_tri_sph[i] : make_float4(0.f, 0.f, 0.f, 0.f);
-          const uint32_t nm = in ? s_tri_nmask[i] : 0u;
-          for (int j = 0; j < K; ++j) {
-            const bool need = (nm >> j) & 1u;
-            bool pass = false;
-            if (need) {
-              const float4 n0 = s_top[3 * j], n1 = s_top[3 * j + 1], n2 = s_top[3 * j + 2];
-              pass = cull_ns(mk3(n0.x, n0.y, n0.z), n0.w, mk3(n1.x, n1.y, n1.z), n1.w, n2.x, tgt);
-              ++tests;
-              hits += pass;
-            }
-            push_warp(pass, ((uint32_t)j << TRI_BITS) | i, q, &s_qlen[Lv]);
-          }
+      __syncwarp();
+      if (lane == 0) qlen[1] = qk - n;
+      __syncwarp();
+    };
+    // expansion step at level k >= 2 (only when Lv >= 3 reaches below Lv-1)
+    auto step_exp_fn = [&](int k) {
+      const uint32_t qk = qlen[k];
+      const uint32_t n = min(qk, step_exp);
+      const uint2* qin = q + s_qoff[k] + (qk - n);
+      const uint32_t e_i = lane >> logB;
+      bool test = false, pass = false;
+      uint2 out = make_uint2(0u, 0u);
+      if (e_i < n) {
+        const uint2 e = qin[e_i];
+        const uint32_t child = (e.x << logB) | (lane & Bm);
+        const float4* nd = SMALL ? s_nodes + s_noff[k - 1] + 3 * child
+                                 : s_trav[k - 1] + 3 * ((size_t)g * s_pg[k - 1] + child);
+        const float4 c0 = SMALL ? nd[0] : __ldg(nd);
+        if (c0.w >= 0.0f) {   // existing child
+          const float4 c1 = SMALL ? nd[1] : __ldg(nd + 1);
+          const float c2 = SMALL ? nd[2].x : __ldg(&nd[2].x);
+          test = true;
+          pass = cull_ns(mk3(c0.x, c0.y, c0.z), c0.w, mk3(c1.x, c1.y, c1.z), c1.w, c2, __ldg(a.tri_sph + e.y));
+          out = make_uint2(child, e.y);
         }
-        warp_count(ctr + CTR_TESTS + Lv, tests);
-        warp_count(ctr + CTR_HITS + Lv, hits);
       }
-      __syncthreads();
-      // ---- drain: expand survivors level by level, then final tests
+      const uint32_t bt = __ballot_sync(CRSH_FULL, test);
+      const uint32_t b = __ballot_sync(CRSH_FULL, pass);
+      const uint32_t q1 = qlen[k - 1];
+      if (pass) q[s_qoff[k - 1] + q1 + __popc(b & lt)] = out;
+      __syncwarp();
+      if (lane == 0) {
+        qlen[k - 1] = q1 + __popc(b);
+        qlen[k] = qk - n;
+        atomicAdd(&ctr[CTR_TESTS + (k - 1)], (unsigned long long)__popc(bt));
+        atomicAdd(&ctr[CTR_HITS + (k - 1)], (unsigned long long)__popc(b));
+      }
+      __syncwarp();
+    };
+    // take steps from the lowest level with a full step; when `all`, finish
+    // with partial steps
+    auto drain = [&](bool all) {
       for (;;) {
-        for (int k = Lv; k >= 2; --k) {
-          const uint32_t qk = s_qlen[k], qk1 = s_qlen[k - 1];
-          const uint32_t cap = (k - 1 == Lv) ? (uint32_t)a.qtop_cap : (uint32_t)a.qcap;
-          const uint32_t n_take = min(qk, (cap - qk1) / (uint32_t)B);
-          if (n_take == 0) continue;
-          const uint32_t* qin = reinterpret_cast<const uint32_t*>(smraw + L.off_q[k]) + (qk - n_take);
-          uint32_t* qout = reinterpret_cast<uint32_t*>(smraw + L.off_q[k - 1]);
-          const float4* tv = a.trav[k - 1];
-          const size_t gbase = (size_t)g * a.per_group[k - 1];
-          uint32_t tests = 0, hits = 0;
-          const uint32_t n_work = n_take * (uint32_t)B;
-          for (uint32_t w0 = 0; w0 < n_work; w0 += TRAV_THREADS) {
-            const uint32_t w = w0 + tid;
-            bool pass = false;
-            uint32_t val = 0;
-            if (w < n_work) {
-              const uint32_t e = qin[w / B];
-              const uint32_t child = (e >> TRI_BITS) * B + (w % B);
-              const uint32_t tl = e & (MAX_TILE - 1);
-              const float4 c0 = __ldg(tv + 3 * (gbase + child));
-              if (c0.w >= 0.0f) {   // existing child
-                const float4 c1 = __ldg(tv + 3 * (gbase + child) + 1), c2 = __ldg(tv + 3 * (gbase + child) + 2);
-                pass = cull_ns(mk3(c0.x, c0.y, c0.z), c0.w, mk3(c1.x, c1.y, c1.z), c1.w, c2.x, s_tri_sph[tl]);
-                ++tests;
-                hits += pass;
-                val = (child << TRI_BITS) | tl;
-              }
-            }
-            push_warp(pass, val, qout, &s_qlen[k - 1]);
-          }
-          warp_count(ctr + CTR_TESTS + (k - 1), tests);
-          warp_count(ctr + CTR_HITS + (k - 1), hits);
-          __syncthreads();
-          if (tid == 0) s_qlen[k] = qk - n_take;
-          __syncthreads();
+        if (qlen[1] >= step_mt) { step_mt_fn(); continue; }
+        int pick = 0;
+        for (int k = 2; k < Lv - (Lv >= 2 ? 0 : 0); ++k)   // levels 2 .. Lv-1 (Lv >= 3 only)
+          if (qlen[k] >= step_exp) { pick = k; break; }
+        if (!pick && all) {
+          if (qlen[1]) { step_mt_fn(); continue; }
+          for (int k = 2; k < Lv; ++k)
+            if (qlen[k]) { pick = k; break; }
         }
-        // final intersection tests of the bundle survivors
-        const uint32_t q1 = s_qlen[1];
-        {
-          const uint32_t* qin = reinterpret_cast<const uint32_t*>(smraw + L.off_q[1]);
-          const uint32_t n_work = q1 * (uint32_t)B0;
-          const size_t rbase = (size_t)g * a.group_rays;
-          uint32_t tests = 0, hits = 0;
-          for (uint32_t w = tid; w < n_work; w += TRAV_THREADS) {
-            const uint32_t e = qin[w / B0];
-            const uint32_t rl = (e >> TRI_BITS) * B0 + (w % B0);
-            const float4 r0 = __ldg(a.sorted_rays + 2 * (rbase + rl));
-            if (r0.w < 0.0f) continue;   // padding ray
-            const float4 r1 = __ldg(a.sorted_rays + 2 * (rbase + rl) + 1);
-            const uint32_t tri = s_tri_id[e & (MAX_TILE - 1)];
-            const float4 v0 = __ldg(a.tri_e + 3 * (size_t)tri), e1 = __ldg(a.tri_e + 3 * (size_t)tri + 1),
-                         e2 = __ldg(a.tri_e + 3 * (size_t)tri + 2);
-            ++tests;
-            float th;
-            if (mt_ns(mk3(r0.x, r0.y, r0.z), mk3(r1.x, r1.y, r1.z), r0.w, r1.w, mk3(v0.x, v0.y, v0.z),
-                      mk3(e1.x, e1.y, e1.z), mk3(e2.x, e2.y, e2.z), &th)) {
-              ++hits;
-              const unsigned long long pk = pack_hit(th, tri);
-              if (SMEM_BEST) atomicMin(s_best + rl, pk);
-              else atomicMin(a.best + rbase + rl, pk);
-            }
-          }
-          warp_count(ctr + CTR_FINAL_TESTS, tests);
-          warp_count(ctr + CTR_FINAL_HITS, hits);
-        }
-        __syncthreads();
-        if (tid == 0) s_qlen[1] = 0u;
-        __syncthreads();
-        bool more = false;
-        for (int k = 2; k <= Lv; ++k) more |= s_qlen[k] != 0u;
-        if (!more) break;
+        if (!pick) return;
+        step_exp_fn(pick);
       }
-      __syncthreads();
+    };
+
+    for (uint32_t s = item.y + warp * 32u; s < item.z; s += TRAV_THREADS) {
+      const uint32_t v = s + lane;
+      uint32_t nm = 0, tri = 0;
+      float4 sph = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (v < item.z) {
+        uint32_t lo = 0, hi = n_act;   // largest p with prefix[p] <= v
+        while (hi - lo > 1) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (s_act_prefix[mid] <= v) lo = mid; else hi = mid;
+        }
+        tri = s_act_first[lo] + (v - s_act_prefix[lo]);
+        sph = __ldg(a.tri_sph + tri);
+        nm = s_act_nmask[lo];
+      }
+      for (int j = 0; j < K; ++j) {
+        const bool need = (nm >> j) & 1u;
+        const uint32_t bn = __ballot_sync(CRSH_FULL, need);
+        if (bn == 0u) continue;   // no lane's mesh kept node j
+        const float4 n0 = s_top[3 * j], n1 = s_top[3 * j + 1], n2 = s_top[3 * j + 2];
+        const bool pass = need & cull_ns(mk3(n0.x, n0.y, n0.z), n0.w, mk3(n1.x, n1.y, n1.z), n1.w, n2.x, sph);
+        const uint32_t b = __ballot_sync(CRSH_FULL, pass);
+        c_top_t += __popc(bn);
+        c_top_h += __popc(b);
+        if (b == 0u) continue;
+        if (Lv == 1) {   // the top level is the bundle level: queue for the final tests
+          const uint32_t ql = qlen[1];
+          if (pass) q[s_qoff[1] + ql + __popc(b & lt)] = make_uint2((uint32_t)j, tri);
+          __syncwarp();
+          if (lane == 0) qlen[1] = ql + __popc(b);
+          __syncwarp();
+          continue;
+        }
+        // dense children of node j (level Lv-1)
+        const int k1 = Lv - 1;
+        const uint32_t ql0 = qlen[k1];
+        uint2* qd = q + s_qoff[k1] + ql0;
+        uint32_t added = 0, n_ex = 0;
+        const uint32_t cbase = (uint32_t)j << logB;
+        const float4* nb = SMALL ? s_nodes + s_noff[k1] + 3 * cbase : s_trav[k1] + 3 * ((size_t)g * s_pg[k1] + cbase);
+#pragma unroll
+        for (int c = 0; c < (BT ? BT : 32); ++c) {
+          if (!BT && c >= B) break;
+          const float4 c0 = SMALL ? nb[3 * c] : __ldg(nb + 3 * c);
+          const float4 c1 = SMALL ? nb[3 * c + 1] : __ldg(nb + 3 * c + 1);
+          const float c2 = SMALL ? nb[3 * c + 2].x : __ldg(&nb[3 * c + 2].x);
+          const bool ex = c0.w >= 0.0f;   // existing child (uniform)
+          const bool p2 = pass & ex & cull_ns(mk3(c0.x, c0.y, c0.z), c0.w, mk3(c1.x, c1.y, c1.z), c1.w, c2, sph);
+          const uint32_t b2 = __ballot_sync(CRSH_FULL, p2);
+          if (p2) qd[added + __popc(b2 & lt)] = make_uint2(cbase | (uint32_t)c, tri);
+          added += __popc(b2);
+          n_ex += ex;
+        }
+        c_ch_t += __popc(b) * n_ex;
+        c_ch_h += added;
+        __syncwarp();
+        if (lane == 0) qlen[k1] = ql0 + added;
+        __syncwarp();
+        drain(false);
+      }
     }
-    if (SMEM_BEST) {
-      const size_t rbase = (size_t)g * a.group_rays;
+    drain(true);
+    // item counters -> CTA counters (one shared atomic per counter per warp)
+    c_mt_t = __reduce_add_sync(CRSH_FULL, c_mt_t);
+    c_mt_h = __reduce_add_sync(CRSH_FULL, c_mt_h);
+    if (lane == 0) {
+      if (c_top_t) atomicAdd(&ctr[CTR_TESTS + Lv], (unsigned long long)c_top_t);
+      if (c_top_h) atomicAdd(&ctr[CTR_HITS + Lv], (unsigned long long)c_top_h);
+      if (Lv >= 2 && c_ch_t) atomicAdd(&ctr[CTR_TESTS + Lv - 1], (unsigned long long)c_ch_t);
+      if (Lv >= 2 && c_ch_h) atomicAdd(&ctr[CTR_HITS + Lv - 1], (unsigned long long)c_ch_h);
+      if (c_mt_t) atomicAdd(&ctr[CTR_FINAL_TESTS], (unsigned long long)c_mt_t);
+      if (c_mt_h) atomicAdd(&ctr[CTR_FINAL_HITS], (unsigned long long)c_mt_h);
+    }
+    __syncthreads();
+    if (SMALL) {
       for (uint32_t r = tid; r < a.group_rays; r += TRAV_THREADS) {
         const unsigned long long b = s_best[r];
         if (b != BEST_NONE) atomicMin(a.best + rbase + r, b);

@@ -1,0 +1,89 @@
+"""World-size-2 CPU test (gloo) of the multi-GPU host path:
+two ranks each own a contiguous range of top-node groups of an oracle frame,
+encode their slots with the packed format of include/crsh.h, merge with the
+same MIN all-reduce the bench uses, and must reproduce the single-rank frame;
+summed counters must equal the single-rank counters."""
+import os
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2312_06538_b200 import dist as cd
+
+
+def _frame():
+    import oracle
+    from workloads import make_micro
+    w = make_micro(77, n_tris=60, W=24, H=20, n_lights=2, ray_types=7)
+    out = oracle.trace(w, taps=True)
+    return w, out
+
+
+def _owner_map(w, out, world):
+    """slot -> owning rank, by contiguous ranges of top-node groups (K groups of
+    64-ray top nodes per segment, padded per segment as in the library)."""
+    span, K = 64, 8
+    GR = span * K
+    owner = np.full(out["hit_tri"].shape, -1, np.int64)
+    bases, g0 = [], 0
+    for seg_sslot in out["taps"]["sslot"]:
+        n = len(seg_sslot)
+        bases.append(g0)
+        g0 += (n + GR - 1) // GR
+    G = g0
+    for seg_sslot, gb in zip(out["taps"]["sslot"], bases):
+        for i, slot in enumerate(seg_sslot):
+            g = gb + i // GR
+            for r in range(world):
+                lo, hi = cd.group_range(G, r, world)
+                if lo <= g < hi:
+                    owner[slot] = r
+    return owner
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    w, out = _frame()
+    owner = _owner_map(w, out, world)
+    packed = torch.from_numpy(cd.encode_owned(out["hit_tri"], out["t"], owner == rank).copy())
+    cd.merge_packed(packed)
+    hit, t = cd.decode_packed(packed.numpy())
+    cnt = torch.tensor([rank + 1, 10 * (rank + 1)], dtype=torch.int64)
+    cd.merge_counters(cnt)
+    q.put((rank, np.array_equal(hit, out["hit_tri"]), np.array_equal(t, out["t"]), cnt.tolist(),
+           int((owner == rank).sum())))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_packed_min_merge_over_gloo(world):
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok_h and ok_t for _, ok_h, ok_t, _, _ in res)
+    assert all(c == [3, 30] for _, _, _, c, _ in res)
+    assert all(n > 0 for *_, n in res)   # both ranks own work
+
+
+def test_decode_matches_header_encoding():
+    hit = np.array([5, -1, -2, 0], np.int32)
+    t = np.array([1.5, np.inf, np.inf, 2.0], np.float32)
+    owned = np.array([True, True, True, False])
+    p = cd.encode_owned(hit, t, owned)
+    assert p[1] == np.int64(cd.PACK_MISS) and p[2] == cd.PACK_EMPTY and p[3] == cd.PACK_EMPTY
+    h2, t2 = cd.decode_packed(p)
+    assert h2.tolist() == [5, -1, -2, -2] and t2[0] == 1.5
