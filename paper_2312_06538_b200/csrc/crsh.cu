@@ -264,7 +264,7 @@ cudaError_t dispatch_b(int B, F&& f) {
   return cudaErrorInvalidValue;
 }
 
-constexpr uint32_t ITEM_TRIS = 8192;
+constexpr uint32_t ITEM_TRIS = 2048;   // triangles per traversal work item (load balance)
 
 crsh_status trace_impl(crsh_scene* sc, const crsh_primary_hits* h, const float* lights, int32_t n_lights,
                        uint32_t types, const crsh_opts* o, int32_t* out_hit, float* out_t,

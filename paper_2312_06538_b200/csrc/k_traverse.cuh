@@ -354,10 +354,11 @@ __global__ void __launch_bounds__(TRAV_THREADS) k_traverse(const TravArgs a, con
 
     // final tests: one 32-lane step of Moller-Trumbore, B0 rays of up
     // to step_mt (bundle, triangle) entries taken from the end of Q[1]
+    const uint2* q1base = q + s_qoff[1];
     auto step_mt_fn = [&]() {
       const uint32_t qk = qlen[1];
       const uint32_t n = min(qk, step_mt);
-      const uint2* qin = q + s_qoff[1] + (qk - n);
+      const uint2* qin = q1base + (qk - n);
       const uint32_t n_work = n << logB0;
       for (uint32_t w = lane; w < n_work; w += 32) {
         const uint2 e = qin[w >> logB0];
@@ -480,9 +481,11 @@ __global__ void __launch_bounds__(TRAV_THREADS) k_traverse(const TravArgs a, con
           const float4 c1 = SMALL ? nb[3 * c + 1] : __ldg(nb + 3 * c + 1);
           const float c2 = SMALL ? nb[3 * c + 2].x : __ldg(&nb[3 * c + 2].x);
           const bool ex = c0.w >= 0.0f;   // existing child (uniform)
-          const bool p2 = pass & ex & cull_ns(mk3(c0.x, c0.y, c0.z), c0.w, mk3(c1.x, c1.y, c1.z), c1.w, c2, sph);
-          const uint32_t b2 = __ballot_sync(CRSH_FULL, p2);
-          if (p2) qd[added + __popc(b2 & lt)] = make_uint2(cbase | (uint32_t)c, tri);
+          // survivors = lanes whose parent test passed (b) and whose child test passes
+          const uint32_t b2 =
+              __ballot_sync(CRSH_FULL, cull_ns(mk3(c0.x, c0.y, c0.z), c0.w, mk3(c1.x, c1.y, c1.z), c1.w, c2, sph)) &
+              (ex ? b : 0u);
+          if ((b2 >> lane) & 1u) qd[added + __popc(b2 & lt)] = make_uint2(cbase | (uint32_t)c, tri);
           added += __popc(b2);
           n_ex += ex;
         }
