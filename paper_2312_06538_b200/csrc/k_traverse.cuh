@@ -210,14 +210,15 @@ struct TravArgs {
 
 // dynamic shared-memory layout (bytes), shared by host and device
 struct TravSmem {
-  uint32_t off_top, off_act_nmask, off_act_prefix, off_act_first, off_q, off_best, off_nodes, off_rays,
-      node_off[MAX_LEVELS + 1], q_off[MAX_LEVELS + 1], q_warp, total;
+  uint32_t off_top, off_exm, off_act_nmask, off_act_prefix, off_act_first, off_q, off_best, off_nodes, off_rays,
+      off_pairs, node_off[MAX_LEVELS + 1], q_off[MAX_LEVELS + 1], q_warp, total;
   __host__ __device__ static TravSmem make(int K, int B, int n_meshes, int Lv, bool small, const uint32_t* per_group,
                                            uint32_t group_rays) {
     TravSmem s;
     uint32_t o = 0;
     auto take = [&](uint32_t bytes) { const uint32_t r = o; o += (bytes + 15u) & ~15u; return r; };
     s.off_top = take(K * 48u);
+    s.off_exm = take(4u * K);   // existing-children mask of each top node
     s.off_act_nmask = take(4u * n_meshes);
     s.off_act_prefix = take(4u * (n_meshes + 1));
     s.off_act_first = take(4u * n_meshes);
@@ -235,13 +236,15 @@ struct TravSmem {
     }
     s.q_warp = qw;
     s.off_q = take(8u * qw * TRAV_WARPS);
-    s.off_best = s.off_nodes = s.off_rays = 0;
+    s.off_best = s.off_nodes = s.off_rays = s.off_pairs = 0;
     if (small) {
       uint32_t n4 = 0;   // float4 slots of the group's nodes below the top level
       for (int k = 1; k < Lv; ++k) { s.node_off[k] = n4; n4 += 3u * per_group[k]; }
       s.off_nodes = take(16u * (n4 ? n4 : 1u));
       s.off_rays = take(32u * group_rays);
       s.off_best = take(8u * group_rays);
+      // level Lv-1 nodes as paired records for the packed child tests (cull2_ns)
+      s.off_pairs = take(Lv >= 2 ? 80u * (per_group[Lv - 1] / 2u) : 16u);
     }
     s.total = o;
     return s;
@@ -259,6 +262,8 @@ __global__ void __launch_bounds__(TRAV_THREADS) k_traverse(const TravArgs a, con
   unsigned long long* s_best = reinterpret_cast<unsigned long long*>(smraw + L.off_best);
   const float4* s_nodes = reinterpret_cast<const float4*>(smraw + L.off_nodes);
   const float4* s_rays = reinterpret_cast<const float4*>(smraw + L.off_rays);
+  uint32_t* s_exm = reinterpret_cast<uint32_t*>(smraw + L.off_exm);
+  float4* s_pairs = reinterpret_cast<float4*>(smraw + L.off_pairs);
   __shared__ uint32_t s_item, s_cur_g, s_n_act, s_carry, s_carry_c;
   __shared__ uint32_t s_warp[8];
   __shared__ unsigned long long s_ctr[MAX_SEG * CTR_STRIDE];
@@ -316,6 +321,32 @@ __global__ void __launch_bounds__(TRAV_THREADS) k_traverse(const TravArgs a, con
       }
       if (tid == 0) { s_carry = 0u; s_carry_c = 0u; }
       __syncthreads();
+      if (Lv >= 2) {   // existing-children masks and (SMALL) paired child records
+        const int k1 = Lv - 1;
+        for (int j = tid; j < K; j += TRAV_THREADS) {
+          uint32_t m = 0;
+          for (int c = 0; c < B; ++c) {
+            const uint32_t child = ((uint32_t)j << logB) | (uint32_t)c;
+            const float r = SMALL ? s_nodes[s_noff[k1] + 3 * child].w
+                                  : __ldg(&s_trav[k1][3 * ((size_t)g * s_pg[k1] + child)].w);
+            m |= (r >= 0.0f ? 1u : 0u) << c;
+          }
+          s_exm[j] = m;
+        }
+        if (SMALL) {
+          const uint32_t n_pairs = s_pg[k1] / 2u;
+          for (uint32_t pp = tid; pp < n_pairs; pp += TRAV_THREADS) {
+            const float4* n0 = s_nodes + s_noff[k1] + 3 * (2 * pp);
+            const float4 a0 = n0[0], a1 = n0[1], a2 = n0[2], b0 = n0[3], b1 = n0[4], b2 = n0[5];
+            float4* rec = s_pairs + 5 * pp;
+            rec[0] = make_float4(a0.x, b0.x, a0.y, b0.y);
+            rec[1] = make_float4(a0.z, b0.z, a0.w, b0.w);
+            rec[2] = make_float4(a1.x, b1.x, a1.y, b1.y);
+            rec[3] = make_float4(a1.z, b1.z, a1.w, b1.w);
+            rec[4] = make_float4(a2.x, b2.x, 0.f, 0.f);
+          }
+        }
+      }
       // compact the meshes any of the K nodes kept, in mesh order, with the
       // exclusive prefix of their triangle counts (the group's virtual
       // triangle index space, cut into work items by k_plan)
@@ -350,7 +381,7 @@ __global__ void __launch_bounds__(TRAV_THREADS) k_traverse(const TravArgs a, con
     __syncthreads();
     const uint32_t n_act = s_n_act;
     const size_t rbase = (size_t)g * a.group_rays;
-    uint32_t c_top_t = 0, c_top_h = 0, c_ch_t = 0, c_ch_h = 0, c_mt_t = 0, c_mt_h = 0;   // item counters
+    uint32_t c_top_t = 0, c_top_h = 0, c_ch_t = 0, c_ch_h = 0, c_mt_t = 0, c_mt_h = 0;   // item counters (c_ch_h, c_mt_*: per lane)
 
     // final tests: one 32-lane step of Moller-Trumbore, B0 rays of up
     // to step_mt (bundle, triangle) entries taken from the end of Q[1]
@@ -449,6 +480,7 @@ __global__ void __launch_bounds__(TRAV_THREADS) k_traverse(const TravArgs a, con
         sph = __ldg(a.tri_sph + tri);
         nm = s_act_nmask[lo];
       }
+      const f2 Px = pk2(sph.x, sph.x), Py = pk2(sph.y, sph.y), Pz = pk2(sph.z, sph.z), Pr = pk2(sph.w, sph.w);
       for (int j = 0; j < K; ++j) {
         const bool need = (nm >> j) & 1u;
         const uint32_t bn = __ballot_sync(CRSH_FULL, need);
@@ -467,32 +499,50 @@ __global__ void __launch_bounds__(TRAV_THREADS) k_traverse(const TravArgs a, con
           __syncwarp();
           continue;
         }
-        // dense children of node j (level Lv-1)
+        // dense children of node j (level Lv-1), two per packed f32x2 test;
+        // per-lane survivor mask, appended once per top node with a warp scan
         const int k1 = Lv - 1;
-        const uint32_t ql0 = qlen[k1];
-        uint2* qd = q + s_qoff[k1] + ql0;
-        uint32_t added = 0, n_ex = 0;
         const uint32_t cbase = (uint32_t)j << logB;
-        const float4* nb = SMALL ? s_nodes + s_noff[k1] + 3 * cbase : s_trav[k1] + 3 * ((size_t)g * s_pg[k1] + cbase);
+        const uint32_t exm = s_exm[j];
+        uint32_t m = 0;
 #pragma unroll
-        for (int c = 0; c < (BT ? BT : 32); ++c) {
+        for (int c = 0; c < (BT ? BT : 32); c += 2) {
           if (!BT && c >= B) break;
-          const float4 c0 = SMALL ? nb[3 * c] : __ldg(nb + 3 * c);
-          const float4 c1 = SMALL ? nb[3 * c + 1] : __ldg(nb + 3 * c + 1);
-          const float c2 = SMALL ? nb[3 * c + 2].x : __ldg(&nb[3 * c + 2].x);
-          const bool ex = c0.w >= 0.0f;   // existing child (uniform)
-          // survivors = lanes whose parent test passed (b) and whose child test passes
-          const uint32_t b2 =
-              __ballot_sync(CRSH_FULL, cull_ns(mk3(c0.x, c0.y, c0.z), c0.w, mk3(c1.x, c1.y, c1.z), c1.w, c2, sph)) &
-              (ex ? b : 0u);
-          if ((b2 >> lane) & 1u) qd[added + __popc(b2 & lt)] = make_uint2(cbase | (uint32_t)c, tri);
-          added += __popc(b2);
-          n_ex += ex;
+          bool p0, p1;
+          if (SMALL) {
+            cull2_ns(s_pairs + 5 * ((cbase >> 1) + (uint32_t)(c >> 1)), Px, Py, Pz, Pr, p0, p1);
+          } else {
+            const float4* nd = s_trav[k1] + 3 * ((size_t)g * s_pg[k1] + cbase + (uint32_t)c);
+            const float4 a0 = __ldg(nd), a1 = __ldg(nd + 1), a2 = __ldg(nd + 2), b0 = __ldg(nd + 3),
+                         b1 = __ldg(nd + 4), b2 = __ldg(nd + 5);
+            const float4 rec[5] = {make_float4(a0.x, b0.x, a0.y, b0.y), make_float4(a0.z, b0.z, a0.w, b0.w),
+                                   make_float4(a1.x, b1.x, a1.y, b1.y), make_float4(a1.z, b1.z, a1.w, b1.w),
+                                   make_float4(a2.x, b2.x, 0.f, 0.f)};
+            cull2_ns(rec, Px, Py, Pz, Pr, p0, p1);
+          }
+          m |= ((p0 ? 1u : 0u) << c) | ((p1 ? 1u : 0u) << (c + 1));
         }
-        c_ch_t += __popc(b) * n_ex;
-        c_ch_h += added;
+        m = pass ? (m & exm) : 0u;
+        c_ch_t += __popc(b) * __popc(exm);
+        const uint32_t cnt = __popc(m);
+        c_ch_h += cnt;
+        uint32_t incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(CRSH_FULL, incl, o);
+          if ((int)lane >= o) incl += y;
+        }
+        const uint32_t tot = __shfl_sync(CRSH_FULL, incl, 31);
+        if (tot == 0u) continue;
+        const uint32_t ql0 = qlen[k1];
+        uint2* qd = q + s_qoff[k1] + ql0 + (incl - cnt);
+        while (m) {
+          const uint32_t c = __ffs(m) - 1;
+          m &= m - 1;
+          *qd++ = make_uint2(cbase | c, tri);
+        }
         __syncwarp();
-        if (lane == 0) qlen[k1] = ql0 + added;
+        if (lane == 0) qlen[k1] = ql0 + tot;
         __syncwarp();
         drain(false);
       }
@@ -501,6 +551,7 @@ __global__ void __launch_bounds__(TRAV_THREADS) k_traverse(const TravArgs a, con
     // item counters -> CTA counters (one shared atomic per counter per warp)
     c_mt_t = __reduce_add_sync(CRSH_FULL, c_mt_t);
     c_mt_h = __reduce_add_sync(CRSH_FULL, c_mt_h);
+    c_ch_h = __reduce_add_sync(CRSH_FULL, c_ch_h);
     if (lane == 0) {
       if (c_top_t) atomicAdd(&ctr[CTR_TESTS + Lv], (unsigned long long)c_top_t);
       if (c_top_h) atomicAdd(&ctr[CTR_HITS + Lv], (unsigned long long)c_top_h);

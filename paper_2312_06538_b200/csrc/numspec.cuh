@@ -239,3 +239,47 @@ __device__ __forceinline__ bool mt_ns(f3 o, f3 d, float tmin, float tmax, f3 v0,
 }
 
 }  // namespace crsh
+
+// ---------------------------------------------------------------- packed f32x2 (sm_100a FFMA2 & co)
+// Two independent IEEE round-to-nearest float32 operations per instruction:
+// each half is bit-identical to the scalar operation, so cull2_ns gives the
+// same decisions as two cull_ns calls.
+namespace crsh {
+typedef unsigned long long f2;
+__device__ __forceinline__ f2 pk2(float lo, float hi) {
+  f2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void up2(f2 v, float& lo, float& hi) { asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v)); }
+__device__ __forceinline__ f2 add2(f2 a, f2 b) { f2 d; asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b)); return d; }
+__device__ __forceinline__ f2 sub2(f2 a, f2 b) { f2 d; asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b)); return d; }
+__device__ __forceinline__ f2 mul2(f2 a, f2 b) { f2 d; asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b)); return d; }
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) { f2 d; asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c)); return d; }
+
+// Paired node record (two children c, c+1), 5 x float4 in shared memory:
+// {Cx0,Cx1,Cy0,Cy1}, {Cz0,Cz1,d0,d1}, {ax0,ax1,ay0,ay1}, {az0,az1,tan0,tan1}, {sec0,sec1,-,-}
+// Eq 9 for both children against one target sphere (px,py,pz,r); same
+// operation order as cull_ns.
+__device__ __forceinline__ void cull2_ns(const float4* rec, f2 Px, f2 Py, f2 Pz, f2 R, bool& p0, bool& p1) {
+  const float4 A = rec[0], Bv = rec[1], Cc = rec[2], D = rec[3], E = rec[4];
+  const f2 cx = pk2(A.x, A.y), cy = pk2(A.z, A.w), cz = pk2(Bv.x, Bv.y), dd = pk2(Bv.z, Bv.w);
+  const f2 ax = pk2(Cc.x, Cc.y), ay = pk2(Cc.z, Cc.w), az = pk2(D.x, D.y), tn = pk2(D.z, D.w), sc = pk2(E.x, E.y);
+  const f2 vx = sub2(Px, cx), vy = sub2(Py, cy), vz = sub2(Pz, cz);
+  const f2 s = fma2(vx, ax, fma2(vy, ay, mul2(vz, az)));
+  const f2 ns = mul2(s, pk2(-1.0f, -1.0f));
+  const f2 wx = fma2(ns, ax, vx), wy = fma2(ns, ay, vy), wz = fma2(ns, az, vz);
+  const f2 w2 = fma2(wx, wx, fma2(wy, wy, mul2(wz, wz)));
+  const f2 dr = add2(dd, R);
+  float s0, s1;
+  up2(s, s0, s1);
+  const f2 rhs = fma2(pk2(fmaxf(s0, 0.0f), fmaxf(s1, 0.0f)), tn, mul2(dr, sc));
+  const f2 rr = mul2(rhs, rhs);
+  float w0, w1, r0, r1, d0, d1;
+  up2(w2, w0, w1);
+  up2(rr, r0, r1);
+  up2(dr, d0, d1);
+  p0 = (s0 >= -d0) & (w0 <= r0);
+  p1 = (s1 >= -d1) & (w1 <= r1);
+}
+}  // namespace crsh
