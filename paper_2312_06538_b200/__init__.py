@@ -16,7 +16,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libcrsh.so")
+LIB_PATH = os.environ.get("CRSH_LIB_PATH") or os.path.join(HERE, "libcrsh.so")   # override: A/B experiments
 HEADER = os.path.join(os.path.dirname(HERE), "include", "crsh.h")
 
 SHADOW, REFLECT, REFRACT = 1, 2, 4

@@ -77,7 +77,7 @@ constexpr int RADIX_BITS = 8;
 constexpr int RADIX_BINS = 256;
 constexpr int SORT_THREADS = 256;
 constexpr int SORT_WARPS = SORT_THREADS / 32;
-constexpr int SORT_ITEMS = 16;
+constexpr int SORT_ITEMS = 8;
 constexpr int SORT_TILE = SORT_THREADS * SORT_ITEMS;   // 4096
 constexpr int SORT_PASSES = 32 / RADIX_BITS;
 
@@ -195,13 +195,24 @@ __global__ void __launch_bounds__(SORT_THREADS) k_onesweep(const SortPassArgs a)
     st_store32(st, (2u << 30) | cnt);
   } else {
     st_store32(st, (1u << 30) | cnt);
+    // batched look-back: 8 predecessors' words are requested at once, so a
+    // one-wave sort (every tile looking back at aggregates) costs ~1/8 of the
+    // round trips of a one-by-one walk; the segment's first tile is inclusive
+    const int first = (int)a.sc.tile_start[seg];
     int p = (int)tile - 1;
-    for (;;) {
-      uint32_t w;
-      do { w = st_load32(a.status + (size_t)p * RADIX_BINS + b); } while ((w >> 30) == 0u);
-      excl += w & 0x3FFFFFFFu;
-      if ((w >> 30) == 2u) break;
-      --p;
+    bool done = false;
+    while (!done) {
+      uint32_t w[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) w[i] = (p - i >= first) ? st_load32(a.status + (size_t)(p - i) * RADIX_BINS + b) : 0u;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if (done || p - i < first) continue;
+        while ((w[i] >> 30) == 0u) w[i] = st_load32(a.status + (size_t)(p - i) * RADIX_BINS + b);
+        excl += w[i] & 0x3FFFFFFFu;
+        done = (w[i] >> 30) == 2u;
+      }
+      p -= 8;
     }
     st_store32(st, (2u << 30) | (excl + cnt));
   }
