@@ -246,19 +246,23 @@ bool cull_test(const Node& n, V3 P, float r) {
   return w2 <= rhs * rhs;                            // >= |P-H|
 }
 
-// Moller-Trumbore ray-triangle test (P:185 [Mol97]; R15), two-sided.
+// Moller-Trumbore ray-triangle test (P:185 [Mol97]; R15), two-sided, in the
+// original paper's division-free decision order: the barycentric numerators
+// are compared against |det| (sign folded in exactly), and the single
+// reciprocal of det is only taken for t of a candidate hit.
 bool moller_trumbore(V3 o, V3 d, float tmin, float tmax, V3 v0, V3 e1, V3 e2, float* t_out) {
   V3 p = cross3(d, e2);
   float det = dot3(e1, p);
   if (det == 0.0f) return false;
-  float inv = 1.0f / det;
+  float sg = det > 0.0f ? 1.0f : -1.0f;
+  float adet = det * sg;                 // |det|
   V3 tv = sub(o, v0);
-  float u = dot3(tv, p) * inv;
-  if (u < 0.0f || u > 1.0f) return false;
+  float un = dot3(tv, p) * sg;           // u * |det|
+  if (un < 0.0f || un > adet) return false;
   V3 q = cross3(tv, e1);
-  float v = dot3(d, q) * inv;
-  if (v < 0.0f || u + v > 1.0f) return false;
-  float t = dot3(e2, q) * inv;
+  float vn = dot3(d, q) * sg;            // v * |det|
+  if (vn < 0.0f || un + vn > adet) return false;
+  float t = dot3(e2, q) * (1.0f / det);
   if (!(t > tmin && t < tmax)) return false;
   *t_out = t;
   return true;

@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(TRAV_THREADS) k_traverse(const TravArgs a, con
   uint2* q = reinterpret_cast<uint2*>(smraw + L.off_q) + warp * L.q_warp;
   uint32_t* qlen = s_qlen[warp];
   const uint32_t step_exp = (32u >> logB) ? (32u >> logB) : 1u;   // entries per expansion step
-  const uint32_t step_mt = (32u >> logB0) ? (32u >> logB0) : 1u;  // entries per final-test step
+  const uint32_t step_mt = 32u;                                   // entries per final-test step (one per lane)
   for (uint32_t i = tid; i < MAX_SEG * CTR_STRIDE; i += TRAV_THREADS) s_ctr[i] = 0ull;
   if (lane <= MAX_LEVELS) qlen[lane] = 0u;
   if (tid == 0) s_cur_g = 0xFFFFFFFFu;
@@ -383,30 +383,33 @@ __global__ void __launch_bounds__(TRAV_THREADS) k_traverse(const TravArgs a, con
     const size_t rbase = (size_t)g * a.group_rays;
     uint32_t c_top_t = 0, c_top_h = 0, c_ch_t = 0, c_ch_h = 0, c_mt_t = 0, c_mt_h = 0;   // item counters (c_ch_h, c_mt_*: per lane)
 
-    // final tests: one 32-lane step of Moller-Trumbore, B0 rays of up
-    // to step_mt (bundle, triangle) entries taken from the end of Q[1]
+    // final tests: one step = up to 32 (bundle, triangle) entries
+    // from the end of Q[1], one per lane; the lane loads its triangle once
+    // and runs Moller-Trumbore against the bundle's B0 rays
     const uint2* q1base = q + s_qoff[1];
+    const int B0 = a.B0;
     auto step_mt_fn = [&]() {
       const uint32_t qk = qlen[1];
       const uint32_t n = min(qk, step_mt);
-      const uint2* qin = q1base + (qk - n);
-      const uint32_t n_work = n << logB0;
-      for (uint32_t w = lane; w < n_work; w += 32) {
-        const uint2 e = qin[w >> logB0];
-        const uint32_t rl = (e.x << logB0) | (w & B0m);
-        const float4 r0 = SMALL ? s_rays[2 * rl] : __ldg(a.sorted_rays + 2 * (rbase + rl));
-        if (r0.w < 0.0f) continue;   // padding ray
-        const float4 r1 = SMALL ? s_rays[2 * rl + 1] : __ldg(a.sorted_rays + 2 * (rbase + rl) + 1);
+      if (lane < n) {
+        const uint2 e = q1base[qk - n + lane];
         const float4* te = a.tri_e + 3 * (size_t)e.y;
-        const float4 v0 = __ldg(te), e1 = __ldg(te + 1), e2 = __ldg(te + 2);
-        ++c_mt_t;
-        float th;
-        if (mt_ns(mk3(r0.x, r0.y, r0.z), mk3(r1.x, r1.y, r1.z), r0.w, r1.w, mk3(v0.x, v0.y, v0.z),
-                  mk3(e1.x, e1.y, e1.z), mk3(e2.x, e2.y, e2.z), &th)) {
-          ++c_mt_h;
-          const unsigned long long pk = pack_hit(th, e.y);
-          if (SMALL) atomicMin(s_best + rl, pk);
-          else atomicMin(a.best + rbase + rl, pk);
+        const float4 tv0 = __ldg(te), te1 = __ldg(te + 1), te2 = __ldg(te + 2);
+        const f3 v0 = mk3(tv0.x, tv0.y, tv0.z), e1 = mk3(te1.x, te1.y, te1.z), e2 = mk3(te2.x, te2.y, te2.z);
+        const uint32_t rl0 = e.x << logB0;
+        for (int r = 0; r < B0; ++r) {
+          const uint32_t rl = rl0 + (uint32_t)r;
+          const float4 r0 = SMALL ? s_rays[2 * rl] : __ldg(a.sorted_rays + 2 * (rbase + rl));
+          if (r0.w < 0.0f) break;   // padding rays are at the end of the bundle
+          const float4 r1 = SMALL ? s_rays[2 * rl + 1] : __ldg(a.sorted_rays + 2 * (rbase + rl) + 1);
+          ++c_mt_t;
+          float th;
+          if (mt_ns(mk3(r0.x, r0.y, r0.z), mk3(r1.x, r1.y, r1.z), r0.w, r1.w, v0, e1, e2, &th)) {
+            ++c_mt_h;
+            const unsigned long long pk = pack_hit(th, e.y);
+            if (SMALL) atomicMin(s_best + rl, pk);
+            else atomicMin(a.best + rbase + rl, pk);
+          }
         }
       }
       __syncwarp();

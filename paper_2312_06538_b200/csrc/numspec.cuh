@@ -220,19 +220,21 @@ __device__ __forceinline__ bool cull_ns(f3 C, float d, f3 a, float tn, float sc,
   return (s >= -dr) & (w2 <= rhs * rhs);
 }
 
-// Moller-Trumbore (R15). Returns t or -1 (no hit in (tmin, tmax)).
+// Moller-Trumbore (R15), two-sided, division-free decision order:
+// barycentric numerators against |det|; one reciprocal for t of a candidate.
 __device__ __forceinline__ bool mt_ns(f3 o, f3 d, float tmin, float tmax, f3 v0, f3 e1, f3 e2, float* tout) {
   const f3 p = cross3(d, e2);
   const float det = dot3(e1, p);
   if (det == 0.0f) return false;
-  const float inv = 1.0f / det;
+  const float sg = det > 0.0f ? 1.0f : -1.0f;
+  const float adet = det * sg;
   const f3 tv = o - v0;
-  const float u = dot3(tv, p) * inv;
-  if (u < 0.0f || u > 1.0f) return false;
+  const float un = dot3(tv, p) * sg;
+  if (un < 0.0f || un > adet) return false;
   const f3 q = cross3(tv, e1);
-  const float v = dot3(d, q) * inv;
-  if (v < 0.0f || u + v > 1.0f) return false;
-  const float t = dot3(e2, q) * inv;
+  const float vn = dot3(d, q) * sg;
+  if (vn < 0.0f || un + vn > adet) return false;
+  const float t = dot3(e2, q) * (1.0f / det);
   if (!(t > tmin && t < tmax)) return false;
   *tout = t;
   return true;
