@@ -243,7 +243,12 @@ def run_crsh(args):
     peaks = measured_peaks()
     clocks = clk.summary()
     sm_max = (clocks or {}).get("sm_max_mhz") or peaks.get("sm_max_mhz", 1965.0)
-    peak_tflops = SM_COUNT * FP32_LANES * FMA_FLOPS * sm_max * 1e6 / 1e12
+    peak_tflops, peak_src = SM_COUNT * FP32_LANES * FMA_FLOPS * sm_max * 1e6 / 1e12, "nominal 148 SM x 128 lanes x 2"
+    try:   # measured FFMA throughput on this pool's B200 (tools/fp32_peak.cu)
+        peak_tflops = float(json.load(open(os.path.join(ROOT, "profiles", "fp32_peak.json")))["ffma_tflops"])
+        peak_src = "measured FFMA microbenchmark (profiles/fp32_peak.json)"
+    except (OSError, ValueError, KeyError):
+        pass
     tflops = trav_flops(st) / (trav_ms * 1e-3) / 1e12 if trav_ms > 0 else 0.0
     traffic = load_traffic()
     brute = rays * tr.M
@@ -269,8 +274,8 @@ def run_crsh(args):
         "stage_ms": {n: round(v / args.steps, 4) for n, v in zip(stage_names, stage)},
         "roofline": {"bound": "alu", "kernel": "k_traverse", "achieved": round(tflops, 3), "peak": round(peak_tflops, 2),
                      "unit": "TFLOP/s", "frac": round(tflops / peak_tflops, 4), "traffic": traffic,
-                     "note": f"FP32: {EQ9_FLOPS} flops per Eq 9 test, {MT_FLOPS} per MT test; peak = 148 SM x 128 "
-                             f"FP32 lanes x 2 x {sm_max:.0f} MHz; kernel time from CUDA events around k_traverse"},
+                     "note": f"FP32: {EQ9_FLOPS} flops per Eq 9 test, {MT_FLOPS} per MT test; peak: {peak_src}; "
+                             f"kernel time from CUDA events around k_traverse"},
         "gpu_launches": launches,
         "e2e": e2e,
         "clocks": clocks,

@@ -315,9 +315,17 @@ __global__ void __launch_bounds__(TRAV_THREADS) k_traverse(const TravArgs a, con
           const float4* src = s_trav[k] + (size_t)g * n4;
           for (uint32_t j = tid; j < n4; j += TRAV_THREADS) sn[s_noff[k] + j] = __ldg(src + j);
         }
+        // the group's rays as paired records (rays 2i, 2i+1) for mt2_ns
         float4* sr = reinterpret_cast<float4*>(smraw + L.off_rays);
         const float4* rs = a.sorted_rays + 2 * (size_t)g * a.group_rays;
-        for (uint32_t j = tid; j < 2 * a.group_rays; j += TRAV_THREADS) sr[j] = __ldg(rs + j);
+        for (uint32_t pp = tid; pp < a.group_rays / 2u; pp += TRAV_THREADS) {
+          const float4 a0 = __ldg(rs + 4 * pp), a1 = __ldg(rs + 4 * pp + 1), b0 = __ldg(rs + 4 * pp + 2),
+                       b1 = __ldg(rs + 4 * pp + 3);
+          sr[4 * pp] = make_float4(a0.x, b0.x, a0.y, b0.y);
+          sr[4 * pp + 1] = make_float4(a0.z, b0.z, a0.w, b0.w);
+          sr[4 * pp + 2] = make_float4(a1.x, b1.x, a1.y, b1.y);
+          sr[4 * pp + 3] = make_float4(a1.z, b1.z, a1.w, b1.w);
+        }
       }
       if (tid == 0) { s_carry = 0u; s_carry_c = 0u; }
       __syncthreads();
@@ -396,20 +404,38 @@ __global__ void __launch_bounds__(TRAV_THREADS) k_traverse(const TravArgs a, con
         const float4* te = a.tri_e + 3 * (size_t)e.y;
         const float4 tv0 = __ldg(te), te1 = __ldg(te + 1), te2 = __ldg(te + 2);
         const f3 v0 = mk3(tv0.x, tv0.y, tv0.z), e1 = mk3(te1.x, te1.y, te1.z), e2 = mk3(te2.x, te2.y, te2.z);
-        const uint32_t rl0 = e.x << logB0;
-        for (int r = 0; r < B0; ++r) {
+        const uint32_t rl0 = e.x << logB0;   // first ray of the bundle (B0 even)
+        for (int r = 0; r < B0; r += 2) {
           const uint32_t rl = rl0 + (uint32_t)r;
-          const float4 r0 = SMALL ? s_rays[2 * rl] : __ldg(a.sorted_rays + 2 * (rbase + rl));
-          if (r0.w < 0.0f) break;   // padding rays are at the end of the bundle
-          const float4 r1 = SMALL ? s_rays[2 * rl + 1] : __ldg(a.sorted_rays + 2 * (rbase + rl) + 1);
-          ++c_mt_t;
-          float th;
-          if (mt_ns(mk3(r0.x, r0.y, r0.z), mk3(r1.x, r1.y, r1.z), r0.w, r1.w, v0, e1, e2, &th)) {
-            ++c_mt_h;
-            const unsigned long long pk = pack_hit(th, e.y);
-            if (SMALL) atomicMin(s_best + rl, pk);
-            else atomicMin(a.best + rbase + rl, pk);
+          float4 A, Bq, Cq, Dq;
+          if (SMALL) {
+            const float4* rp = s_rays + 2 * rl;   // paired record of rays rl, rl+1
+            A = rp[0]; Bq = rp[1]; Cq = rp[2]; Dq = rp[3];
+          } else {
+            const float4* rs = a.sorted_rays + 2 * (rbase + rl);
+            const float4 a0 = __ldg(rs), a1 = __ldg(rs + 1), b0 = __ldg(rs + 2), b1 = __ldg(rs + 3);
+            A = make_float4(a0.x, b0.x, a0.y, b0.y); Bq = make_float4(a0.z, b0.z, a0.w, b0.w);
+            Cq = make_float4(a1.x, b1.x, a1.y, b1.y); Dq = make_float4(a1.z, b1.z, a1.w, b1.w);
           }
+          const bool real0 = Bq.z >= 0.0f, real1 = Bq.w >= 0.0f;   // padding rays (tmin -1) come last
+          if (!real0) break;
+          c_mt_t += 1u + (uint32_t)real1;
+          bool h0, h1;
+          float t0, t1;
+          mt2_ns(A, Bq, Cq, Dq, v0, e1, e2, h0, t0, h1, t1);
+          h1 &= real1;
+          if (h0 | h1) {
+            c_mt_h += (uint32_t)h0 + (uint32_t)h1;
+            if (h0) {
+              const unsigned long long pk = pack_hit(t0, e.y);
+              if (SMALL) atomicMin(s_best + rl, pk); else atomicMin(a.best + rbase + rl, pk);
+            }
+            if (h1) {
+              const unsigned long long pk = pack_hit(t1, e.y);
+              if (SMALL) atomicMin(s_best + rl + 1, pk); else atomicMin(a.best + rbase + rl + 1, pk);
+            }
+          }
+          if (!real1) break;
         }
       }
       __syncwarp();

@@ -285,3 +285,48 @@ __device__ __forceinline__ void cull2_ns(const float4* rec, f2 Px, f2 Py, f2 Pz,
   p1 = (s1 >= -d1) & (w1 <= r1);
 }
 }  // namespace crsh
+
+namespace crsh {
+// Moller-Trumbore (mt_ns, same per-half operation order) for two rays given
+// as a paired record {ox0,ox1,oy0,oy1} {oz0,oz1,tmin0,tmin1}
+// {dx0,dx1,dy0,dy1} {dz0,dz1,tmax0,tmax1} against one triangle; the
+// triangle's scalars enter the packed instructions as broadcast operands.
+__device__ __forceinline__ void mt2_ns(float4 A, float4 Bq, float4 Cq, float4 Dq, f3 v0, f3 e1, f3 e2, bool& h0,
+                                       float& t0, bool& h1, float& t1) {
+  const f2 ox = pk2(A.x, A.y), oy = pk2(A.z, A.w), oz = pk2(Bq.x, Bq.y);
+  const f2 dx = pk2(Cq.x, Cq.y), dy = pk2(Cq.z, Cq.w), dz = pk2(Dq.x, Dq.y);
+  const f2 px = fma2(dy, pk2(e2.z, e2.z), mul2(dz, pk2(-e2.y, -e2.y)));
+  const f2 py = fma2(dz, pk2(e2.x, e2.x), mul2(dx, pk2(-e2.z, -e2.z)));
+  const f2 pz = fma2(dx, pk2(e2.y, e2.y), mul2(dy, pk2(-e2.x, -e2.x)));
+  const f2 det = fma2(pk2(e1.x, e1.x), px, fma2(pk2(e1.y, e1.y), py, mul2(pk2(e1.z, e1.z), pz)));
+  float d0, d1;
+  up2(det, d0, d1);
+  const f2 sg = pk2(d0 > 0.0f ? 1.0f : -1.0f, d1 > 0.0f ? 1.0f : -1.0f);
+  const f2 adet = mul2(det, sg);
+  const f2 tx = sub2(ox, pk2(v0.x, v0.x)), ty = sub2(oy, pk2(v0.y, v0.y)), tz = sub2(oz, pk2(v0.z, v0.z));
+  const f2 un = mul2(fma2(tx, px, fma2(ty, py, mul2(tz, pz))), sg);
+  float u0, u1, a0v, a1v;
+  up2(un, u0, u1);
+  up2(adet, a0v, a1v);
+  bool k0 = (d0 != 0.0f) & (u0 >= 0.0f) & (u0 <= a0v);
+  bool k1 = (d1 != 0.0f) & (u1 >= 0.0f) & (u1 <= a1v);
+  h0 = h1 = false;
+  if (!(k0 | k1)) return;
+  const f2 qx = fma2(ty, pk2(e1.z, e1.z), mul2(tz, pk2(-e1.y, -e1.y)));
+  const f2 qy = fma2(tz, pk2(e1.x, e1.x), mul2(tx, pk2(-e1.z, -e1.z)));
+  const f2 qz = fma2(tx, pk2(e1.y, e1.y), mul2(ty, pk2(-e1.x, -e1.x)));
+  const f2 vn = mul2(fma2(dx, qx, fma2(dy, qy, mul2(dz, qz))), sg);
+  const f2 s = add2(un, vn);
+  float v0f, v1f, s0, s1;
+  up2(vn, v0f, v1f);
+  up2(s, s0, s1);
+  k0 &= (v0f >= 0.0f) & (s0 <= a0v);
+  k1 &= (v1f >= 0.0f) & (s1 <= a1v);
+  if (!(k0 | k1)) return;
+  const f2 tt = mul2(fma2(pk2(e2.x, e2.x), qx, fma2(pk2(e2.y, e2.y), qy, mul2(pk2(e2.z, e2.z), qz))),
+                     pk2(1.0f / d0, 1.0f / d1));
+  up2(tt, t0, t1);
+  h0 = k0 & (t0 > Bq.z) & (t0 < Dq.z);
+  h1 = k1 & (t1 > Bq.w) & (t1 < Dq.w);
+}
+}  // namespace crsh
