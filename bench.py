@@ -318,6 +318,81 @@ def run_reference(args):
     print(json.dumps(out), flush=True)
 
 
+# ----------------------------------------------------------------------------- extra reports (not the contract line)
+def _time_frames(tr, steps, stream):
+    import torch
+    ms = []
+    for _ in range(steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        tr.run(stream)
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms.append(a.elapsed_time(b))
+    return float(np.median(ms))
+
+
+def run_table4(args):
+    """The paper's Table 4 comparison on the synthetic workload:
+    total ray-primitive tests and frame time of CRSH, CRSH with the Z-order
+    hash, RAH (no sort, no mesh culling) and naive N x M."""
+    import torch
+
+    import paper_2312_06538_b200 as crsh
+    from paper_2312_06538_b200.api import tracer_for
+    from workloads import make_workload
+    w = make_workload(args.config)
+    stream = torch.cuda.current_stream()
+    rows = {}
+    for name, flags in (("brute", crsh.F_BRUTE), ("rah", 0), ("crsh", 3), ("crsh_zorder", 7)):
+        tr = tracer_for(w, flags=flags)
+        tr.run(stream)
+        torch.cuda.synchronize()
+        ms = _time_frames(tr, max(1, args.steps if name != "brute" else 2), stream)
+        st = tr.stats()
+        total = int(np.asarray(st["tests"]).sum()) + int(sum(st["final_tests"]))
+        rows[name] = {"ms_per_frame": round(ms, 3), "total_tests": total, "mesh_tests": int(sum(st["mesh_tests"])),
+                      "tests_per_ray": round(total / max(1, sum(st["rays"])), 2),
+                      "mrays_per_s": round(sum(st["rays"]) / (ms * 1e-3) / 1e6, 3),
+                      "by_level": {f"L{k}": int(np.asarray(st["tests"])[:, k].sum()) for k in range(w.levels, 0, -1)},
+                      "final_tests": int(sum(st["final_tests"]))}
+    bt = rows["brute"]["total_tests"]
+    for r in rows.values():
+        r["relative_pct"] = round(100.0 * r["total_tests"] / bt, 4)
+    rows["crsh_reduction_vs_rah_pct"] = round(100.0 * (1 - rows["crsh"]["total_tests"] / rows["rah"]["total_tests"]), 2)
+    rows["crsh_zorder_reduction_vs_rah_pct"] = round(
+        100.0 * (1 - rows["crsh_zorder"]["total_tests"] / rows["rah"]["total_tests"]), 2)
+    print(json.dumps({"mode": "table4", "workload": w.name, "rays": int(sum(tr.stats()["rays"])), "M": tr.M,
+                      "engines": rows}), flush=True)
+
+
+def run_sweep(args):
+    """cfg5 (BASELINE configs[4]): hierarchy depth Lv 2..6 x bundle size B0 in
+    {4, 8, 16, 32, 64} at 1024x1024, ~250k triangles in 30 meshes."""
+    import torch
+
+    from paper_2312_06538_b200.api import tracer_for
+    from workloads import make_workload
+    stream = torch.cuda.current_stream()
+    base = make_workload(5)
+    for lv in (2, 3, 4, 5, 6):
+        for b0 in (4, 8, 16, 32, 64):
+            base.levels, base.leaf_size, base.branching = lv, b0, 8
+            tr = tracer_for(base, flags=7 if args.zorder else 3)
+            tr.run(stream)
+            torch.cuda.synchronize()
+            ms = _time_frames(tr, max(1, args.steps), stream)
+            st = tr.stats()
+            total = int(np.asarray(st["tests"]).sum()) + int(sum(st["final_tests"]))
+            print(json.dumps({"mode": "sweep", "levels": lv, "leaf_size": b0, "branching": 8,
+                              "hash": "zorder" if args.zorder else "R6", "ms_per_frame": round(ms, 3),
+                              "mrays_per_s": round(sum(st["rays"]) / (ms * 1e-3) / 1e6, 3),
+                              "tests_per_ray": round(total / max(1, sum(st["rays"])), 2),
+                              "by_level": {f"L{k}": int(np.asarray(st["tests"])[:, k].sum()) for k in range(lv, 0, -1)},
+                              "final_tests": int(sum(st["final_tests"]))}), flush=True)
+            del tr
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -327,7 +402,13 @@ def main():
     ap.add_argument("--impl", default="crsh", choices=["crsh", "reference"])
     ap.add_argument("--zorder", action="store_true", help="Z-order hash layout (SURVEY §8(f) NEXT-4)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--table4", action="store_true", help="CRSH vs RAH vs N x M report (not the contract line)")
+    ap.add_argument("--sweep", action="store_true", help="cfg5 depth/bundle sweep (not the contract line)")
     args = ap.parse_args()
+    if args.table4:
+        return run_table4(args)
+    if args.sweep:
+        return run_sweep(args)
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":

@@ -48,12 +48,16 @@ enum { CRSH_SHADOW = 1u, CRSH_REFLECT = 2u, CRSH_REFRACT = 4u };
  * the RAH baseline of P:47-49 (rays in generation order, no mesh spheres).
  * CRSH_F_ZORDER selects the Z-order (bit-interleaved) hash layout instead of
  * the concatenated layout of R6.
- * CRSH_F_STAGE_TIMING records per-stage CUDA-event times into stage_ms. */
+ * CRSH_F_STAGE_TIMING records per-stage CUDA-event times into stage_ms.
+ * CRSH_F_BRUTE replaces the hierarchy by the N x M baseline (final_tests =
+ * rays * M); the other flags are then ignored. */
 enum {
   CRSH_F_SORT = 1u,
   CRSH_F_MESH_CULL = 2u,
   CRSH_F_ZORDER = 4u,
-  CRSH_F_STAGE_TIMING = 8u
+  CRSH_F_STAGE_TIMING = 8u,
+  CRSH_F_BRUTE = 16u   /* naive N x M ray tracing: every ray
+                          against every triangle, no hierarchy; same outputs */
 };
 
 /* Build a scene (untimed preparation): copies the geometry, computes

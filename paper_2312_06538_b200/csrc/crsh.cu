@@ -288,7 +288,7 @@ crsh_status trace_impl(crsh_scene* sc, const crsh_primary_hits* h, const float* 
   if (span > (1ull << 22)) return fail(CRSH_ELIMIT, "leaf_size * branching^(levels-1) > 2^22");
   const int world = std::max(1, o->shard_world), rank = o->shard_rank;
   if (rank < 0 || rank >= world) return fail(CRSH_EINVAL, "bad shard rank/world");
-  if ((o->flags & ~15u) != 0) return fail(CRSH_EINVAL, "unknown flags");
+  if ((o->flags & ~31u) != 0) return fail(CRSH_EINVAL, "unknown flags");
   if (!out_packed && (!out_hit || !out_t)) return fail(CRSH_EINVAL, "null output");
 
   FrameInfo fi;
@@ -368,6 +368,25 @@ crsh_status trace_impl(crsh_scene* sc, const crsh_primary_hits* h, const float* 
     std::memset(sc->h_counters, 0, 8 * MAX_SEG * CTR_STRIDE);
     CK(cudaMemsetAsync(counters, 0, 8, st));
     sc->fi = fi; sc->fi.valid = true;
+    return CRSH_OK;
+  }
+
+  if (o->flags & CRSH_F_BRUTE) {   // N x M baseline (NEXT-1): no hierarchy
+    for (int i = 2; i <= 7; ++i) CK(mark(i));
+    if (rank == 0) {
+      BruteArgs b{};
+      b.N = N; b.vals_c = sc->vals_c.as<uint32_t>(); b.rays = sc->rays.as<float4>(); b.tri_e = sc->tri_e.as<float4>();
+      b.M = sc->M; b.n_seg = fi.n_seg;
+      for (int s = 0; s <= fi.n_seg; ++s) b.seg_comp_start[s] = fi.seg_comp_start[s];
+      b.out_hit = out_hit; b.out_t = out_t; b.out_packed = out_packed; b.counters = counters;
+      k_brute<<<cdiv(N, 256), 256, 0, st>>>(b);
+      CK(cudaGetLastError());
+      ++sc->launches;
+    }
+    CK(mark(8));
+    CK(cudaMemcpyAsync(sc->h_counters, counters, 8 * MAX_SEG * CTR_STRIDE, cudaMemcpyDeviceToHost, st));
+    sc->fi = fi;
+    sc->fi.valid = true;
     return CRSH_OK;
   }
 

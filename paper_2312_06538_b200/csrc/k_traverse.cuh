@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(TRAV_THREADS) k_traverse(const TravArgs a, con
   const int Lv = a.Lv, K = a.K, logB0 = a.logB0;
   const int B = BT ? BT : a.B;
   const int logB = BT ? __builtin_ctz(BT) : a.logB;
-  const uint32_t Bm = (uint32_t)B - 1u, B0m = (uint32_t)a.B0 - 1u;
+  const uint32_t Bm = (uint32_t)B - 1u;
   const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
   const uint32_t lt = lanemask_lt();
   uint2* q = reinterpret_cast<uint2*>(smraw + L.off_q) + warp * L.q_warp;
@@ -600,6 +600,75 @@ __global__ void __launch_bounds__(TRAV_THREADS) k_traverse(const TravArgs a, con
   __syncthreads();
   for (uint32_t i = tid; i < MAX_SEG * CTR_STRIDE; i += TRAV_THREADS)
     if (s_ctr[i]) atomicAdd(a.counters + i, s_ctr[i]);
+}
+
+// ============================================================== brute force (N x M)
+struct BruteArgs {
+  uint32_t N;
+  const uint32_t* vals_c;       // compacted slot ids
+  const float4* rays;           // [slots][2]
+  const float4* tri_e;
+  int64_t M;
+  int32_t n_seg;
+  uint32_t seg_comp_start[MAX_SEG + 1];
+  int32_t* out_hit;
+  float* out_t;
+  unsigned long long* out_packed;
+  unsigned long long* counters;
+};
+
+// Naive ray tracing: one thread per ray, every triangle, staged 256 at
+// a time through shared memory (broadcast reads); closest hit with the same
+// (t, tri) order as the hierarchy path.
+__global__ void __launch_bounds__(256) k_brute(const BruteArgs a) {
+  __shared__ float4 s_tri[3 * 256];
+  __shared__ unsigned long long s_hit[MAX_SEG], s_tests[MAX_SEG];
+  if (threadIdx.x < MAX_SEG) { s_hit[threadIdx.x] = 0ull; s_tests[threadIdx.x] = 0ull; }
+  const uint32_t i = blockIdx.x * 256u + threadIdx.x;
+  const bool ok = i < a.N;
+  uint32_t slot = 0;
+  float4 r0 = make_float4(0.f, 0.f, 0.f, 1.f), r1 = make_float4(0.f, 0.f, 1.f, -1.f);
+  if (ok) {
+    slot = __ldg(a.vals_c + i);
+    r0 = __ldg(a.rays + 2 * (size_t)slot);
+    r1 = __ldg(a.rays + 2 * (size_t)slot + 1);
+  }
+  const f3 o = mk3(r0.x, r0.y, r0.z), d = mk3(r1.x, r1.y, r1.z);
+  unsigned long long best = BEST_NONE;
+  for (int64_t t0 = 0; t0 < a.M; t0 += 256) {
+    __syncthreads();
+    const int nt = (int)((a.M - t0) < 256 ? (a.M - t0) : 256);
+    for (int j = threadIdx.x; j < 3 * nt; j += 256) s_tri[j] = __ldg(a.tri_e + 3 * t0 + j);
+    __syncthreads();
+    if (ok) {
+      for (int k = 0; k < nt; ++k) {
+        const float4 v0 = s_tri[3 * k], e1 = s_tri[3 * k + 1], e2 = s_tri[3 * k + 2];
+        float th;
+        if (mt_ns(o, d, r0.w, r1.w, mk3(v0.x, v0.y, v0.z), mk3(e1.x, e1.y, e1.z), mk3(e2.x, e2.y, e2.z), &th)) {
+          const unsigned long long pk = pack_hit(th, (uint32_t)(t0 + k));
+          best = pk < best ? pk : best;
+        }
+      }
+    }
+  }
+  if (ok) {
+    int s = 0;
+    for (int q = 1; q < a.n_seg; ++q) s = (i >= a.seg_comp_start[q]) ? q : s;
+    const bool hit = best != BEST_NONE;
+    if (a.out_packed) {
+      a.out_packed[slot] = hit ? best : PACK_MISS;
+    } else {
+      a.out_hit[slot] = hit ? (int32_t)(uint32_t)(best & 0xFFFFFFFFull) : -1;
+      a.out_t[slot] = hit ? __uint_as_float((uint32_t)(best >> 32)) : __int_as_float(0x7f800000);
+    }
+    if (hit) atomicAdd(&s_hit[s], 1ull);
+    atomicAdd(&s_tests[s], (unsigned long long)a.M);
+  }
+  __syncthreads();
+  if (threadIdx.x < MAX_SEG) {
+    if (s_hit[threadIdx.x]) atomicAdd(a.counters + threadIdx.x * CTR_STRIDE + CTR_RAYS_HIT, s_hit[threadIdx.x]);
+    if (s_tests[threadIdx.x]) atomicAdd(a.counters + threadIdx.x * CTR_STRIDE + CTR_FINAL_TESTS, s_tests[threadIdx.x]);
+  }
 }
 
 // ============================================================== K9

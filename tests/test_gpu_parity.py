@@ -200,3 +200,20 @@ def test_host_variant_and_determinism():
     tr.run_host(np.ascontiguousarray(w.pos), np.ascontiguousarray(w.nrm), np.ascontiguousarray(w.mat),
                 np.ascontiguousarray(w.materials), hh, th)
     assert np.array_equal(hh, h1) and np.array_equal(th, t1)
+
+
+def test_brute_mode_equals_oracle_brute():
+    """CRSH_F_BRUTE (the N x M baseline) gives the oracle's brute-force
+    closest hits and counts rays x M final tests."""
+    for w in (make_workload(1), make_micro(9, n_tris=150, W=20, H=17, ray_types=7, n_lights=3)):
+        tr = tracer_for(w, flags=crsh.F_BRUTE)
+        tr.run()
+        hit, t = tr.results()
+        prep = oracle.ScenePrep(w.tris, w.mesh_ids)
+        rays, keys, empty = oracle.generate(w, prep)
+        ok = empty == 0
+        bt, btt = oracle.unpack(oracle.brute(rays[ok], prep))
+        assert np.array_equal(hit[ok], bt) and np.array_equal(t[ok].view(np.uint32), btt.view(np.uint32))
+        assert np.all(hit[~ok] == -2)
+        st = crsh.stats(tr.scene)
+        assert sum(st["final_tests"]) == int(ok.sum()) * w.M
