@@ -162,7 +162,7 @@ def run_crsh(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     flags = crsh.F_SORT | crsh.F_MESH_CULL | (crsh.F_ZORDER if args.zorder else 0)
     w = make_workload(args.config)
-    tr = tracer_for(w, device=local, flags=flags | crsh.F_STAGE_TIMING, shard_rank=rank, shard_world=world)
+    tr = tracer_for(w, device=local, flags=flags | crsh.F_KERNEL_TIMING, shard_rank=rank, shard_world=world)
     stream = torch.cuda.current_stream()
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device="cuda")
     packed = torch.empty(max(tr.slots, 1), dtype=torch.int64, device="cuda") if world > 1 else None
@@ -201,6 +201,22 @@ def run_crsh(args):
     ms = np.array([a.elapsed_time(b) for a, b in ev])
     total_ms = float(ms.sum())
     trav_ms = stage[6] / args.steps
+    # per-stage breakdown (diagnostic, outside the timed region): same frames with all stage events
+    trs = tracer_for(w, device=local, flags=flags | crsh.F_STAGE_TIMING, shard_rank=rank, shard_world=world)
+    stage = np.zeros(8)
+    n_diag = 3
+    for _ in range(n_diag + 1):
+        if world == 1:
+            trs.run(stream)
+        else:
+            trs.run_packed(packed, stream)
+            dist.all_reduce(packed, op=dist.ReduceOp.MIN)
+            trs.unpack(packed, stream)
+        s_ = trs.stats()
+        if _ > 0:
+            stage += np.asarray(s_["stage_ms"])
+    stage *= args.steps / n_diag
+    del trs
     st = tr.stats()
     # counters: traversal counters are per rank (sum); ray counts are global
     vec = torch.tensor([total_ms, trav_ms], dtype=torch.float64, device="cuda")

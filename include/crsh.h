@@ -56,8 +56,9 @@ enum {
   CRSH_F_MESH_CULL = 2u,
   CRSH_F_ZORDER = 4u,
   CRSH_F_STAGE_TIMING = 8u,
-  CRSH_F_BRUTE = 16u   /* naive N x M ray tracing: every ray
+  CRSH_F_BRUTE = 16u,  /* naive N x M ray tracing: every ray
                           against every triangle, no hierarchy; same outputs */
+  CRSH_F_KERNEL_TIMING = 32u /* time only the traversal kernel (stage_ms[6]) */
 };
 
 /* Build a scene (untimed preparation): copies the geometry, computes
@@ -138,9 +139,13 @@ int64_t crsh_num_slots(int32_t P, int32_t n_lights, uint32_t ray_types);
  *   ray_types   CRSH_SHADOW | CRSH_REFLECT | CRSH_REFRACT
  *   hit_tri     device [slots] int32 out: closest triangle, -1 miss, -2 no ray
  *   t           device [slots] float32 out: hit distance, +inf on miss / no ray
- *   stream      cudaStream_t (NULL = legacy default stream); work is enqueued
- *               on it. The call synchronises the stream twice (to read the
- *               ray and chunk counts) and returns with the traversal enqueued.
+ *   stream      cudaStream_t (NULL = legacy default stream). The call does not
+ *               synchronise: the whole frame is one CUDA graph (captured on the
+ *               first call with these arguments, replayed afterwards) that runs
+ *               on the scene's internal stream, ordered after the work already
+ *               on `stream` and before anything enqueued on `stream` later.
+ *               Data-dependent counts stay on the device (every grid is sized
+ *               from upper bounds). Set CRSH_NO_GRAPH=1 to launch directly.
  * Ties in t go to the smaller triangle index. */
 crsh_status crsh_trace_secondary(crsh_scene_t scene, const crsh_primary_hits* hits, const float* lights,
                                  int32_t n_lights, uint32_t ray_types, const crsh_opts* opts, int32_t* hit_tri,

@@ -20,7 +20,7 @@ LIB_PATH = os.environ.get("CRSH_LIB_PATH") or os.path.join(HERE, "libcrsh.so")  
 HEADER = os.path.join(os.path.dirname(HERE), "include", "crsh.h")
 
 SHADOW, REFLECT, REFRACT = 1, 2, 4
-F_SORT, F_MESH_CULL, F_ZORDER, F_STAGE_TIMING, F_BRUTE = 1, 2, 4, 8, 16
+F_SORT, F_MESH_CULL, F_ZORDER, F_STAGE_TIMING, F_BRUTE, F_KERNEL_TIMING = 1, 2, 4, 8, 16, 32
 TAP_KEYS, TAP_VALS, TAP_CHUNK_KEYS, TAP_CHUNK_BASE, TAP_SORTED_KEYS, TAP_SORTED_SLOTS = 1, 2, 3, 4, 5, 6
 TAP_NODES, TAP_SORTED_RAYS, TAP_TRI_SPHERES, TAP_MESH_SPHERES, TAP_SCENE_CONSTS = 7, 8, 9, 10, 11
 STATUS = {0: "OK", 2: "EINVAL", 3: "EIO", 4: "ELIMIT", 5: "ENOMEM", 6: "ECUDA", 7: "ENCCL"}

@@ -12,6 +12,44 @@ namespace crsh {
 constexpr int MAX_SEG = 3;
 constexpr int MAX_LEVELS = 8;
 
+// ---------------------------------------------------------------- frame descriptor
+// Per-frame counts that only the GPU knows (rays after trimming, chunks, the
+// padded segment layout, level sizes, work items). Written by k_raygen /
+// k_frame_plan / k_rle / k_chunk_plan / k_plan and read by every later kernel,
+// so the host never waits for them: all grids are sized from static upper
+// bounds and surplus blocks exit, and the whole frame is one CUDA graph.
+struct FrameDesc {
+  uint32_t N;                          // non-empty rays (all segments)
+  uint32_t seg_comp_start[MAX_SEG + 1];// compacted start of each segment; [n_seg] = N
+  uint32_t seg_n[MAX_SEG];
+  uint32_t seg_pad_base[MAX_SEG + 1];  // padded sorted-ray base (multiple of the group span); [n_seg] = Np
+  uint32_t Np, G;                      // padded rays, traversal groups
+  uint32_t C;                          // chunks
+  uint32_t seg_chunk_start[MAX_SEG + 1];
+  uint32_t seg_C[MAX_SEG];
+  uint32_t sort_tile_start[MAX_SEG + 1];
+  uint32_t n_items;                    // traversal work items
+  uint32_t level_n[MAX_LEVELS + 1];    // padded nodes at level k
+};
+
+// k_frame_plan: padded layout from the segment counts (one warp).
+__global__ void k_frame_plan(FrameDesc* fd, int n_seg, uint32_t GR, uint32_t B0, uint32_t B, int Lv) {
+  if (threadIdx.x != 0) return;
+  uint32_t base = 0;
+  for (int s = 0; s < n_seg; ++s) {
+    const uint32_t n = fd->seg_comp_start[s + 1] - fd->seg_comp_start[s];
+    fd->seg_n[s] = n;
+    fd->seg_pad_base[s] = base;
+    base += (n + GR - 1) / GR * GR;
+  }
+  fd->seg_pad_base[n_seg] = base;
+  fd->N = fd->seg_comp_start[n_seg];
+  fd->Np = base;
+  fd->G = base / GR;
+  uint32_t per = B0;
+  for (int k = 1; k <= Lv; ++k) { fd->level_n[k] = base / per; per *= B; }
+}
+
 // ---------------------------------------------------------------- scan tiles
 // 256 threads x 8 items, striped (item i of thread t = tile_base + i*256 + t):
 // coalesced loads, and the (item, warp) lexicographic order equals slot order.

@@ -173,24 +173,25 @@ void mesh_sphere(const float* tris, int64_t t0, int64_t t1, float pad, float out
 }  // namespace
 
 // ============================================================== scene
+// Static (host-known) plan of a frame: slot layout, hierarchy shape and the
+// upper bounds every grid and buffer is sized from. The data-dependent counts
+// live in the device FrameDesc; `fd` below is its host copy after the frame.
 struct FrameInfo {
   bool valid = false;
   int n_seg = 0;
   int seg_type[MAX_SEG] = {0, 0, 0};
-  uint32_t slots = 0, N = 0, C = 0, Np = 0, G = 0;
+  uint64_t S = 0;
   uint32_t seg_slot_start[MAX_SEG + 1] = {0};
-  uint32_t seg_comp_start[MAX_SEG + 1] = {0};
-  uint32_t seg_n[MAX_SEG] = {0};
-  uint32_t seg_chunk_start[MAX_SEG + 1] = {0};
-  uint32_t seg_C[MAX_SEG] = {0};
-  uint32_t seg_pad_base[MAX_SEG + 1] = {0};
   int Lv = 0, B0 = 0, B = 0, K = 0;
   uint32_t span = 0, GR = 0;
-  bool sorted = false;
-  size_t level_off[MAX_LEVELS + 1] = {0};   // node offset (in nodes) of level k in the node arrays
-  uint32_t level_n[MAX_LEVELS + 1] = {0};   // padded nodes at level k
-  float stage_ms[8] = {0};
-  bool timed = false;
+  uint64_t Np_max = 0, G_max = 0;
+  size_t level_off[MAX_LEVELS + 1] = {0};   // node offset of level k in the node arrays (from the bounds)
+  uint64_t level_max[MAX_LEVELS + 1] = {0};
+  uint32_t flags = 0;
+  int rank = 0, world = 1;
+  bool sorted = false, timed = false, ktimed = false, brute = false;
+  FrameDesc fd{};                           // host copy of the device counts (refreshed lazily)
+  bool fd_fresh = false;
 };
 
 struct crsh_scene {
@@ -200,36 +201,50 @@ struct crsh_scene {
   float box_min[3], box_max[3], box_ext[3], pad = 0, eps_t = 0;
   Buf tri_e, tri_sph, mesh_sph, mesh_first, mesh_count;
   std::vector<float> h_mesh_sph;
-  // per-frame arena
+  // per-frame arena (grow-only; `gen` counts reallocations, which invalidate the graph)
   Buf rays, keys_c, vals_c, ckey, cbase, k1, v1, k2, v2, pos, first_chunk, sorted_key, sorted_slot, sorted_rays,
-      nodes, trav, masks, items, best, zero, small, packed_tmp, stage_in, stage_out;
+      nodes, trav, masks, items, best, zero, stage_in, stage_out;
+  uint64_t gen = 0;
   unsigned long long* h_counters = nullptr;   // pinned
-  uint32_t* h_small = nullptr;                 // pinned
+  FrameDesc* h_fd = nullptr;                   // pinned
   FrameInfo fi;
   int64_t launches = 0;
   cudaStream_t last_stream = nullptr;
+  cudaStream_t gstream = nullptr;              // non-blocking stream the frame graph runs on
   cudaEvent_t ev[10] = {nullptr};
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  std::vector<unsigned char> gkey;
+  int64_t graph_launches = 0;                  // kernels inside the cached graph
   int sm_count = 148;
 };
 
 namespace {
 
-// zero region layout (bytes), sized by the slot bound
+cudaError_t grow(crsh_scene* sc, Buf& b, size_t bytes) {
+  if (bytes <= b.cap && b.p) return cudaSuccess;
+  ++sc->gen;
+  return ensure(b, bytes);
+}
+
+// zero region layout (bytes), sized by the slot bound; reset at every frame
 struct ZeroLayout {
-  size_t counters, tickets, hist, st_rg, st_rle, st_scan, st_plan, st_radix, radix_tiles_cap, total;
-  static ZeroLayout make(uint64_t S) {
+  size_t fd, counters, tickets, hist, st_rg, st_rle, st_scan, st_plan, st_radix, radix_tiles_cap, total;
+  static ZeroLayout make(uint64_t S, uint64_t G_max) {
     ZeroLayout z;
     size_t o = 0;
     auto take = [&](size_t b) { size_t r = o; o += (b + 255) & ~size_t(255); return r; };
     const uint64_t scan_tiles = cdiv(std::max<uint64_t>(S, 1), SCAN_TILE) + 1;
+    const uint64_t plan_tiles = cdiv(std::max<uint64_t>(G_max, 1), SCAN_TILE) + 1;
     z.radix_tiles_cap = cdiv(std::max<uint64_t>(S, 1), SORT_TILE) + MAX_SEG + 1;
+    z.fd = take(sizeof(FrameDesc));
     z.counters = take(8 * MAX_SEG * CTR_STRIDE);
     z.tickets = take(4 * 32);
     z.hist = take(4 * MAX_SEG * SORT_PASSES * RADIX_BINS);
     z.st_rg = take(8 * scan_tiles);
     z.st_rle = take(8 * scan_tiles);
     z.st_scan = take(8 * scan_tiles);
-    z.st_plan = take(8 * scan_tiles);
+    z.st_plan = take(8 * plan_tiles);
     z.st_radix = take(4 * SORT_PASSES * z.radix_tiles_cap * RADIX_BINS);
     z.total = o;
     return z;
@@ -266,6 +281,245 @@ cudaError_t dispatch_b(int B, F&& f) {
 
 constexpr uint32_t ITEM_TRIS = 2048;   // triangles per traversal work item (load balance)
 
+// Everything a frame's launch sequence depends on: if the key of a call equals
+// the cached one, the cached CUDA graph is replayed.
+struct CallKey {
+  const void *pos, *nrm, *mat, *materials, *out_hit, *out_t, *out_packed;
+  int32_t W, H, n_mat, n_lights;
+  float eye[3], lights[48];
+  uint32_t types;
+  crsh_opts o;
+  uint64_t gen;
+};
+
+// Enqueue one frame on `st` (directly or under graph capture). Returns the
+// number of kernels launched.
+crsh_status enqueue_frame(crsh_scene* sc, const FrameInfo& fi, const crsh_primary_hits* h, const float* lights,
+                          int32_t n_lights, int32_t* out_hit, float* out_t, unsigned long long* out_packed,
+                          cudaStream_t st, int64_t* n_launch) {
+  const uint64_t S = fi.S;
+  const int Lv = fi.Lv, B0 = fi.B0, B = fi.B;
+  const ZeroLayout Z = ZeroLayout::make(S, fi.G_max);
+  char* zb = sc->zero.as<char>();
+  FrameDesc* fd = reinterpret_cast<FrameDesc*>(zb + Z.fd);
+  unsigned long long* counters = reinterpret_cast<unsigned long long*>(zb + Z.counters);
+  uint32_t* tickets = reinterpret_cast<uint32_t*>(zb + Z.tickets);
+  int64_t nl = 0;
+  // stage marks (all with CRSH_F_STAGE_TIMING, only around k_traverse with
+  // CRSH_F_KERNEL_TIMING); under capture they must be external record nodes
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  CK(cudaStreamIsCapturing(st, &cap));
+  auto mark = [&](int i) -> cudaError_t {
+    if (!(fi.timed || (fi.ktimed && (i == 6 || i == 7)))) return cudaSuccess;
+    return cap == cudaStreamCaptureStatusActive ? cudaEventRecordWithFlags(sc->ev[i], st, cudaEventRecordExternal)
+                                                : cudaEventRecord(sc->ev[i], st);
+  };
+  CK(cudaMemsetAsync(sc->zero.p, 0, Z.total, st));
+  CK(mark(0));
+
+  // ---------------------------------------------------------------- K1: generate + hash + trim
+  {
+    RaygenArgs a{};
+    a.P = h->width * h->height; a.pos = h->pos; a.nrm = h->nrm; a.mat = h->mat; a.materials = h->materials;
+    a.n_mat = h->n_mat;
+    for (int i = 0; i < 3; ++i) a.eye[i] = h->eye[i];
+    for (int i = 0; i < 3 * n_lights; ++i) a.lights[i] = lights[i];
+    a.n_lights = n_lights; a.zorder = (fi.flags & CRSH_F_ZORDER) ? 1 : 0;
+    for (int i = 0; i < 3; ++i) { a.box_min[i] = sc->box_min[i]; a.box_ext[i] = sc->box_ext[i]; }
+    a.eps_t = sc->eps_t; a.n_slots = (uint32_t)S; a.n_seg = fi.n_seg;
+    for (int s = 0; s < fi.n_seg; ++s) a.seg_type[s] = fi.seg_type[s];
+    for (int s = 0; s <= fi.n_seg; ++s) a.seg_slot_start[s] = fi.seg_slot_start[s];
+    a.rays = sc->rays.as<float4>(); a.keys_c = sc->keys_c.as<uint32_t>(); a.vals_c = sc->vals_c.as<uint32_t>();
+    a.out_hit = out_packed ? nullptr : out_hit; a.out_t = out_packed ? nullptr : out_t; a.out_packed = out_packed;
+    a.status = reinterpret_cast<unsigned long long*>(zb + Z.st_rg); a.ticket = tickets + T_RG;
+    a.fd = fd;
+    k_raygen<<<cdiv(S, SCAN_TILE), SCAN_THREADS, 0, st>>>(a);
+    CK(cudaGetLastError());
+    k_frame_plan<<<1, 32, 0, st>>>(fd, fi.n_seg, fi.GR, (uint32_t)B0, (uint32_t)B, Lv);
+    CK(cudaGetLastError());
+    nl += 2;
+  }
+  CK(mark(1));
+
+  if (fi.brute) {   // N x M baseline (NEXT-1): no hierarchy
+    for (int i = 2; i <= 7; ++i) CK(mark(i));
+    if (fi.rank == 0) {
+      BruteArgs b{};
+      b.fd = fd; b.vals_c = sc->vals_c.as<uint32_t>(); b.rays = sc->rays.as<float4>(); b.tri_e = sc->tri_e.as<float4>();
+      b.M = sc->M; b.n_seg = fi.n_seg;
+      b.out_hit = out_hit; b.out_t = out_t; b.out_packed = out_packed; b.counters = counters;
+      k_brute<<<cdiv(S, 256), 256, 0, st>>>(b);
+      CK(cudaGetLastError());
+      ++nl;
+    }
+  } else {
+    // ---------------------------------------------------------------- K2-K4: compress, sort, decompress
+    if (fi.sorted) {
+      {
+        RleArgs a{};
+        a.fd = fd; a.keys = sc->keys_c.as<uint32_t>(); a.n_seg = fi.n_seg;
+        a.ckey = sc->ckey.as<uint32_t>(); a.cbase = sc->cbase.as<uint32_t>();
+        a.status = reinterpret_cast<unsigned long long*>(zb + Z.st_rle); a.ticket = tickets + T_RLE;
+        k_rle<<<cdiv(S, SCAN_TILE), SCAN_THREADS, 0, st>>>(a);
+        CK(cudaGetLastError());
+        k_chunk_plan<<<1, 32, 0, st>>>(fd, fi.n_seg, (uint32_t)SORT_TILE);
+        CK(cudaGetLastError());
+        nl += 2;
+      }
+      CK(mark(2));
+      uint32_t* hist = reinterpret_cast<uint32_t*>(zb + Z.hist);
+      k_radix_hist<<<std::min<uint32_t>(cdiv(S, 256 * 8), 4 * sc->sm_count), 256, 0, st>>>(fd, fi.n_seg,
+                                                                                           sc->ckey.as<uint32_t>(), hist);
+      CK(cudaGetLastError());
+      ++nl;
+      const size_t sm_bytes = (2 * SORT_TILE + SORT_WARPS * RADIX_BINS) * 4;
+      const uint32_t* kin = sc->ckey.as<uint32_t>();
+      const uint32_t* vin = nullptr;
+      for (int p = 0; p < SORT_PASSES; ++p) {
+        SortPassArgs a{};
+        a.fd = fd; a.n_seg = fi.n_seg; a.pass = p; a.keys_in = kin; a.vals_in = vin;
+        a.keys_out = (p & 1) ? sc->k2.as<uint32_t>() : sc->k1.as<uint32_t>();
+        a.vals_out = (p & 1) ? sc->v2.as<uint32_t>() : sc->v1.as<uint32_t>();
+        a.hist = hist;
+        a.status = reinterpret_cast<uint32_t*>(zb + Z.st_radix) + (size_t)p * Z.radix_tiles_cap * RADIX_BINS;
+        a.ticket = tickets + T_RADIX + p;
+        k_onesweep<<<(uint32_t)Z.radix_tiles_cap, SORT_THREADS, sm_bytes, st>>>(a);
+        CK(cudaGetLastError());
+        ++nl;
+        kin = a.keys_out; vin = a.vals_out;
+      }
+      CK(mark(3));
+      {
+        ScanSizeArgs a{};
+        a.fd = fd; a.sorted_cidx = sc->v2.as<uint32_t>(); a.cbase = sc->cbase.as<uint32_t>();
+        a.pos = sc->pos.as<uint32_t>(); a.first_chunk = sc->first_chunk.as<uint32_t>();
+        a.status = reinterpret_cast<unsigned long long*>(zb + Z.st_scan); a.ticket = tickets + T_SCAN;
+        k_scan_sizes<<<cdiv(S, SCAN_TILE), SCAN_THREADS, 0, st>>>(a);
+        CK(cudaGetLastError());
+        ++nl;
+      }
+      {
+        ExpandArgs a{};
+        a.fd = fd; a.pos = sc->pos.as<uint32_t>(); a.first_chunk = sc->first_chunk.as<uint32_t>();
+        a.skey = sc->k2.as<uint32_t>(); a.scidx = sc->v2.as<uint32_t>(); a.cbase = sc->cbase.as<uint32_t>();
+        a.vals_c = sc->vals_c.as<uint32_t>(); a.n_seg = fi.n_seg;
+        a.sorted_key = sc->sorted_key.as<uint32_t>(); a.sorted_slot = sc->sorted_slot.as<uint32_t>();
+        k_expand<<<cdiv(S, EXP_TILE), 256, 0, st>>>(a);
+        CK(cudaGetLastError());
+        ++nl;
+      }
+    } else {
+      CK(mark(2));
+      CK(mark(3));
+      ExpandArgs a{};
+      a.fd = fd; a.skey = sc->keys_c.as<uint32_t>(); a.vals_c = sc->vals_c.as<uint32_t>(); a.n_seg = fi.n_seg;
+      a.sorted_key = sc->sorted_key.as<uint32_t>(); a.sorted_slot = sc->sorted_slot.as<uint32_t>();
+      k_copy_unsorted<<<std::min<uint32_t>(cdiv(S, 256), 8 * sc->sm_count), 256, 0, st>>>(a);
+      CK(cudaGetLastError());
+      ++nl;
+    }
+    CK(mark(4));
+
+    // ---------------------------------------------------------------- K5-K6: hierarchy build
+    float4* nodes = sc->nodes.as<float4>();
+    float4* trav = sc->trav.as<float4>();
+    {
+      LeafArgs a{};
+      a.fd = fd; a.n_seg = fi.n_seg;
+      a.sorted_slot = sc->sorted_slot.as<uint32_t>(); a.rays = sc->rays.as<float4>();
+      a.sorted_rays = sc->sorted_rays.as<float4>(); a.nodes = nodes; a.trav = trav;
+      const uint32_t grid = cdiv(std::max<uint64_t>(fi.level_max[1], 1), 128);
+      CK(dispatch_b0(B0, [&](auto b0) {
+        k_leaves<decltype(b0)::value><<<grid, 128, 0, st>>>(a);
+        return cudaGetLastError();
+      }));
+      ++nl;
+    }
+    for (int k = 2; k <= Lv; ++k) {
+      UpperArgs a{};
+      a.fd = fd; a.level = k;
+      a.child_nodes = nodes + 2 * fi.level_off[k - 1];
+      a.nodes = nodes + 2 * fi.level_off[k];
+      a.trav = trav + 3 * fi.level_off[k];
+      const uint32_t grid = cdiv(std::max<uint64_t>(fi.level_max[k], 1), 128);
+      CK(dispatch_b(B, [&](auto b) {
+        k_upper<decltype(b)::value><<<grid, 128, 0, st>>>(a);
+        return cudaGetLastError();
+      }));
+      ++nl;
+    }
+    CK(mark(5));
+
+    // ---------------------------------------------------------------- K7-K9: traversal
+    const int W = (sc->n_meshes + 31) / 32;
+    CK(cudaMemsetAsync(sc->best.p, 0xFF, 8 * (size_t)fi.Np_max, st));
+    {
+      CullArgs a{};
+      a.fd = fd; a.K = fi.K; a.rank = fi.rank; a.world = fi.world; a.span = fi.span; a.W = W;
+      a.trav_top = trav + 3 * fi.level_off[Lv];
+      a.n_meshes = sc->n_meshes; a.mesh_sph = sc->mesh_sph.as<float4>(); a.mesh_count = sc->mesh_count.as<uint32_t>();
+      a.cull_on = (fi.flags & CRSH_F_MESH_CULL) ? 1 : 0;
+      a.masks = sc->masks.as<uint32_t>(); a.counters = counters; a.n_seg = fi.n_seg;
+      k_mesh_cull<<<cdiv(std::max<uint64_t>(fi.G_max * fi.K * W, 1), 256), 256, 0, st>>>(a);
+      CK(cudaGetLastError());
+      PlanArgs p{};
+      p.fd = fd; p.rank = fi.rank; p.world = fi.world;
+      p.K = fi.K; p.W = W; p.masks = sc->masks.as<uint32_t>();
+      p.n_meshes = sc->n_meshes; p.mesh_count = sc->mesh_count.as<uint32_t>(); p.item_tris = ITEM_TRIS;
+      p.items = sc->items.as<uint4>();
+      p.status = reinterpret_cast<unsigned long long*>(zb + Z.st_plan); p.ticket = tickets + T_PLAN;
+      k_plan<<<cdiv(std::max<uint64_t>(fi.G_max, 1), SCAN_TILE), SCAN_THREADS, 0, st>>>(p);
+      CK(cudaGetLastError());
+      nl += 2;
+    }
+    CK(mark(6));
+    {
+      TravArgs t{};
+      t.Lv = Lv; t.B0 = B0; t.B = B; t.K = fi.K; t.group_rays = fi.GR;
+      t.logB0 = __builtin_ctz((unsigned)B0); t.logB = __builtin_ctz((unsigned)B);
+      uint64_t per = 1;
+      for (int k = Lv; k >= 1; --k) { t.per_group[k] = (uint32_t)(fi.K * per); per *= B; }
+      for (int k = 1; k <= Lv; ++k) t.trav[k] = trav + 3 * fi.level_off[k];
+      t.sorted_rays = sc->sorted_rays.as<float4>(); t.tri_e = sc->tri_e.as<float4>();
+      t.tri_sph = sc->tri_sph.as<float4>();
+      t.masks = sc->masks.as<uint32_t>(); t.W = W; t.n_meshes = sc->n_meshes;
+      t.mesh_first = sc->mesh_first.as<uint32_t>(); t.mesh_count = sc->mesh_count.as<uint32_t>();
+      t.items = sc->items.as<uint4>(); t.fd = fd; t.ticket = tickets + T_TRAV;
+      t.best = sc->best.as<unsigned long long>(); t.counters = counters; t.n_seg = fi.n_seg;
+      const bool small = fi.GR <= SMALL_GROUP_RAYS;
+      const TravSmem L = TravSmem::make(fi.K, B, sc->n_meshes, Lv, small, t.per_group, fi.GR);
+      auto launch = [&](auto kern) -> cudaError_t {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
+        if (e != cudaSuccess) return e;
+        int per_sm = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TRAV_THREADS, L.total);
+        if (e != cudaSuccess) return e;
+        per_sm = std::max(1, per_sm);
+        kern<<<per_sm * sc->sm_count, TRAV_THREADS, L.total, st>>>(t, L);
+        return cudaGetLastError();
+      };
+      if (B == 8) CK(small ? launch(k_traverse<true, 8>) : launch(k_traverse<false, 8>));
+      else CK(small ? launch(k_traverse<true, 0>) : launch(k_traverse<false, 0>));
+      ++nl;
+    }
+    CK(mark(7));
+    {
+      UnpackArgs a{};
+      a.fd = fd; a.rank = fi.rank; a.world = fi.world; a.group_rays = fi.GR; a.n_seg = fi.n_seg;
+      a.sorted_slot = sc->sorted_slot.as<uint32_t>(); a.best = sc->best.as<unsigned long long>();
+      a.out_hit = out_hit; a.out_t = out_t; a.out_packed = out_packed; a.counters = counters;
+      k_unpack<<<cdiv(std::max<uint64_t>(fi.Np_max, 1), 256), 256, 0, st>>>(a);
+      CK(cudaGetLastError());
+      ++nl;
+    }
+  }
+  CK(mark(8));
+  CK(cudaMemcpyAsync(sc->h_counters, counters, 8 * MAX_SEG * CTR_STRIDE, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(sc->h_fd, fd, sizeof(FrameDesc), cudaMemcpyDeviceToHost, st));
+  *n_launch = nl;
+  return CRSH_OK;
+}
+
 crsh_status trace_impl(crsh_scene* sc, const crsh_primary_hits* h, const float* lights, int32_t n_lights,
                        uint32_t types, const crsh_opts* o, int32_t* out_hit, float* out_t,
                        unsigned long long* out_packed, cudaStream_t st) {
@@ -288,18 +542,22 @@ crsh_status trace_impl(crsh_scene* sc, const crsh_primary_hits* h, const float* 
   if (span > (1ull << 22)) return fail(CRSH_ELIMIT, "leaf_size * branching^(levels-1) > 2^22");
   const int world = std::max(1, o->shard_world), rank = o->shard_rank;
   if (rank < 0 || rank >= world) return fail(CRSH_EINVAL, "bad shard rank/world");
-  if ((o->flags & ~31u) != 0) return fail(CRSH_EINVAL, "unknown flags");
+  if ((o->flags & ~63u) != 0) return fail(CRSH_EINVAL, "unknown flags");
   if (!out_packed && (!out_hit || !out_t)) return fail(CRSH_EINVAL, "null output");
 
+  // ---------------------------------------------------------------- static plan
   FrameInfo fi;
   fi.Lv = Lv; fi.B0 = B0; fi.B = B;
   fi.span = (uint32_t)span;
   fi.K = span >= 512 ? 1 : (int)std::min<uint64_t>(32, 512 / span);
   fi.GR = fi.K * fi.span;
+  fi.flags = o->flags;
   fi.sorted = (o->flags & CRSH_F_SORT) != 0;
   fi.timed = (o->flags & CRSH_F_STAGE_TIMING) != 0;
+  fi.ktimed = (o->flags & CRSH_F_KERNEL_TIMING) != 0;
+  fi.brute = (o->flags & CRSH_F_BRUTE) != 0;
+  fi.rank = rank; fi.world = world;
   uint64_t S = 0;
-  fi.n_seg = 0;
   const int type_bits[3] = {1, 2, 4};
   for (int t = 0; t < 3; ++t) {
     if (!(types & type_bits[t])) continue;
@@ -312,303 +570,111 @@ crsh_status trace_impl(crsh_scene* sc, const crsh_primary_hits* h, const float* 
   }
   if (S >= (1ull << 30)) return fail(CRSH_ELIMIT, "slots >= 2^30");
   fi.seg_slot_start[fi.n_seg] = (uint32_t)S;
-  fi.slots = (uint32_t)S;
-  CK(cudaSetDevice(sc->device));
-  sc->launches = 0;
-  sc->last_stream = st;
-  sc->fi.valid = false;
-  if (S == 0) { sc->fi = fi; sc->fi.valid = true; std::memset(sc->h_counters, 0, 8 * MAX_SEG * CTR_STRIDE); return CRSH_OK; }
-  auto mark = [&](int i) -> cudaError_t { return fi.timed ? cudaEventRecord(sc->ev[i], st) : cudaSuccess; };
-
-  // ---------------------------------------------------------------- buffers (slot-bound)
-  const ZeroLayout Z = ZeroLayout::make(S);
-  CK(ensure(sc->zero, Z.total));
-  CK(ensure(sc->small, 256));
-  CK(ensure(sc->rays, 32 * S));
-  CK(ensure(sc->keys_c, 4 * S));
-  CK(ensure(sc->vals_c, 4 * S));
-  CK(cudaMemsetAsync(sc->zero.p, 0, Z.total, st));
-  char* zb = sc->zero.as<char>();
-  unsigned long long* counters = reinterpret_cast<unsigned long long*>(zb + Z.counters);
-  uint32_t* tickets = reinterpret_cast<uint32_t*>(zb + Z.tickets);
-  uint32_t* d_small = sc->small.as<uint32_t>();   // [0..3] comp starts, [4..7] chunk starts, [8] n_items
-  CK(mark(0));
-
-  // ---------------------------------------------------------------- K1: generate + hash + trim
+  fi.S = S;
+  fi.Np_max = roundup(S + (uint64_t)fi.n_seg * fi.GR, fi.GR);
+  fi.G_max = fi.Np_max / fi.GR;
   {
-    RaygenArgs a{};
-    a.P = P; a.pos = h->pos; a.nrm = h->nrm; a.mat = h->mat; a.materials = h->materials; a.n_mat = h->n_mat;
-    for (int i = 0; i < 3; ++i) a.eye[i] = h->eye[i];
-    for (int i = 0; i < 3 * n_lights; ++i) a.lights[i] = lights[i];
-    a.n_lights = n_lights; a.zorder = (o->flags & CRSH_F_ZORDER) ? 1 : 0;
-    for (int i = 0; i < 3; ++i) { a.box_min[i] = sc->box_min[i]; a.box_ext[i] = sc->box_ext[i]; }
-    a.eps_t = sc->eps_t; a.n_slots = (uint32_t)S; a.n_seg = fi.n_seg;
-    for (int s = 0; s < fi.n_seg; ++s) a.seg_type[s] = fi.seg_type[s];
-    for (int s = 0; s <= fi.n_seg; ++s) a.seg_slot_start[s] = fi.seg_slot_start[s];
-    a.rays = sc->rays.as<float4>(); a.keys_c = sc->keys_c.as<uint32_t>(); a.vals_c = sc->vals_c.as<uint32_t>();
-    a.out_hit = out_packed ? nullptr : out_hit; a.out_t = out_packed ? nullptr : out_t; a.out_packed = out_packed;
-    a.status = reinterpret_cast<unsigned long long*>(zb + Z.st_rg); a.ticket = tickets + T_RG;
-    a.seg_comp_start = d_small;
-    k_raygen<<<cdiv(S, SCAN_TILE), SCAN_THREADS, 0, st>>>(a);
-    CK(cudaGetLastError());
-    ++sc->launches;
-  }
-  CK(cudaMemcpyAsync(sc->h_small, d_small, 4 * (MAX_SEG + 1), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  for (int s = 0; s <= fi.n_seg; ++s) fi.seg_comp_start[s] = sc->h_small[s];
-  fi.N = fi.seg_comp_start[fi.n_seg];
-  for (int s = 0; s < fi.n_seg; ++s) fi.seg_n[s] = fi.seg_comp_start[s + 1] - fi.seg_comp_start[s];
-  fi.seg_pad_base[0] = 0;
-  for (int s = 0; s < fi.n_seg; ++s) fi.seg_pad_base[s + 1] = (uint32_t)(fi.seg_pad_base[s] + roundup(fi.seg_n[s], fi.GR));
-  fi.Np = fi.seg_pad_base[fi.n_seg];
-  fi.G = fi.Np / fi.GR;
-  CK(mark(1));
-  const uint32_t N = fi.N;
-  if (N == 0) {
-    std::memset(sc->h_counters, 0, 8 * MAX_SEG * CTR_STRIDE);
-    CK(cudaMemsetAsync(counters, 0, 8, st));
-    sc->fi = fi; sc->fi.valid = true;
-    return CRSH_OK;
-  }
-
-  if (o->flags & CRSH_F_BRUTE) {   // N x M baseline (NEXT-1): no hierarchy
-    for (int i = 2; i <= 7; ++i) CK(mark(i));
-    if (rank == 0) {
-      BruteArgs b{};
-      b.N = N; b.vals_c = sc->vals_c.as<uint32_t>(); b.rays = sc->rays.as<float4>(); b.tri_e = sc->tri_e.as<float4>();
-      b.M = sc->M; b.n_seg = fi.n_seg;
-      for (int s = 0; s <= fi.n_seg; ++s) b.seg_comp_start[s] = fi.seg_comp_start[s];
-      b.out_hit = out_hit; b.out_t = out_t; b.out_packed = out_packed; b.counters = counters;
-      k_brute<<<cdiv(N, 256), 256, 0, st>>>(b);
-      CK(cudaGetLastError());
-      ++sc->launches;
+    size_t off = 0;
+    uint64_t per = B0;
+    for (int k = 1; k <= Lv; ++k) {
+      fi.level_off[k] = off;
+      fi.level_max[k] = fi.Np_max / per;
+      off += fi.level_max[k];
+      per *= B;
     }
-    CK(mark(8));
-    CK(cudaMemcpyAsync(sc->h_counters, counters, 8 * MAX_SEG * CTR_STRIDE, cudaMemcpyDeviceToHost, st));
-    sc->fi = fi;
+  }
+  CK(cudaSetDevice(sc->device));
+  sc->last_stream = st;
+  sc->fi = fi;
+  sc->fi.valid = false;
+  if (S == 0) {
+    std::memset(sc->h_counters, 0, 8 * MAX_SEG * CTR_STRIDE);
+    std::memset(sc->h_fd, 0, sizeof(FrameDesc));
+    sc->launches = 0;
     sc->fi.valid = true;
     return CRSH_OK;
   }
 
-  // ---------------------------------------------------------------- K2-K4: compress, sort, decompress
-  CK(ensure(sc->sorted_key, 4 * (size_t)fi.Np));
-  CK(ensure(sc->sorted_slot, 4 * (size_t)fi.Np));
-  if (fi.sorted) {
-    CK(ensure(sc->ckey, 4 * (size_t)N));
-    CK(ensure(sc->cbase, 4 * (size_t)(N + 1)));
-    {
-      RleArgs a{};
-      a.N = N; a.keys = sc->keys_c.as<uint32_t>(); a.n_seg = fi.n_seg;
-      for (int s = 0; s <= fi.n_seg; ++s) a.seg_comp_start[s] = fi.seg_comp_start[s];
-      a.ckey = sc->ckey.as<uint32_t>(); a.cbase = sc->cbase.as<uint32_t>(); a.seg_chunk_start = d_small + 4;
-      a.status = reinterpret_cast<unsigned long long*>(zb + Z.st_rle); a.ticket = tickets + T_RLE;
-      k_rle<<<cdiv(N, SCAN_TILE), SCAN_THREADS, 0, st>>>(a);
-      CK(cudaGetLastError());
-      ++sc->launches;
-    }
-    CK(cudaMemcpyAsync(sc->h_small + 4, d_small + 4, 4 * (MAX_SEG + 1), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    for (int s = 0; s <= fi.n_seg; ++s) fi.seg_chunk_start[s] = sc->h_small[4 + s];
-    fi.C = fi.seg_chunk_start[fi.n_seg];
-    for (int s = 0; s < fi.n_seg; ++s) fi.seg_C[s] = fi.seg_n[s] ? fi.seg_chunk_start[s + 1] - fi.seg_chunk_start[s] : 0;
-    CK(mark(2));
-    const uint32_t C = fi.C;
-    CK(ensure(sc->k1, 4 * (size_t)C)); CK(ensure(sc->v1, 4 * (size_t)C));
-    CK(ensure(sc->k2, 4 * (size_t)C)); CK(ensure(sc->v2, 4 * (size_t)C));
-    SegChunks scn{};
-    scn.n_seg = fi.n_seg;
-    uint32_t tiles = 0;
-    for (int s = 0; s < fi.n_seg; ++s) {
-      scn.start[s] = fi.seg_chunk_start[s];
-      scn.count[s] = fi.seg_C[s];
-      scn.tile_start[s] = tiles;
-      tiles += cdiv(fi.seg_C[s], SORT_TILE);
-    }
-    scn.start[fi.n_seg] = C;
-    scn.tile_start[fi.n_seg] = tiles;
-    uint32_t* hist = reinterpret_cast<uint32_t*>(zb + Z.hist);
-    k_radix_hist<<<std::min<uint32_t>(cdiv(C, 256 * 8), 4 * sc->sm_count), 256, 0, st>>>(scn, sc->ckey.as<uint32_t>(), C, hist);
-    CK(cudaGetLastError());
-    ++sc->launches;
-    const size_t sm_bytes = (2 * SORT_TILE + SORT_WARPS * RADIX_BINS) * 4;
-    const uint32_t* kin = sc->ckey.as<uint32_t>();
-    const uint32_t* vin = nullptr;
-    for (int p = 0; p < SORT_PASSES; ++p) {
-      SortPassArgs a{};
-      a.sc = scn; a.pass = p; a.keys_in = kin; a.vals_in = vin;
-      a.keys_out = (p & 1) ? sc->k2.as<uint32_t>() : sc->k1.as<uint32_t>();
-      a.vals_out = (p & 1) ? sc->v2.as<uint32_t>() : sc->v1.as<uint32_t>();
-      a.hist = hist;
-      a.status = reinterpret_cast<uint32_t*>(zb + Z.st_radix) + (size_t)p * Z.radix_tiles_cap * RADIX_BINS;
-      a.ticket = tickets + T_RADIX + p;
-      if (tiles) {
-        k_onesweep<<<tiles, SORT_THREADS, sm_bytes, st>>>(a);
-        CK(cudaGetLastError());
-        ++sc->launches;
-      }
-      kin = a.keys_out; vin = a.vals_out;
-    }
-    CK(mark(3));
-    // K4: decompression
-    CK(ensure(sc->pos, 4 * (size_t)(C + 1)));
-    CK(ensure(sc->first_chunk, 4 * (size_t)(cdiv(N, EXP_TILE) + 1)));
-    {
-      ScanSizeArgs a{};
-      a.C = C; a.N = N; a.sorted_cidx = sc->v2.as<uint32_t>(); a.cbase = sc->cbase.as<uint32_t>();
-      a.pos = sc->pos.as<uint32_t>(); a.first_chunk = sc->first_chunk.as<uint32_t>();
-      a.status = reinterpret_cast<unsigned long long*>(zb + Z.st_scan); a.ticket = tickets + T_SCAN;
-      k_scan_sizes<<<cdiv(C, SCAN_TILE), SCAN_THREADS, 0, st>>>(a);
-      CK(cudaGetLastError());
-      ++sc->launches;
-    }
-    {
-      ExpandArgs a{};
-      a.N = N; a.C = C; a.pos = sc->pos.as<uint32_t>(); a.first_chunk = sc->first_chunk.as<uint32_t>();
-      a.skey = sc->k2.as<uint32_t>(); a.scidx = sc->v2.as<uint32_t>(); a.cbase = sc->cbase.as<uint32_t>();
-      a.vals_c = sc->vals_c.as<uint32_t>(); a.n_seg = fi.n_seg;
-      for (int s = 0; s <= fi.n_seg; ++s) { a.seg_comp_start[s] = fi.seg_comp_start[s]; a.seg_pad_base[s] = fi.seg_pad_base[s]; }
-      a.sorted_key = sc->sorted_key.as<uint32_t>(); a.sorted_slot = sc->sorted_slot.as<uint32_t>();
-      k_expand<<<cdiv(N, EXP_TILE), 256, 0, st>>>(a);
-      CK(cudaGetLastError());
-      ++sc->launches;
-    }
-  } else {
-    CK(mark(2));
-    CK(mark(3));
-    ExpandArgs a{};
-    a.N = N; a.skey = sc->keys_c.as<uint32_t>(); a.vals_c = sc->vals_c.as<uint32_t>(); a.n_seg = fi.n_seg;
-    for (int s = 0; s <= fi.n_seg; ++s) { a.seg_comp_start[s] = fi.seg_comp_start[s]; a.seg_pad_base[s] = fi.seg_pad_base[s]; }
-    a.sorted_key = sc->sorted_key.as<uint32_t>(); a.sorted_slot = sc->sorted_slot.as<uint32_t>();
-    k_copy_unsorted<<<std::min<uint32_t>(cdiv(N, 256), 8 * sc->sm_count), 256, 0, st>>>(a);
-    CK(cudaGetLastError());
-    ++sc->launches;
-  }
-  CK(mark(4));
-
-  // ---------------------------------------------------------------- K5-K6: hierarchy build
+  // ---------------------------------------------------------------- buffers (upper bounds)
+  const ZeroLayout Z = ZeroLayout::make(S, fi.G_max);
   size_t total_nodes = 0;
-  {
-    uint64_t per = B0;
-    for (int k = 1; k <= Lv; ++k) {
-      fi.level_off[k] = total_nodes;
-      fi.level_n[k] = (uint32_t)(fi.Np / per);
-      total_nodes += fi.level_n[k];
-      per *= B;
-    }
-  }
-  CK(ensure(sc->sorted_rays, 32 * (size_t)fi.Np));
-  CK(ensure(sc->nodes, 32 * total_nodes));
-  CK(ensure(sc->trav, 48 * total_nodes));
-  float4* nodes = sc->nodes.as<float4>();
-  float4* trav = sc->trav.as<float4>();
-  {
-    LeafArgs a{};
-    a.n_leaves = fi.level_n[1]; a.n_seg = fi.n_seg;
-    for (int s = 0; s <= fi.n_seg; ++s) a.seg_pad_base[s] = fi.seg_pad_base[s];
-    for (int s = 0; s < fi.n_seg; ++s) a.seg_n[s] = fi.seg_n[s];
-    a.sorted_slot = sc->sorted_slot.as<uint32_t>(); a.rays = sc->rays.as<float4>();
-    a.sorted_rays = sc->sorted_rays.as<float4>(); a.nodes = nodes; a.trav = trav;
-    CK(dispatch_b0(B0, [&](auto b0) {
-      k_leaves<decltype(b0)::value><<<cdiv(a.n_leaves, 128), 128, 0, st>>>(a);
-      return cudaGetLastError();
-    }));
-    ++sc->launches;
-  }
-  for (int k = 2; k <= Lv; ++k) {
-    UpperArgs a{};
-    a.n_nodes = fi.level_n[k];
-    a.child_nodes = nodes + 2 * fi.level_off[k - 1];
-    a.nodes = nodes + 2 * fi.level_off[k];
-    a.trav = trav + 3 * fi.level_off[k];
-    CK(dispatch_b(B, [&](auto b) {
-      k_upper<decltype(b)::value><<<cdiv(a.n_nodes, 128), 128, 0, st>>>(a);
-      return cudaGetLastError();
-    }));
-    ++sc->launches;
-  }
-  CK(mark(5));
-
-  // ---------------------------------------------------------------- K7-K9: traversal
+  for (int k = 1; k <= Lv; ++k) total_nodes += fi.level_max[k];
   const int W = (sc->n_meshes + 31) / 32;
-  const uint32_t g_lo = (uint32_t)((uint64_t)fi.G * rank / world), g_hi = (uint32_t)((uint64_t)fi.G * (rank + 1) / world);
-  const uint32_t n_top = fi.level_n[Lv];
-  CK(ensure(sc->masks, 4 * (size_t)n_top * W + 4));
-  CK(ensure(sc->best, 8 * (size_t)fi.Np));
-  const uint64_t items_cap = (uint64_t)std::max<uint32_t>(g_hi - g_lo, 1) * cdiv(std::max<int64_t>(sc->M, 1), ITEM_TRIS);
-  CK(ensure(sc->items, 16 * items_cap));
-  CK(cudaMemsetAsync(sc->best.p, 0xFF, 8 * (size_t)fi.Np, st));
-  uint32_t seg_group_start[MAX_SEG + 1], seg_top_start[MAX_SEG + 1];
-  for (int s = 0; s <= fi.n_seg; ++s) {
-    seg_group_start[s] = fi.seg_pad_base[s] / fi.GR;
-    seg_top_start[s] = fi.seg_pad_base[s] / fi.span;
+  const uint64_t items_cap = std::max<uint64_t>(fi.G_max, 1) * cdiv(std::max<int64_t>(sc->M, 1), ITEM_TRIS);
+  CK(grow(sc, sc->zero, Z.total));
+  CK(grow(sc, sc->rays, 32 * S));
+  CK(grow(sc, sc->keys_c, 4 * S));
+  CK(grow(sc, sc->vals_c, 4 * S));
+  if (!fi.brute) {
+    CK(grow(sc, sc->ckey, 4 * S));
+    CK(grow(sc, sc->cbase, 4 * (S + 1)));
+    CK(grow(sc, sc->k1, 4 * S)); CK(grow(sc, sc->v1, 4 * S));
+    CK(grow(sc, sc->k2, 4 * S)); CK(grow(sc, sc->v2, 4 * S));
+    CK(grow(sc, sc->pos, 4 * (S + 1)));
+    CK(grow(sc, sc->first_chunk, 4 * ((size_t)cdiv(S, EXP_TILE) + 1)));
+    CK(grow(sc, sc->sorted_key, 4 * fi.Np_max));
+    CK(grow(sc, sc->sorted_slot, 4 * fi.Np_max));
+    CK(grow(sc, sc->sorted_rays, 32 * fi.Np_max));
+    CK(grow(sc, sc->nodes, 32 * total_nodes));
+    CK(grow(sc, sc->trav, 48 * total_nodes));
+    CK(grow(sc, sc->masks, 4 * (size_t)fi.G_max * fi.K * W + 4));
+    CK(grow(sc, sc->best, 8 * fi.Np_max));
+    CK(grow(sc, sc->items, 16 * items_cap));
   }
-  if (g_hi > g_lo) {
-    CullArgs a{};
-    a.top_lo = g_lo * fi.K; a.top_hi = g_hi * fi.K; a.W = W;
-    a.trav_top = trav + 3 * fi.level_off[Lv];
-    a.n_meshes = sc->n_meshes; a.mesh_sph = sc->mesh_sph.as<float4>(); a.mesh_count = sc->mesh_count.as<uint32_t>();
-    a.cull_on = (o->flags & CRSH_F_MESH_CULL) ? 1 : 0;
-    a.masks = sc->masks.as<uint32_t>(); a.counters = counters; a.n_seg = fi.n_seg;
-    for (int s = 0; s <= fi.n_seg; ++s) a.seg_top_start[s] = seg_top_start[s];
-    k_mesh_cull<<<cdiv((uint64_t)(a.top_hi - a.top_lo) * W, 256), 256, 0, st>>>(a);
-    CK(cudaGetLastError());
-    ++sc->launches;
-    PlanArgs p{};
-    p.g_lo = g_lo; p.g_hi = g_hi; p.K = fi.K; p.W = W; p.masks = sc->masks.as<uint32_t>();
-    p.n_meshes = sc->n_meshes; p.mesh_count = sc->mesh_count.as<uint32_t>(); p.item_tris = ITEM_TRIS;
-    p.items = sc->items.as<uint4>(); p.n_items = d_small + 8;
-    p.status = reinterpret_cast<unsigned long long*>(zb + Z.st_plan); p.ticket = tickets + T_PLAN;
-    k_plan<<<cdiv(g_hi - g_lo, SCAN_TILE), SCAN_THREADS, 0, st>>>(p);
-    CK(cudaGetLastError());
-    ++sc->launches;
-    CK(mark(6));
 
-    TravArgs t{};
-    t.Lv = Lv; t.B0 = B0; t.B = B; t.K = fi.K; t.group_rays = fi.GR;
-    t.logB0 = __builtin_ctz((unsigned)B0); t.logB = __builtin_ctz((unsigned)B);
-    uint64_t per = 1;
-    for (int k = Lv; k >= 1; --k) { t.per_group[k] = (uint32_t)(fi.K * per); per *= B; }
-    for (int k = 1; k <= Lv; ++k) t.trav[k] = trav + 3 * fi.level_off[k];
-    t.sorted_rays = sc->sorted_rays.as<float4>(); t.tri_e = sc->tri_e.as<float4>(); t.tri_sph = sc->tri_sph.as<float4>();
-    t.masks = sc->masks.as<uint32_t>(); t.W = W; t.n_meshes = sc->n_meshes;
-    t.mesh_first = sc->mesh_first.as<uint32_t>(); t.mesh_count = sc->mesh_count.as<uint32_t>();
-    t.items = sc->items.as<uint4>(); t.n_items = d_small + 8; t.ticket = tickets + T_TRAV;
-    t.best = sc->best.as<unsigned long long>(); t.counters = counters; t.n_seg = fi.n_seg;
-    for (int s = 0; s <= fi.n_seg; ++s) t.seg_group_start[s] = seg_group_start[s];
-    const bool small = fi.GR <= SMALL_GROUP_RAYS;
-    const TravSmem L = TravSmem::make(fi.K, B, sc->n_meshes, Lv, small, t.per_group, fi.GR);
-    auto launch = [&](auto kern) -> cudaError_t {
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
-      if (e != cudaSuccess) return e;
-      int per_sm = 0;
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TRAV_THREADS, L.total);
-      if (e != cudaSuccess) return e;
-      per_sm = std::max(1, per_sm);
-      kern<<<per_sm * sc->sm_count, TRAV_THREADS, L.total, st>>>(t, L);
-      return cudaGetLastError();
-    };
-    if (B == 8) CK(small ? launch(k_traverse<true, 8>) : launch(k_traverse<false, 8>));
-    else CK(small ? launch(k_traverse<true, 0>) : launch(k_traverse<false, 0>));
-    ++sc->launches;
+  // ---------------------------------------------------------------- graph replay or capture
+  CallKey key{};
+  key.pos = h->pos; key.nrm = h->nrm; key.mat = h->mat; key.materials = h->materials;
+  key.out_hit = out_hit; key.out_t = out_t; key.out_packed = out_packed;
+  key.W = h->width; key.H = h->height; key.n_mat = h->n_mat; key.n_lights = n_lights;
+  for (int i = 0; i < 3; ++i) key.eye[i] = h->eye[i];
+  for (int i = 0; i < 3 * n_lights; ++i) key.lights[i] = lights[i];
+  key.types = types; key.o = *o; key.gen = sc->gen;
+  std::vector<unsigned char> kb(sizeof(CallKey));
+  std::memcpy(kb.data(), &key, sizeof(CallKey));
+  static const bool use_graph = !std::getenv("CRSH_NO_GRAPH");
+  if (!use_graph) {
+    int64_t nl = 0;
+    crsh_status rc = enqueue_frame(sc, fi, h, lights, n_lights, out_hit, out_t, out_packed, st, &nl);
+    if (rc != CRSH_OK) return rc;
+    sc->launches = nl;
   } else {
-    CK(mark(6));
+    if (!sc->gexec || kb != sc->gkey) {
+      if (sc->gexec) { cudaGraphExecDestroy(sc->gexec); sc->gexec = nullptr; }
+      CK(cudaStreamBeginCapture(sc->gstream, cudaStreamCaptureModeThreadLocal));
+      int64_t nl = 0;
+      crsh_status rc = enqueue_frame(sc, fi, h, lights, n_lights, out_hit, out_t, out_packed, sc->gstream, &nl);
+      cudaGraph_t g = nullptr;
+      cudaError_t e = cudaStreamEndCapture(sc->gstream, &g);
+      if (rc != CRSH_OK) { if (g) cudaGraphDestroy(g); return rc; }
+      CK(e);
+      e = cudaGraphInstantiate(&sc->gexec, g, 0);
+      cudaGraphDestroy(g);
+      CK(e);
+      sc->gkey = kb;
+      sc->graph_launches = nl;
+    }
+    CK(cudaEventRecord(sc->ev_in, st));
+    CK(cudaStreamWaitEvent(sc->gstream, sc->ev_in, 0));
+    CK(cudaGraphLaunch(sc->gexec, sc->gstream));
+    CK(cudaEventRecord(sc->ev_out, sc->gstream));
+    CK(cudaStreamWaitEvent(st, sc->ev_out, 0));
+    sc->launches = sc->graph_launches;
   }
-  CK(mark(7));
-  if (g_hi > g_lo) {
-    UnpackArgs a{};
-    a.r_lo = g_lo * fi.GR; a.r_hi = g_hi * fi.GR; a.n_seg = fi.n_seg;
-    for (int s = 0; s <= fi.n_seg; ++s) a.seg_pad_base[s] = fi.seg_pad_base[s];
-    for (int s = 0; s < fi.n_seg; ++s) a.seg_n[s] = fi.seg_n[s];
-    a.sorted_slot = sc->sorted_slot.as<uint32_t>(); a.best = sc->best.as<unsigned long long>();
-    a.out_hit = out_hit; a.out_t = out_t; a.out_packed = out_packed; a.counters = counters;
-    k_unpack<<<cdiv(a.r_hi - a.r_lo, 256), 256, 0, st>>>(a);
-    CK(cudaGetLastError());
-    ++sc->launches;
-  }
-  CK(mark(8));
-  CK(cudaMemcpyAsync(sc->h_counters, counters, 8 * MAX_SEG * CTR_STRIDE, cudaMemcpyDeviceToHost, st));
-  sc->fi = fi;
   sc->fi.valid = true;
+  sc->fi.fd_fresh = false;
+  return CRSH_OK;
+}
+
+// wait for the last frame and refresh the host copy of its FrameDesc
+crsh_status sync_frame(crsh_scene* sc) {
+  CK(cudaSetDevice(sc->device));
+  CK(cudaStreamSynchronize(sc->last_stream));
+  if (sc->gstream) CK(cudaStreamSynchronize(sc->gstream));
+  if (sc->fi.valid && !sc->fi.fd_fresh) {
+    sc->fi.fd = *sc->h_fd;
+    sc->fi.fd_fresh = true;
+  }
   return CRSH_OK;
 }
 
@@ -677,7 +743,10 @@ crsh_status crsh_scene_create(const float* tris, const int32_t* mesh_ids, int64_
   ck(ensure(sc->mesh_first, 4 * (size_t)n_meshes), "alloc mesh_first");
   ck(ensure(sc->mesh_count, 4 * (size_t)n_meshes), "alloc mesh_count");
   ck(cudaMallocHost(&sc->h_counters, 8 * MAX_SEG * CTR_STRIDE), "alloc pinned");
-  ck(cudaMallocHost(&sc->h_small, 64), "alloc pinned");
+  ck(cudaMallocHost(&sc->h_fd, sizeof(FrameDesc)), "alloc pinned");
+  ck(cudaStreamCreateWithFlags(&sc->gstream, cudaStreamNonBlocking), "graph stream");
+  ck(cudaEventCreateWithFlags(&sc->ev_in, cudaEventDisableTiming), "event");
+  ck(cudaEventCreateWithFlags(&sc->ev_out, cudaEventDisableTiming), "event");
   for (int i = 0; i < 10 && rc == CRSH_OK; ++i) ck(cudaEventCreate(&sc->ev[i]), "event");
   if (rc != CRSH_OK) return bail(rc);
   std::memset(sc->h_counters, 0, 8 * MAX_SEG * CTR_STRIDE);
@@ -709,10 +778,14 @@ void crsh_scene_destroy(crsh_scene_t sc) {
   Buf* bufs[] = {&sc->tri_e, &sc->tri_sph, &sc->mesh_sph, &sc->mesh_first, &sc->mesh_count, &sc->rays, &sc->keys_c,
                  &sc->vals_c, &sc->ckey, &sc->cbase, &sc->k1, &sc->v1, &sc->k2, &sc->v2, &sc->pos, &sc->first_chunk,
                  &sc->sorted_key, &sc->sorted_slot, &sc->sorted_rays, &sc->nodes, &sc->trav, &sc->masks, &sc->items,
-                 &sc->best, &sc->zero, &sc->small, &sc->packed_tmp, &sc->stage_in, &sc->stage_out};
+                 &sc->best, &sc->zero, &sc->stage_in, &sc->stage_out};
   for (Buf* b : bufs) b->release();
   if (sc->h_counters) cudaFreeHost(sc->h_counters);
-  if (sc->h_small) cudaFreeHost(sc->h_small);
+  if (sc->h_fd) cudaFreeHost(sc->h_fd);
+  if (sc->gexec) cudaGraphExecDestroy(sc->gexec);
+  if (sc->gstream) cudaStreamDestroy(sc->gstream);
+  if (sc->ev_in) cudaEventDestroy(sc->ev_in);
+  if (sc->ev_out) cudaEventDestroy(sc->ev_out);
   for (auto& e : sc->ev) if (e) cudaEventDestroy(e);
   delete sc;
 }
@@ -776,8 +849,8 @@ crsh_status crsh_trace_secondary_host(crsh_scene_t sc, const crsh_primary_hits* 
 
 crsh_status crsh_stats(crsh_scene_t sc, crsh_stats_t* out) {
   if (!sc || !out) return fail(CRSH_EINVAL, "null argument");
-  CK(cudaSetDevice(sc->device));
-  CK(cudaStreamSynchronize(sc->last_stream));
+  crsh_status rc = sync_frame(sc);
+  if (rc != CRSH_OK) return rc;
   std::memset(out, 0, sizeof(*out));
   const FrameInfo& fi = sc->fi;
   if (!fi.valid) return CRSH_OK;
@@ -785,22 +858,25 @@ crsh_status crsh_stats(crsh_scene_t sc, crsh_stats_t* out) {
   for (int s = 0; s < fi.n_seg; ++s) {
     const int ty = fi.seg_type[s];
     const unsigned long long* c = sc->h_counters + s * CTR_STRIDE;
-    out->rays[ty] = fi.seg_n[s];
+    out->rays[ty] = fi.fd.seg_n[s];
     out->slots[ty] = fi.seg_slot_start[s + 1] - fi.seg_slot_start[s];
-    out->chunks[ty] = fi.sorted ? fi.seg_C[s] : 0;
+    out->chunks[ty] = (fi.sorted && !fi.brute) ? fi.fd.seg_C[s] : 0;
     for (int k = 1; k <= MAX_LEVELS; ++k) { out->tests[ty][k] = c[CTR_TESTS + k]; out->hits[ty][k] = c[CTR_HITS + k]; }
     out->mesh_tests[ty] = c[CTR_MESH_TESTS];
     out->mesh_hits[ty] = c[CTR_MESH_HITS];
     out->final_tests[ty] = c[CTR_FINAL_TESTS];
     out->final_hits[ty] = c[CTR_FINAL_HITS];
     out->rays_hit[ty] = c[CTR_RAYS_HIT];
-    out->brute[ty] = (uint64_t)fi.seg_n[s] * (uint64_t)sc->M;
+    out->brute[ty] = (uint64_t)fi.fd.seg_n[s] * (uint64_t)sc->M;
   }
-  if (fi.timed && fi.N > 0) {
+  if ((fi.timed || fi.ktimed) && fi.fd.N > 0) {
     for (int i = 0; i < 8; ++i) {
+      if (!fi.timed && i != 6) continue;
       float ms = 0.f;
       if (cudaEventElapsedTime(&ms, sc->ev[i], sc->ev[i + 1]) == cudaSuccess) out->stage_ms[i] = ms;
+      else out->stage_ms[i] = -1.0f;
     }
+    (void)cudaGetLastError();   // a failed timing query must not poison the next launch check
   }
   return CRSH_OK;
 }
@@ -810,10 +886,11 @@ int64_t crsh_launch_count(crsh_scene_t sc) { return sc ? sc->launches : 0; }
 crsh_status crsh_debug_tap(crsh_scene_t sc, int32_t tap, int32_t seg_type, int32_t level, void* host_dst,
                            size_t cap_bytes, size_t* n_out) {
   if (!sc || !n_out) return fail(CRSH_EINVAL, "null argument");
-  CK(cudaSetDevice(sc->device));
-  CK(cudaStreamSynchronize(sc->last_stream));
+  crsh_status rc0 = sync_frame(sc);
+  if (rc0 != CRSH_OK) return rc0;
   *n_out = 0;
   const FrameInfo& fi = sc->fi;
+  const FrameDesc& fd = fi.fd;
   const void* src = nullptr;
   size_t n = 0, esz = 4;
   std::vector<uint32_t> rel;
@@ -830,33 +907,33 @@ crsh_status crsh_debug_tap(crsh_scene_t sc, int32_t tap, int32_t seg_type, int32
     int s = -1;
     for (int q = 0; q < fi.n_seg; ++q) if (fi.seg_type[q] == seg_type) s = q;
     if (s < 0) return CRSH_OK;   // segment not present: empty
-    const size_t ns = fi.seg_n[s];
+    const size_t ns = fd.seg_n[s];
     switch (tap) {
-      case CRSH_TAP_KEYS: src = sc->keys_c.as<uint32_t>() + fi.seg_comp_start[s]; n = ns; break;
-      case CRSH_TAP_VALS: src = sc->vals_c.as<uint32_t>() + fi.seg_comp_start[s]; n = ns; break;
+      case CRSH_TAP_KEYS: src = sc->keys_c.as<uint32_t>() + fd.seg_comp_start[s]; n = ns; break;
+      case CRSH_TAP_VALS: src = sc->vals_c.as<uint32_t>() + fd.seg_comp_start[s]; n = ns; break;
       case CRSH_TAP_CHUNK_KEYS:
-        if (!fi.sorted) return CRSH_OK;
-        src = sc->ckey.as<uint32_t>() + fi.seg_chunk_start[s]; n = fi.seg_C[s]; break;
+        if (!fi.sorted || fi.brute) return CRSH_OK;
+        src = sc->ckey.as<uint32_t>() + fd.seg_chunk_start[s]; n = fd.seg_C[s]; break;
       case CRSH_TAP_CHUNK_BASE: {
-        if (!fi.sorted) return CRSH_OK;
-        n = fi.seg_C[s];
+        if (!fi.sorted || fi.brute) return CRSH_OK;
+        n = fd.seg_C[s];
         rel.resize(n);
-        if (n) CK(cudaMemcpy(rel.data(), sc->cbase.as<uint32_t>() + fi.seg_chunk_start[s], 4 * n, cudaMemcpyDeviceToHost));
-        for (auto& v : rel) v -= fi.seg_comp_start[s];
+        if (n) CK(cudaMemcpy(rel.data(), sc->cbase.as<uint32_t>() + fd.seg_chunk_start[s], 4 * n, cudaMemcpyDeviceToHost));
+        for (auto& v : rel) v -= fd.seg_comp_start[s];
         *n_out = n;
         if (cap_bytes < 4 * n) return fail(CRSH_EIO, "buffer too small");
         if (n) std::memcpy(host_dst, rel.data(), 4 * n);
         return CRSH_OK;
       }
-      case CRSH_TAP_SORTED_KEYS: src = sc->sorted_key.as<uint32_t>() + fi.seg_pad_base[s]; n = ns; break;
-      case CRSH_TAP_SORTED_SLOTS: src = sc->sorted_slot.as<uint32_t>() + fi.seg_pad_base[s]; n = ns; break;
-      case CRSH_TAP_SORTED_RAYS: src = sc->sorted_rays.as<float4>() + 2 * (size_t)fi.seg_pad_base[s]; n = ns; esz = 32; break;
+      case CRSH_TAP_SORTED_KEYS: src = sc->sorted_key.as<uint32_t>() + fd.seg_pad_base[s]; n = ns; break;
+      case CRSH_TAP_SORTED_SLOTS: src = sc->sorted_slot.as<uint32_t>() + fd.seg_pad_base[s]; n = ns; break;
+      case CRSH_TAP_SORTED_RAYS: src = sc->sorted_rays.as<float4>() + 2 * (size_t)fd.seg_pad_base[s]; n = ns; esz = 32; break;
       case CRSH_TAP_NODES: {
         if (level < 1 || level > fi.Lv) return fail(CRSH_EINVAL, "bad level");
         uint64_t per = fi.B0;
         for (int k = 1; k < level; ++k) per *= fi.B;
         n = (size_t)((ns + per - 1) / per);
-        src = sc->nodes.as<float4>() + 2 * (fi.level_off[level] + fi.seg_pad_base[s] / per);
+        src = sc->nodes.as<float4>() + 2 * (fi.level_off[level] + fd.seg_pad_base[s] / per);
         esz = 32;
         break;
       }

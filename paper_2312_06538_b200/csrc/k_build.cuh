@@ -94,10 +94,8 @@ __device__ __forceinline__ NodeV load_node(const float4* nodes, size_t j) {
 }
 
 struct LeafArgs {
-  uint32_t n_leaves;                      // padded, all segments
+  const FrameDesc* fd;                    // level_n[1], seg_pad_base, seg_n
   int32_t n_seg;
-  uint32_t seg_pad_base[MAX_SEG + 1];
-  uint32_t seg_n[MAX_SEG];
   const uint32_t* sorted_slot;
   const float4* rays;                     // [slots][2]
   float4* sorted_rays;                    // [Np][2]
@@ -111,12 +109,13 @@ struct LeafArgs {
 template <int B0>
 __global__ void __launch_bounds__(128) k_leaves(const LeafArgs a) {
   const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= a.n_leaves) return;
+  if (j >= a.fd->level_n[1]) return;
   const uint32_t p0 = j * B0;
   int s = 0;
-  for (int q = 1; q < a.n_seg; ++q) s = (p0 >= a.seg_pad_base[q]) ? q : s;
-  const uint32_t local = p0 - a.seg_pad_base[s];
-  const int real = (int)min((uint32_t)B0, a.seg_n[s] > local ? a.seg_n[s] - local : 0u);
+  for (int q = 1; q < a.n_seg; ++q) s = (p0 >= a.fd->seg_pad_base[q]) ? q : s;
+  const uint32_t local = p0 - a.fd->seg_pad_base[s];
+  const uint32_t ns = a.fd->seg_n[s];
+  const int real = (int)min((uint32_t)B0, ns > local ? ns - local : 0u);
   f3 sc[B0];
   float sr[B0];
   f3 x = mk3(0.f, 0.f, 1.f);
@@ -162,7 +161,8 @@ __global__ void __launch_bounds__(128) k_leaves(const LeafArgs a) {
 }
 
 struct UpperArgs {
-  uint32_t n_nodes;          // padded nodes of this level
+  const FrameDesc* fd;
+  int32_t level;             // padded nodes of this level: fd->level_n[level]
   const float4* child_nodes; // paper layout of level k-1
   float4* nodes;
   float4* trav;
@@ -173,7 +173,7 @@ struct UpperArgs {
 template <int B>
 __global__ void __launch_bounds__(128) k_upper(const UpperArgs a) {
   const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= a.n_nodes) return;
+  if (j >= a.fd->level_n[a.level]) return;
   NodeV st[B];
 #pragma unroll
   for (int i = 0; i < B; ++i) st[i] = load_node(a.child_nodes, (size_t)j * B + i);

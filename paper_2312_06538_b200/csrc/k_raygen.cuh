@@ -40,7 +40,7 @@ struct RaygenArgs {
   unsigned long long* out_packed;     // optional: sentinel for every slot
   unsigned long long* status;         // look-back, one word per tile
   uint32_t* ticket;
-  uint32_t* seg_comp_start;           // out [n_seg + 1]
+  FrameDesc* fd;                      // out: seg_comp_start[0..n_seg]
 };
 
 __device__ __forceinline__ bool gen_ray(const RaygenArgs& a, uint32_t slot, float4& r0, float4& r1, uint32_t& key) {
@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_raygen(const RaygenArgs a) {
       a.vals_c[pos] = slot;
     }
     for (int s = 0; s < a.n_seg; ++s)
-      if (slot == a.seg_slot_start[s] && slot < a.n_slots) a.seg_comp_start[s] = pos;
+      if (slot == a.seg_slot_start[s] && slot < a.n_slots) a.fd->seg_comp_start[s] = pos;
   }
   const uint32_t n_tiles = (a.n_slots + SCAN_TILE - 1) / SCAN_TILE;
   if (tile == n_tiles - 1 && threadIdx.x == 0) {
@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_raygen(const RaygenArgs a) {
       for (int q = 0; q < SCAN_ITEMS * 8; ++q) t += s_cnt[q];
       return t;
     }();
-    a.seg_comp_start[a.n_seg] = total;
+    a.fd->seg_comp_start[a.n_seg] = total;
   }
 }
 

@@ -10,13 +10,11 @@ namespace crsh {
 
 // ============================================================== K2: compression
 struct RleArgs {
-  uint32_t N;
+  FrameDesc* fd;                        // in: N, seg_comp_start; out: seg_chunk_start, C
   const uint32_t* keys;                 // compacted keys [N]
   int32_t n_seg;
-  uint32_t seg_comp_start[MAX_SEG + 1];
   uint32_t* ckey;                       // [C]
   uint32_t* cbase;                      // [C + 1], global compacted index of each chunk head
-  uint32_t* seg_chunk_start;            // out [n_seg + 1]
   unsigned long long* status;
   uint32_t* ticket;
 };
@@ -29,6 +27,11 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_rle(const RleArgs a) {
   if (threadIdx.x == 0) s_tile = atomicAdd(a.ticket, 1u);
   __syncthreads();
   const uint32_t tile = s_tile;
+  const uint32_t N = a.fd->N;
+  const uint32_t n_tiles = (N + SCAN_TILE - 1) / SCAN_TILE;
+  if (tile >= n_tiles) return;   // surplus block (grid sized from the slot bound)
+  uint32_t segst[MAX_SEG + 1];
+  for (int s = 0; s <= a.n_seg; ++s) segst[s] = a.fd->seg_comp_start[s];
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
   uint32_t key[SCAN_ITEMS], ballot[SCAN_ITEMS];
 #pragma unroll
@@ -36,10 +39,10 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_rle(const RleArgs a) {
     const uint32_t i = tile * SCAN_TILE + it * SCAN_THREADS + threadIdx.x;
     bool head = false;
     uint32_t k = 0;
-    if (i < a.N) {
+    if (i < N) {
       k = __ldg(a.keys + i);
       head = (i == 0) || (k != __ldg(a.keys + i - 1));
-      for (int s = 0; s < a.n_seg; ++s) head |= (i == a.seg_comp_start[s]);
+      for (int s = 0; s < a.n_seg; ++s) head |= (i == segst[s]);
     }
     key[it] = k;
     ballot[it] = __ballot_sync(CRSH_FULL, head);
@@ -57,19 +60,32 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_rle(const RleArgs a) {
       a.ckey[c] = key[it];
       a.cbase[c] = i;
       for (int s = 0; s < a.n_seg; ++s)
-        if (i == a.seg_comp_start[s]) a.seg_chunk_start[s] = c;
+        if (i == segst[s]) a.fd->seg_chunk_start[s] = c;
     }
   }
-  const uint32_t n_tiles = (a.N + SCAN_TILE - 1) / SCAN_TILE;
   if (tile == n_tiles - 1 && threadIdx.x == 0) {
     uint32_t t = 0;
     for (int q = 0; q < SCAN_ITEMS * 8; ++q) t += s_cnt[q];
     const uint32_t C = prefix + t;
-    a.cbase[C] = a.N;
-    a.seg_chunk_start[a.n_seg] = C;
+    a.cbase[C] = N;
+    a.fd->seg_chunk_start[a.n_seg] = C;
+    a.fd->C = C;
     for (int s = 0; s < a.n_seg; ++s)
-      if (a.seg_comp_start[s] >= a.N) a.seg_chunk_start[s] = C;   // empty trailing segment
+      if (segst[s] >= N) a.fd->seg_chunk_start[s] = C;   // empty trailing segment
   }
+}
+
+// per-segment chunk counts and sort-tile offsets (one thread)
+__global__ void k_chunk_plan(FrameDesc* fd, int n_seg, uint32_t sort_tile) {
+  if (threadIdx.x != 0) return;
+  uint32_t tiles = 0;
+  for (int s = 0; s < n_seg; ++s) {
+    const uint32_t c = fd->seg_n[s] ? fd->seg_chunk_start[s + 1] - fd->seg_chunk_start[s] : 0u;
+    fd->seg_C[s] = c;
+    fd->sort_tile_start[s] = tiles;
+    tiles += (c + sort_tile - 1) / sort_tile;
+  }
+  fd->sort_tile_start[n_seg] = tiles;
 }
 
 // ============================================================== K3: radix sort
@@ -81,11 +97,16 @@ constexpr int SORT_ITEMS = 8;
 constexpr int SORT_TILE = SORT_THREADS * SORT_ITEMS;   // 4096
 constexpr int SORT_PASSES = 32 / RADIX_BITS;
 
-struct SegChunks {
+struct SegChunks {   // per-segment chunk ranges, loaded from the FrameDesc
   int32_t n_seg;
   uint32_t start[MAX_SEG + 1];     // global chunk index of each segment's first chunk
   uint32_t count[MAX_SEG];
   uint32_t tile_start[MAX_SEG + 1];
+  __device__ void load(const FrameDesc* fd, int ns) {
+    n_seg = ns;
+    for (int s = 0; s <= ns; ++s) { start[s] = fd->seg_chunk_start[s]; tile_start[s] = fd->sort_tile_start[s]; }
+    for (int s = 0; s < ns; ++s) count[s] = fd->seg_C[s];
+  }
 };
 
 __device__ __forceinline__ int seg_of(const uint32_t* starts, int n, uint32_t i) {
@@ -95,9 +116,12 @@ __device__ __forceinline__ int seg_of(const uint32_t* starts, int n, uint32_t i)
 }
 
 // Per-segment digit histograms of all passes in one read of the keys.
-__global__ void __launch_bounds__(256) k_radix_hist(const SegChunks sc, const uint32_t* __restrict__ keys,
-                                                    uint32_t C, uint32_t* __restrict__ hist /*[3][4][256]*/) {
+__global__ void __launch_bounds__(256) k_radix_hist(const FrameDesc* fd, int n_seg, const uint32_t* __restrict__ keys,
+                                                    uint32_t* __restrict__ hist /*[3][4][256]*/) {
   __shared__ uint32_t h[MAX_SEG * SORT_PASSES * RADIX_BINS];
+  SegChunks sc;
+  sc.load(fd, n_seg);
+  const uint32_t C = fd->C;
   for (int i = threadIdx.x; i < MAX_SEG * SORT_PASSES * RADIX_BINS; i += blockDim.x) h[i] = 0;
   __syncthreads();
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < C; i += gridDim.x * blockDim.x) {
@@ -112,7 +136,8 @@ __global__ void __launch_bounds__(256) k_radix_hist(const SegChunks sc, const ui
 }
 
 struct SortPassArgs {
-  SegChunks sc;
+  const FrameDesc* fd;
+  int32_t n_seg;
   int32_t pass;
   const uint32_t* keys_in;
   const uint32_t* vals_in;   // nullptr on the first pass: values = global chunk index
@@ -147,9 +172,12 @@ __global__ void __launch_bounds__(SORT_THREADS) k_onesweep(const SortPassArgs a)
   for (int i = threadIdx.x; i < SORT_WARPS * RADIX_BINS; i += SORT_THREADS) s_whist[i] = 0;
   __syncthreads();
   const uint32_t tile = s_tile;
-  const int seg = seg_of(a.sc.tile_start, a.sc.n_seg, tile);
-  const uint32_t t_local = tile - a.sc.tile_start[seg];
-  const uint32_t n = a.sc.count[seg], seg0 = a.sc.start[seg];
+  SegChunks sc;
+  sc.load(a.fd, a.n_seg);
+  if (tile >= sc.tile_start[sc.n_seg]) return;   // surplus block
+  const int seg = seg_of(sc.tile_start, sc.n_seg, tile);
+  const uint32_t t_local = tile - sc.tile_start[seg];
+  const uint32_t n = sc.count[seg], seg0 = sc.start[seg];
   const int shift = RADIX_BITS * a.pass;
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5, lt = lanemask_lt();
 
@@ -198,7 +226,7 @@ __global__ void __launch_bounds__(SORT_THREADS) k_onesweep(const SortPassArgs a)
     // batched look-back: 8 predecessors' words are requested at once, so a
     // one-wave sort (every tile looking back at aggregates) costs ~1/8 of the
     // round trips of a one-by-one walk; the segment's first tile is inclusive
-    const int first = (int)a.sc.tile_start[seg];
+    const int first = (int)sc.tile_start[seg];
     int p = (int)tile - 1;
     bool done = false;
     while (!done) {
@@ -248,7 +276,7 @@ __global__ void __launch_bounds__(SORT_THREADS) k_onesweep(const SortPassArgs a)
 constexpr int EXP_TILE = 2048;
 
 struct ScanSizeArgs {
-  uint32_t C, N;
+  const FrameDesc* fd;                // C, N
   const uint32_t* sorted_cidx;   // chunk index of each sorted chunk
   const uint32_t* cbase;         // [C + 1]
   uint32_t* pos;                 // out [C + 1]: exclusive scan of the skeleton
@@ -264,13 +292,16 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_sizes(const ScanSizeArgs 
   if (threadIdx.x == 0) s_tile = atomicAdd(a.ticket, 1u);
   __syncthreads();
   const uint32_t tile = s_tile;
+  const uint32_t C = a.fd->C, N = a.fd->N;
+  const uint32_t n_tiles = (C + SCAN_TILE - 1) / SCAN_TILE;
+  if (tile >= n_tiles) return;   // surplus block
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
   uint32_t size[SCAN_ITEMS], wex[SCAN_ITEMS];
 #pragma unroll
   for (int it = 0; it < SCAN_ITEMS; ++it) {
     const uint32_t c = tile * SCAN_TILE + it * SCAN_THREADS + threadIdx.x;
     uint32_t sz = 0;
-    if (c < a.C) {
+    if (c < C) {
       const uint32_t ci = __ldg(a.sorted_cidx + c);
       sz = __ldg(a.cbase + ci + 1) - __ldg(a.cbase + ci);
     }
@@ -291,19 +322,18 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_sizes(const ScanSizeArgs 
 #pragma unroll
   for (int it = 0; it < SCAN_ITEMS; ++it) {
     const uint32_t c = tile * SCAN_TILE + it * SCAN_THREADS + threadIdx.x;
-    if (c < a.C) {
+    if (c < C) {
       const uint32_t p = prefix + s_excl[it * 8 + warp] + wex[it];
       a.pos[c] = p;
       // the chunk covering each output tile start k*EXP_TILE in [p, p + size)
       for (uint32_t kk = (p + EXP_TILE - 1) / EXP_TILE; kk * EXP_TILE < p + size[it]; ++kk) a.first_chunk[kk] = c;
     }
   }
-  const uint32_t n_tiles = (a.C + SCAN_TILE - 1) / SCAN_TILE;
-  if (tile == n_tiles - 1 && threadIdx.x == 0) a.pos[a.C] = a.N;
+  if (tile == n_tiles - 1 && threadIdx.x == 0) a.pos[C] = N;
 }
 
 struct ExpandArgs {
-  uint32_t N, C;
+  const FrameDesc* fd;      // N, C, seg_comp_start, seg_pad_base
   const uint32_t* pos;
   const uint32_t* first_chunk;
   const uint32_t* skey;
@@ -311,8 +341,6 @@ struct ExpandArgs {
   const uint32_t* cbase;
   const uint32_t* vals_c;
   int32_t n_seg;
-  uint32_t seg_comp_start[MAX_SEG + 1];
-  uint32_t seg_pad_base[MAX_SEG + 1];
   uint32_t* sorted_key;     // padded layout
   uint32_t* sorted_slot;
 };
@@ -322,10 +350,15 @@ struct ExpandArgs {
 // tiles), then gathers the slot id of the run element.
 __global__ void __launch_bounds__(256) k_expand(const ExpandArgs a) {
   __shared__ uint32_t s_pos[EXP_TILE + 2];
+  const uint32_t N = a.fd->N, C = a.fd->C;
+  const uint32_t nb = (N + EXP_TILE - 1) / EXP_TILE;
+  if (blockIdx.x >= nb) return;   // surplus block
+  uint32_t segc[MAX_SEG + 1], segp[MAX_SEG + 1];
+  for (int s = 0; s <= a.n_seg; ++s) { segc[s] = a.fd->seg_comp_start[s]; segp[s] = a.fd->seg_pad_base[s]; }
   const uint32_t o0 = blockIdx.x * EXP_TILE;
-  const uint32_t o1 = min(o0 + EXP_TILE, a.N);
+  const uint32_t o1 = min(o0 + EXP_TILE, N);
   const uint32_t c_lo = __ldg(a.first_chunk + blockIdx.x);
-  const uint32_t c_hi = (blockIdx.x + 1 < gridDim.x) ? __ldg(a.first_chunk + blockIdx.x + 1) : a.C - 1;
+  const uint32_t c_hi = (blockIdx.x + 1 < nb) ? __ldg(a.first_chunk + blockIdx.x + 1) : C - 1;
   const uint32_t nc = c_hi - c_lo + 1;
   for (uint32_t j = threadIdx.x; j <= nc; j += blockDim.x) s_pos[j] = __ldg(a.pos + c_lo + j);
   __syncthreads();
@@ -337,8 +370,8 @@ __global__ void __launch_bounds__(256) k_expand(const ExpandArgs a) {
     }
     const uint32_t c = c_lo + lo;
     const uint32_t src = __ldg(a.cbase + __ldg(a.scidx + c)) + (o - s_pos[lo]);
-    const int s = seg_of(a.seg_comp_start, a.n_seg, o);
-    const uint32_t dst = a.seg_pad_base[s] + (o - a.seg_comp_start[s]);
+    const int s = seg_of(segc, a.n_seg, o);
+    const uint32_t dst = segp[s] + (o - segc[s]);
     a.sorted_key[dst] = __ldg(a.skey + c);
     a.sorted_slot[dst] = __ldg(a.vals_c + src);
   }
@@ -346,9 +379,12 @@ __global__ void __launch_bounds__(256) k_expand(const ExpandArgs a) {
 
 // RAH (CRSH_F_SORT off): rays stay in generation order.
 __global__ void k_copy_unsorted(const ExpandArgs a) {
-  for (uint32_t o = blockIdx.x * blockDim.x + threadIdx.x; o < a.N; o += gridDim.x * blockDim.x) {
-    const int s = seg_of(a.seg_comp_start, a.n_seg, o);
-    const uint32_t dst = a.seg_pad_base[s] + (o - a.seg_comp_start[s]);
+  const uint32_t N = a.fd->N;
+  uint32_t segc[MAX_SEG + 1], segp[MAX_SEG + 1];
+  for (int s = 0; s <= a.n_seg; ++s) { segc[s] = a.fd->seg_comp_start[s]; segp[s] = a.fd->seg_pad_base[s]; }
+  for (uint32_t o = blockIdx.x * blockDim.x + threadIdx.x; o < N; o += gridDim.x * blockDim.x) {
+    const int s = seg_of(segc, a.n_seg, o);
+    const uint32_t dst = segp[s] + (o - segc[s]);
     a.sorted_key[dst] = __ldg(a.skey + o);
     a.sorted_slot[dst] = __ldg(a.vals_c + o);
   }

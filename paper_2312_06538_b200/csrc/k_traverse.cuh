@@ -46,7 +46,9 @@ __device__ __forceinline__ unsigned long long pack_hit(float t, uint32_t tri) {
 
 // ============================================================== K7
 struct CullArgs {
-  uint32_t top_lo, top_hi;     // padded top-node range of this shard
+  const FrameDesc* fd;         // G, seg_pad_base -> this shard's top-node range
+  int32_t K, rank, world;
+  uint32_t span;
   int32_t W;                   // mask words per node = ceil(n_meshes / 32)
   const float4* trav_top;      // level Lv, traversal layout
   int32_t n_meshes;
@@ -56,17 +58,19 @@ struct CullArgs {
   uint32_t* masks;             // [n_top_padded][W]
   unsigned long long* counters;
   int32_t n_seg;
-  uint32_t seg_top_start[MAX_SEG + 1];
 };
 
 __global__ void __launch_bounds__(256) k_mesh_cull(const CullArgs a) {
   __shared__ unsigned long long s_ctr[MAX_SEG][2];
   if (threadIdx.x < MAX_SEG * 2) (&s_ctr[0][0])[threadIdx.x] = 0ull;
   __syncthreads();
+  const uint32_t G = a.fd->G;
+  const uint32_t top_lo = (uint32_t)((uint64_t)G * a.rank / a.world) * a.K;
+  const uint32_t top_hi = (uint32_t)((uint64_t)G * (a.rank + 1) / a.world) * a.K;
   const uint64_t gid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  const uint64_t total = (uint64_t)(a.top_hi - a.top_lo) * a.W;
+  const uint64_t total = (uint64_t)(top_hi - top_lo) * a.W;
   if (gid < total) {
-    const uint32_t n = a.top_lo + (uint32_t)(gid / a.W);
+    const uint32_t n = top_lo + (uint32_t)(gid / a.W);
     const int w = (int)(gid % a.W);
     const float4 p0 = __ldg(a.trav_top + 3 * (size_t)n), p1 = __ldg(a.trav_top + 3 * (size_t)n + 1),
                  p2 = __ldg(a.trav_top + 3 * (size_t)n + 2);
@@ -88,7 +92,7 @@ __global__ void __launch_bounds__(256) k_mesh_cull(const CullArgs a) {
     a.masks[(size_t)n * a.W + w] = bits;
     if (tests) {
       int s = 0;
-      for (int q = 1; q < a.n_seg; ++q) s = (n >= a.seg_top_start[q]) ? q : s;
+      for (int q = 1; q < a.n_seg; ++q) s = (n >= a.fd->seg_pad_base[q] / a.span) ? q : s;
       atomicAdd(&s_ctr[s][0], (unsigned long long)tests);
       atomicAdd(&s_ctr[s][1], (unsigned long long)hits);
     }
@@ -102,14 +106,14 @@ __global__ void __launch_bounds__(256) k_mesh_cull(const CullArgs a) {
 
 // ============================================================== K7b
 struct PlanArgs {
-  uint32_t g_lo, g_hi;         // group range of this shard
+  FrameDesc* fd;               // G -> this shard's group range; out: n_items
+  int32_t rank, world;
   int32_t K, W;
   const uint32_t* masks;
   int32_t n_meshes;
   const uint32_t* mesh_count;
   uint32_t item_tris;
   uint4* items;                // (group, v_begin, v_end, 0)
-  uint32_t* n_items;
   unsigned long long* status;
   uint32_t* ticket;
 };
@@ -120,13 +124,20 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_plan(const PlanArgs a) {
   if (threadIdx.x == 0) s_tile = atomicAdd(a.ticket, 1u);
   __syncthreads();
   const uint32_t tile = s_tile;
+  const uint32_t G = a.fd->G;
+  const uint32_t g_lo = (uint32_t)((uint64_t)G * a.rank / a.world), g_hi = (uint32_t)((uint64_t)G * (a.rank + 1) / a.world);
+  const uint32_t n_tiles = (g_hi - g_lo + SCAN_TILE - 1) / SCAN_TILE;
+  if (tile >= n_tiles) {   // surplus block; the first one reports "no items" for an empty range
+    if (tile == 0 && threadIdx.x == 0) a.fd->n_items = 0u;
+    return;
+  }
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
   uint32_t ntri[SCAN_ITEMS], nit[SCAN_ITEMS], wex[SCAN_ITEMS];
 #pragma unroll
   for (int it = 0; it < SCAN_ITEMS; ++it) {
-    const uint32_t g = a.g_lo + tile * SCAN_TILE + it * SCAN_THREADS + threadIdx.x;
+    const uint32_t g = g_lo + tile * SCAN_TILE + it * SCAN_THREADS + threadIdx.x;
     uint32_t T = 0;
-    if (g < a.g_hi) {
+    if (g < g_hi) {
       for (int w = 0; w < a.W; ++w) {
         uint32_t m = 0;
         for (int j = 0; j < a.K; ++j) m |= __ldg(a.masks + ((size_t)g * a.K + j) * a.W + w);
@@ -155,16 +166,15 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_plan(const PlanArgs a) {
   const uint32_t prefix = s_prefix;
 #pragma unroll
   for (int it = 0; it < SCAN_ITEMS; ++it) {
-    const uint32_t g = a.g_lo + tile * SCAN_TILE + it * SCAN_THREADS + threadIdx.x;
+    const uint32_t g = g_lo + tile * SCAN_TILE + it * SCAN_THREADS + threadIdx.x;
     const uint32_t off = prefix + s_excl[it * 8 + warp] + wex[it];
     for (uint32_t q = 0; q < nit[it]; ++q)
       a.items[off + q] = make_uint4(g, q * a.item_tris, min(ntri[it], (q + 1) * a.item_tris), 0u);
   }
-  const uint32_t n_tiles = (a.g_hi - a.g_lo + SCAN_TILE - 1) / SCAN_TILE;
   if (tile == n_tiles - 1 && threadIdx.x == 0) {
     uint32_t t = 0;
     for (int q = 0; q < SCAN_ITEMS * 8; ++q) t += s_cnt[q];
-    *a.n_items = prefix + t;
+    a.fd->n_items = prefix + t;
   }
 }
 
@@ -200,12 +210,11 @@ struct TravArgs {
   const uint32_t* mesh_first;
   const uint32_t* mesh_count;
   const uint4* items;
-  const uint32_t* n_items;
+  const FrameDesc* fd;                // n_items, seg_pad_base (group starts)
   uint32_t* ticket;
   unsigned long long* best;           // [Np]
   unsigned long long* counters;
   int32_t n_seg;
-  uint32_t seg_group_start[MAX_SEG + 1];
 };
 
 // dynamic shared-memory layout (bytes), shared by host and device
@@ -292,7 +301,9 @@ __global__ void __launch_bounds__(TRAV_THREADS) k_traverse(const TravArgs a, con
   for (uint32_t i = tid; i < MAX_SEG * CTR_STRIDE; i += TRAV_THREADS) s_ctr[i] = 0ull;
   if (lane <= MAX_LEVELS) qlen[lane] = 0u;
   if (tid == 0) s_cur_g = 0xFFFFFFFFu;
-  const uint32_t n_items = *a.n_items;
+  const uint32_t n_items = a.fd->n_items;
+  uint32_t seg_group_start[MAX_SEG + 1];
+  for (int q = 0; q <= a.n_seg; ++q) seg_group_start[q] = a.fd->seg_pad_base[q] / a.group_rays;
 
   for (;;) {
     __syncthreads();
@@ -303,7 +314,7 @@ __global__ void __launch_bounds__(TRAV_THREADS) k_traverse(const TravArgs a, con
     const uint4 item = __ldg(a.items + it);
     const uint32_t g = item.x;
     int seg = 0;
-    for (int qq = 1; qq < a.n_seg; ++qq) seg = (g >= a.seg_group_start[qq]) ? qq : seg;
+    for (int qq = 1; qq < a.n_seg; ++qq) seg = (g >= seg_group_start[qq]) ? qq : seg;
     unsigned long long* ctr = s_ctr + seg * CTR_STRIDE;
 
     if (g != s_cur_g) {   // uniform: group setup (top nodes, surviving meshes, group data)
@@ -604,13 +615,12 @@ __global__ void __launch_bounds__(TRAV_THREADS) k_traverse(const TravArgs a, con
 
 // ============================================================== brute force (N x M)
 struct BruteArgs {
-  uint32_t N;
+  const FrameDesc* fd;          // N, seg_comp_start
   const uint32_t* vals_c;       // compacted slot ids
   const float4* rays;           // [slots][2]
   const float4* tri_e;
   int64_t M;
   int32_t n_seg;
-  uint32_t seg_comp_start[MAX_SEG + 1];
   int32_t* out_hit;
   float* out_t;
   unsigned long long* out_packed;
@@ -625,7 +635,9 @@ __global__ void __launch_bounds__(256) k_brute(const BruteArgs a) {
   __shared__ unsigned long long s_hit[MAX_SEG], s_tests[MAX_SEG];
   if (threadIdx.x < MAX_SEG) { s_hit[threadIdx.x] = 0ull; s_tests[threadIdx.x] = 0ull; }
   const uint32_t i = blockIdx.x * 256u + threadIdx.x;
-  const bool ok = i < a.N;
+  const uint32_t N = a.fd->N;
+  if (blockIdx.x * 256u >= N) return;   // surplus block (uniform)
+  const bool ok = i < N;
   uint32_t slot = 0;
   float4 r0 = make_float4(0.f, 0.f, 0.f, 1.f), r1 = make_float4(0.f, 0.f, 1.f, -1.f);
   if (ok) {
@@ -653,7 +665,7 @@ __global__ void __launch_bounds__(256) k_brute(const BruteArgs a) {
   }
   if (ok) {
     int s = 0;
-    for (int q = 1; q < a.n_seg; ++q) s = (i >= a.seg_comp_start[q]) ? q : s;
+    for (int q = 1; q < a.n_seg; ++q) s = (i >= a.fd->seg_comp_start[q]) ? q : s;
     const bool hit = best != BEST_NONE;
     if (a.out_packed) {
       a.out_packed[slot] = hit ? best : PACK_MISS;
@@ -673,10 +685,10 @@ __global__ void __launch_bounds__(256) k_brute(const BruteArgs a) {
 
 // ============================================================== K9
 struct UnpackArgs {
-  uint32_t r_lo, r_hi;          // padded sorted-ray range of this shard
+  const FrameDesc* fd;          // G, seg_pad_base, seg_n -> this shard's sorted-ray range
+  int32_t rank, world;
+  uint32_t group_rays;
   int32_t n_seg;
-  uint32_t seg_pad_base[MAX_SEG + 1];
-  uint32_t seg_n[MAX_SEG];
   const uint32_t* sorted_slot;
   const unsigned long long* best;
   int32_t* out_hit;
@@ -689,11 +701,14 @@ __global__ void __launch_bounds__(256) k_unpack(const UnpackArgs a) {
   __shared__ unsigned long long s_hit[MAX_SEG];
   if (threadIdx.x < MAX_SEG) s_hit[threadIdx.x] = 0ull;
   __syncthreads();
-  const uint32_t i = a.r_lo + blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < a.r_hi) {
+  const uint32_t G = a.fd->G;
+  const uint32_t r_lo = (uint32_t)((uint64_t)G * a.rank / a.world) * a.group_rays;
+  const uint32_t r_hi = (uint32_t)((uint64_t)G * (a.rank + 1) / a.world) * a.group_rays;
+  const uint32_t i = r_lo + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < r_hi) {
     int s = 0;
-    for (int q = 1; q < a.n_seg; ++q) s = (i >= a.seg_pad_base[q]) ? q : s;
-    if (i - a.seg_pad_base[s] < a.seg_n[s]) {
+    for (int q = 1; q < a.n_seg; ++q) s = (i >= a.fd->seg_pad_base[q]) ? q : s;
+    if (i - a.fd->seg_pad_base[s] < a.fd->seg_n[s]) {
       const uint32_t slot = __ldg(a.sorted_slot + i);
       const unsigned long long b = __ldg(a.best + i);
       const bool hit = b != BEST_NONE;
