@@ -123,26 +123,34 @@ def measured_peaks():
         return {}
 
 
-def oracle_sample(w, flags, target_s=12.0, max_rows=None):
-    """Time the oracle (as it stands) on a band of image rows sized to about
-    target_s seconds of host CPU work; returns (rays, seconds, rows, cores)."""
+def oracle_band(w, flags, rows, prep=None):
+    """Time the oracle (as it stands) on the centre band of `rows` image rows;
+    returns (rays, seconds)."""
     import oracle
     from workloads.scenes import Workload
+    prep = prep or oracle.ScenePrep(w.tris, w.mesh_ids)
+    r0 = (w.height - rows) // 2
+    P = w.width
+    sub = Workload(w.name, w.tris, w.mesh_ids, w.tri_mat, w.materials, w.lights, w.eye, w.width, rows,
+                   np.ascontiguousarray(w.pos.reshape(3, w.height, P)[:, r0:r0 + rows].reshape(3, -1)),
+                   np.ascontiguousarray(w.nrm.reshape(3, w.height, P)[:, r0:r0 + rows].reshape(3, -1)),
+                   np.ascontiguousarray(w.mat.reshape(w.height, P)[r0:r0 + rows].reshape(-1)), w.ray_types,
+                   w.levels, w.leaf_size, w.branching)
+    t0 = time.perf_counter()
+    out = oracle.trace(sub, prep, flags=flags)
+    return int(sum(out["stats"]["rays"])), time.perf_counter() - t0
+
+
+def oracle_sample(w, flags, target_s=12.0):
+    """Grow a centre band of image rows until one oracle run takes about
+    target_s seconds of host CPU work (or the whole image); returns (rays,
+    seconds, rows, cores)."""
+    import oracle
     prep = oracle.ScenePrep(w.tris, w.mesh_ids)
     rows = max(1, w.height // 64)
     while True:
-        r0 = (w.height - rows) // 2
-        P = w.width
-        sub = Workload(w.name, w.tris, w.mesh_ids, w.tri_mat, w.materials, w.lights, w.eye, w.width, rows,
-                       np.ascontiguousarray(w.pos.reshape(3, w.height, P)[:, r0:r0 + rows].reshape(3, -1)),
-                       np.ascontiguousarray(w.nrm.reshape(3, w.height, P)[:, r0:r0 + rows].reshape(3, -1)),
-                       np.ascontiguousarray(w.mat.reshape(w.height, P)[r0:r0 + rows].reshape(-1)), w.ray_types,
-                       w.levels, w.leaf_size, w.branching)
-        t0 = time.perf_counter()
-        out = oracle.trace(sub, prep, flags=flags)
-        dt = time.perf_counter() - t0
-        rays = int(sum(out["stats"]["rays"]))
-        if dt >= target_s / 4 or rows >= w.height or (max_rows and rows >= max_rows):
+        rays, dt = oracle_band(w, flags, rows, prep)
+        if dt >= target_s / 4 or rows >= w.height:
             return rays, dt, rows, oracle.default_threads()
         rows = min(w.height, max(rows + 1, int(rows * min(8.0, target_s / max(dt, 1e-3)))))
 
@@ -317,9 +325,10 @@ def run_reference(args):
     flags = 3 | (4 if args.zorder else 0)
     budget = 150.0 / max(1, args.steps + args.warmup)      # whole run within a few minutes
     rows_probe = oracle_sample(w, flags, target_s=min(budget, 8.0))[2]
+    prep = oracle.ScenePrep(w.tris, w.mesh_ids)
     times, rays = [], 0
     for i in range(args.warmup + args.steps):
-        r, dt, rows, cores = oracle_sample(w, flags, target_s=0.0, max_rows=rows_probe)
+        r, dt = oracle_band(w, flags, rows_probe, prep)
         if i >= args.warmup:
             times.append(dt)
             rays += r
