@@ -196,6 +196,7 @@ constexpr int TRAV_THREADS = 256;
 constexpr int TRAV_WARPS = TRAV_THREADS / 32;
 constexpr uint32_t SMALL_GROUP_RAYS = 512;   // groups up to this size live in shared memory
 constexpr int LOWQ = 64;                     // capacity of a warp queue below level Lv-1
+__device__ __forceinline__ uint32_t ray_swz(uint32_t pp) { return (pp >> 1) & 3u; }
 
 struct TravArgs {
   int32_t Lv, B0, B, K, logB0, logB;
@@ -326,16 +327,21 @@ __global__ void __launch_bounds__(TRAV_THREADS) k_traverse(const TravArgs a, con
           const float4* src = s_trav[k] + (size_t)g * n4;
           for (uint32_t j = tid; j < n4; j += TRAV_THREADS) sn[s_noff[k] + j] = __ldg(src + j);
         }
-        // the group's rays as paired records (rays 2i, 2i+1) for mt2_ns
+        // the group's rays as paired records (rays 2i, 2i+1) for mt2_ns; the
+        // four float4 of record pp sit in slots k ^ ray_swz(pp), so that the
+        // k-th load of 32 lanes at random records spreads over all eight
+        // 16-byte bank groups of a 128-byte line (unswizzled, 64-byte records
+        // put every lane on 2 of the 8 and each LDS.128 replays 16 times)
         float4* sr = reinterpret_cast<float4*>(smraw + L.off_rays);
         const float4* rs = a.sorted_rays + 2 * (size_t)g * a.group_rays;
         for (uint32_t pp = tid; pp < a.group_rays / 2u; pp += TRAV_THREADS) {
           const float4 a0 = __ldg(rs + 4 * pp), a1 = __ldg(rs + 4 * pp + 1), b0 = __ldg(rs + 4 * pp + 2),
                        b1 = __ldg(rs + 4 * pp + 3);
-          sr[4 * pp] = make_float4(a0.x, b0.x, a0.y, b0.y);
-          sr[4 * pp + 1] = make_float4(a0.z, b0.z, a0.w, b0.w);
-          sr[4 * pp + 2] = make_float4(a1.x, b1.x, a1.y, b1.y);
-          sr[4 * pp + 3] = make_float4(a1.z, b1.z, a1.w, b1.w);
+          const uint32_t sw = ray_swz(pp);
+          sr[4 * pp + (0u ^ sw)] = make_float4(a0.x, b0.x, a0.y, b0.y);
+          sr[4 * pp + (1u ^ sw)] = make_float4(a0.z, b0.z, a0.w, b0.w);
+          sr[4 * pp + (2u ^ sw)] = make_float4(a1.x, b1.x, a1.y, b1.y);
+          sr[4 * pp + (3u ^ sw)] = make_float4(a1.z, b1.z, a1.w, b1.w);
         }
       }
       if (tid == 0) { s_carry = 0u; s_carry_c = 0u; }
@@ -420,8 +426,9 @@ __global__ void __launch_bounds__(TRAV_THREADS) k_traverse(const TravArgs a, con
           const uint32_t rl = rl0 + (uint32_t)r;
           float4 A, Bq, Cq, Dq;
           if (SMALL) {
-            const float4* rp = s_rays + 2 * rl;   // paired record of rays rl, rl+1
-            A = rp[0]; Bq = rp[1]; Cq = rp[2]; Dq = rp[3];
+            const float4* rp = s_rays + 2 * rl;   // paired record of rays rl, rl+1 (swizzled slots)
+            const uint32_t sw = ray_swz(rl >> 1);
+            A = rp[0u ^ sw]; Bq = rp[1u ^ sw]; Cq = rp[2u ^ sw]; Dq = rp[3u ^ sw];
           } else {
             const float4* rs = a.sorted_rays + 2 * (rbase + rl);
             const float4 a0 = __ldg(rs), a1 = __ldg(rs + 1), b0 = __ldg(rs + 2), b1 = __ldg(rs + 3);
