@@ -261,8 +261,8 @@ struct TravSmem {
   }
 };
 
-// BT: compile-time branching factor (0 = runtime a.B)
-template <bool SMALL, int BT>
+// BT / B0T: compile-time branching factor / bundle size (0 = runtime a.B / a.B0)
+template <bool SMALL, int BT, int B0T>
 __global__ void __launch_bounds__(TRAV_THREADS) k_traverse(const TravArgs a, const TravSmem L) {
   extern __shared__ __align__(16) unsigned char smraw[];
   float4* s_top = reinterpret_cast<float4*>(smraw + L.off_top);
@@ -303,8 +303,9 @@ __global__ void __launch_bounds__(TRAV_THREADS) k_traverse(const TravArgs a, con
   if (lane <= MAX_LEVELS) qlen[lane] = 0u;
   if (tid == 0) s_cur_g = 0xFFFFFFFFu;
   const uint32_t n_items = a.fd->n_items;
-  uint32_t seg_group_start[MAX_SEG + 1];
+  uint32_t seg_group_start[MAX_SEG + 1], seg_real_end[MAX_SEG];   // real rays of segment s end at seg_real_end[s]
   for (int q = 0; q <= a.n_seg; ++q) seg_group_start[q] = a.fd->seg_pad_base[q] / a.group_rays;
+  for (int q = 0; q < a.n_seg; ++q) seg_real_end[q] = a.fd->seg_pad_base[q] + a.fd->seg_n[q];
 
   for (;;) {
     __syncthreads();
@@ -317,6 +318,15 @@ __global__ void __launch_bounds__(TRAV_THREADS) k_traverse(const TravArgs a, con
     int seg = 0;
     for (int qq = 1; qq < a.n_seg; ++qq) seg = (g >= seg_group_start[qq]) ? qq : seg;
     unsigned long long* ctr = s_ctr + seg * CTR_STRIDE;
+    // rays [0, g_real) of the group are real, the rest padding (segments are
+    // padded at their end): ray validity without loading the ray
+    uint32_t g_real = 0;
+    {
+      uint32_t se = 0;
+      for (int qq = 0; qq < a.n_seg; ++qq) se = (qq == seg) ? seg_real_end[qq] : se;
+      const uint32_t g0 = g * a.group_rays;
+      g_real = se > g0 ? min(se - g0, a.group_rays) : 0u;
+    }
 
     if (g != s_cur_g) {   // uniform: group setup (top nodes, surviving meshes, group data)
       for (int j = tid; j < 3 * K; j += TRAV_THREADS) s_top[j] = __ldg(s_trav[Lv] + (size_t)g * K * 3 + j);
@@ -412,7 +422,7 @@ __global__ void __launch_bounds__(TRAV_THREADS) k_traverse(const TravArgs a, con
     // from the end of Q[1], one per lane; the lane loads its triangle once
     // and runs Moller-Trumbore against the bundle's B0 rays
     const uint2* q1base = q + s_qoff[1];
-    const int B0 = a.B0;
+    const int B0 = B0T ? B0T : a.B0;
     auto step_mt_fn = [&]() {
       const uint32_t qk = qlen[1];
       const uint32_t n = min(qk, step_mt);
@@ -422,7 +432,11 @@ __global__ void __launch_bounds__(TRAV_THREADS) k_traverse(const TravArgs a, con
         const float4 tv0 = __ldg(te), te1 = __ldg(te + 1), te2 = __ldg(te + 2);
         const f3 v0 = mk3(tv0.x, tv0.y, tv0.z), e1 = mk3(te1.x, te1.y, te1.z), e2 = mk3(te2.x, te2.y, te2.z);
         const uint32_t rl0 = e.x << logB0;   // first ray of the bundle (B0 even)
-        for (int r = 0; r < B0; r += 2) {
+        const uint32_t nr = min((uint32_t)B0, g_real - rl0);   // real rays of the bundle (>= 1: the bundle exists)
+#pragma unroll
+        for (int r = 0; r < (B0T ? B0T : 64); r += 2) {
+          if (!B0T && r >= B0) break;
+          if ((uint32_t)r >= nr) break;
           const uint32_t rl = rl0 + (uint32_t)r;
           float4 A, Bq, Cq, Dq;
           if (SMALL) {
@@ -435,8 +449,7 @@ __global__ void __launch_bounds__(TRAV_THREADS) k_traverse(const TravArgs a, con
             A = make_float4(a0.x, b0.x, a0.y, b0.y); Bq = make_float4(a0.z, b0.z, a0.w, b0.w);
             Cq = make_float4(a1.x, b1.x, a1.y, b1.y); Dq = make_float4(a1.z, b1.z, a1.w, b1.w);
           }
-          const bool real0 = Bq.z >= 0.0f, real1 = Bq.w >= 0.0f;   // padding rays (tmin -1) come last
-          if (!real0) break;
+          const bool real1 = (uint32_t)r + 1u < nr;   // padding rays come last
           c_mt_t += 1u + (uint32_t)real1;
           bool h0, h1;
           float t0, t1;
@@ -453,7 +466,6 @@ __global__ void __launch_bounds__(TRAV_THREADS) k_traverse(const TravArgs a, con
               if (SMALL) atomicMin(s_best + rl + 1, pk); else atomicMin(a.best + rbase + rl + 1, pk);
             }
           }
-          if (!real1) break;
         }
       }
       __syncwarp();
@@ -573,6 +585,7 @@ __global__ void __launch_bounds__(TRAV_THREADS) k_traverse(const TravArgs a, con
         c_ch_t += __popc(b) * __popc(exm);
         const uint32_t cnt = __popc(m);
         c_ch_h += cnt;
+        if (__ballot_sync(CRSH_FULL, m != 0u) == 0u) continue;   // the common case: no child survived
         uint32_t incl = cnt;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -580,7 +593,6 @@ __global__ void __launch_bounds__(TRAV_THREADS) k_traverse(const TravArgs a, con
           if ((int)lane >= o) incl += y;
         }
         const uint32_t tot = __shfl_sync(CRSH_FULL, incl, 31);
-        if (tot == 0u) continue;
         const uint32_t ql0 = qlen[k1];
         uint2* qd = q + s_qoff[k1] + ql0 + (incl - cnt);
         while (m) {
