@@ -220,7 +220,7 @@ struct TravArgs {
 
 // dynamic shared-memory layout (bytes), shared by host and device
 struct TravSmem {
-  uint32_t off_top, off_exm, off_act_nmask, off_act_prefix, off_act_first, off_q, off_best, off_nodes, off_rays,
+  uint32_t off_top, off_tpairs, off_exm, off_act_nmask, off_act_prefix, off_act_first, off_q, off_best, off_nodes, off_rays,
       off_pairs, node_off[MAX_LEVELS + 1], q_off[MAX_LEVELS + 1], q_warp, total;
   __host__ __device__ static TravSmem make(int K, int B, int n_meshes, int Lv, bool small, const uint32_t* per_group,
                                            uint32_t group_rays) {
@@ -228,6 +228,7 @@ struct TravSmem {
     uint32_t o = 0;
     auto take = [&](uint32_t bytes) { const uint32_t r = o; o += (bytes + 15u) & ~15u; return r; };
     s.off_top = take(K * 48u);
+    s.off_tpairs = take(80u * ((K + 1) / 2));   // top nodes as paired records (cull2_ns); odd K: zero partner
     s.off_exm = take(4u * K);   // existing-children mask of each top node
     s.off_act_nmask = take(4u * n_meshes);
     s.off_act_prefix = take(4u * (n_meshes + 1));
@@ -263,7 +264,10 @@ struct TravSmem {
 
 // BT / B0T: compile-time branching factor / bundle size (0 = runtime a.B / a.B0)
 template <bool SMALL, int BT, int B0T>
-__global__ void __launch_bounds__(TRAV_THREADS) k_traverse(const TravArgs a, const TravSmem L) {
+#ifndef CRSH_TRAV_MINB
+#define CRSH_TRAV_MINB 3
+#endif
+__global__ void __launch_bounds__(TRAV_THREADS, CRSH_TRAV_MINB) k_traverse(const TravArgs a, const TravSmem L) {
   extern __shared__ __align__(16) unsigned char smraw[];
   float4* s_top = reinterpret_cast<float4*>(smraw + L.off_top);
   uint32_t* s_act_nmask = reinterpret_cast<uint32_t*>(smraw + L.off_act_nmask);
@@ -274,6 +278,7 @@ __global__ void __launch_bounds__(TRAV_THREADS) k_traverse(const TravArgs a, con
   const float4* s_rays = reinterpret_cast<const float4*>(smraw + L.off_rays);
   uint32_t* s_exm = reinterpret_cast<uint32_t*>(smraw + L.off_exm);
   float4* s_pairs = reinterpret_cast<float4*>(smraw + L.off_pairs);
+  float4* s_tpairs = reinterpret_cast<float4*>(smraw + L.off_tpairs);
   __shared__ uint32_t s_item, s_cur_g, s_n_act, s_carry, s_carry_c;
   __shared__ uint32_t s_warp[8];
   __shared__ unsigned long long s_ctr[MAX_SEG * CTR_STRIDE];
@@ -356,6 +361,18 @@ __global__ void __launch_bounds__(TRAV_THREADS) k_traverse(const TravArgs a, con
       }
       if (tid == 0) { s_carry = 0u; s_carry_c = 0u; }
       __syncthreads();
+      for (int jp = tid; jp < (K + 1) / 2; jp += TRAV_THREADS) {
+        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 a0 = s_top[6 * jp], a1 = s_top[6 * jp + 1], a2 = s_top[6 * jp + 2];
+        const bool has1 = 2 * jp + 1 < K;
+        const float4 b0 = has1 ? s_top[6 * jp + 3] : z, b1 = has1 ? s_top[6 * jp + 4] : z, b2 = has1 ? s_top[6 * jp + 5] : z;
+        float4* rec = s_tpairs + 5 * jp;
+        rec[0] = make_float4(a0.x, b0.x, a0.y, b0.y);
+        rec[1] = make_float4(a0.z, b0.z, a0.w, b0.w);
+        rec[2] = make_float4(a1.x, b1.x, a1.y, b1.y);
+        rec[3] = make_float4(a1.z, b1.z, a1.w, b1.w);
+        rec[4] = make_float4(a2.x, b2.x, 0.f, 0.f);
+      }
       if (Lv >= 2) {   // existing-children masks and (SMALL) paired child records
         const int k1 = Lv - 1;
         for (int j = tid; j < K; j += TRAV_THREADS) {
@@ -416,7 +433,7 @@ __global__ void __launch_bounds__(TRAV_THREADS) k_traverse(const TravArgs a, con
     __syncthreads();
     const uint32_t n_act = s_n_act;
     const size_t rbase = (size_t)g * a.group_rays;
-    uint32_t c_top_t = 0, c_top_h = 0, c_ch_t = 0, c_ch_h = 0, c_mt_t = 0, c_mt_h = 0;   // item counters (c_ch_h, c_mt_*: per lane)
+    uint32_t c_top_t = 0, c_top_h = 0, c_ch_t = 0, c_ch_h = 0, c_mt_t = 0, c_mt_h = 0;   // item counters (all but c_ch_t per lane)
 
     // final tests: one step = up to 32 (bundle, triangle) entries
     // from the end of Q[1], one per lane; the lane loads its triangle once
@@ -540,22 +557,33 @@ __global__ void __launch_bounds__(TRAV_THREADS) k_traverse(const TravArgs a, con
         nm = s_act_nmask[lo];
       }
       const f2 Px = pk2(sph.x, sph.x), Py = pk2(sph.y, sph.y), Pz = pk2(sph.z, sph.z), Pr = pk2(sph.w, sph.w);
-      for (int j = 0; j < K; ++j) {
-        const bool need = (nm >> j) & 1u;
-        const uint32_t bn = __ballot_sync(CRSH_FULL, need);
-        if (bn == 0u) continue;   // no lane's mesh kept node j
-        const float4 n0 = s_top[3 * j], n1 = s_top[3 * j + 1], n2 = s_top[3 * j + 2];
-        const bool pass = need & cull_ns(mk3(n0.x, n0.y, n0.z), n0.w, mk3(n1.x, n1.y, n1.z), n1.w, n2.x, sph);
+      // top level, all K nodes first: nodes (j, j+1) per packed test (paired
+      // records); a lane tests node j only if its triangle's mesh survived
+      // j's mesh cull. pm = the lane's passing top nodes.
+      uint32_t pm = 0;
+      for (int j = 0; j < K; j += 2) {
+        const bool n0 = (nm >> j) & 1u, n1 = (nm >> (j + 1)) & 1u;
+        if (__ballot_sync(CRSH_FULL, n0 | n1) == 0u) continue;   // no lane's mesh kept node j or j+1
+        bool p0, p1;
+        cull2_ns(s_tpairs + 5 * (j >> 1), Px, Py, Pz, Pr, p0, p1);
+        p0 &= n0;
+        p1 &= n1;
+        c_top_t += (uint32_t)n0 + (uint32_t)n1;
+        c_top_h += (uint32_t)p0 + (uint32_t)p1;
+        pm |= ((uint32_t)p0 << j) | ((uint32_t)p1 << (j + 1));
+      }
+      // then each top node that passed for some lane
+      for (uint32_t jm = __reduce_or_sync(CRSH_FULL, pm); jm; jm &= jm - 1) {
+        const int j = __ffs(jm) - 1;
+        const bool pass = (pm >> j) & 1u;
         const uint32_t b = __ballot_sync(CRSH_FULL, pass);
-        c_top_t += __popc(bn);
-        c_top_h += __popc(b);
-        if (b == 0u) continue;
         if (Lv == 1) {   // the top level is the bundle level: queue for the final tests
           const uint32_t ql = qlen[1];
           if (pass) q[s_qoff[1] + ql + __popc(b & lt)] = make_uint2((uint32_t)j, tri);
           __syncwarp();
           if (lane == 0) qlen[1] = ql + __popc(b);
           __syncwarp();
+          drain(false);   // keeps the queue below one top node's passes plus a partial step
           continue;
         }
         // dense children of node j (level Lv-1), two per packed f32x2 test;
@@ -608,6 +636,8 @@ __global__ void __launch_bounds__(TRAV_THREADS) k_traverse(const TravArgs a, con
     }
     drain(true);
     // item counters -> CTA counters (one shared atomic per counter per warp)
+    c_top_t = __reduce_add_sync(CRSH_FULL, c_top_t);
+    c_top_h = __reduce_add_sync(CRSH_FULL, c_top_h);
     c_mt_t = __reduce_add_sync(CRSH_FULL, c_mt_t);
     c_mt_h = __reduce_add_sync(CRSH_FULL, c_mt_h);
     c_ch_h = __reduce_add_sync(CRSH_FULL, c_ch_h);

@@ -247,17 +247,15 @@ __device__ __forceinline__ bool mt_ns(f3 o, f3 d, float tmin, float tmax, f3 v0,
 // each half is bit-identical to the scalar operation, so cull2_ns gives the
 // same decisions as two cull_ns calls.
 namespace crsh {
-typedef unsigned long long f2;
-__device__ __forceinline__ f2 pk2(float lo, float hi) {
-  f2 r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
-  return r;
-}
-__device__ __forceinline__ void up2(f2 v, float& lo, float& hi) { asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v)); }
-__device__ __forceinline__ f2 add2(f2 a, f2 b) { f2 d; asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b)); return d; }
-__device__ __forceinline__ f2 sub2(f2 a, f2 b) { f2 d; asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b)); return d; }
-__device__ __forceinline__ f2 mul2(f2 a, f2 b) { f2 d; asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b)); return d; }
-__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) { f2 d; asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c)); return d; }
+typedef float2 f2;
+// the sm_100 f32x2 builtins (fma/add/mul .rn.f32x2): the compiler sees them as
+// arithmetic on register pairs, so packed operands stay in aligned pairs
+__device__ __forceinline__ f2 pk2(float lo, float hi) { return make_float2(lo, hi); }
+__device__ __forceinline__ void up2(f2 v, float& lo, float& hi) { lo = v.x; hi = v.y; }
+__device__ __forceinline__ f2 add2(f2 a, f2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ f2 sub2(f2 a, f2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }   // negation is exact
+__device__ __forceinline__ f2 mul2(f2 a, f2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) { return __ffma2_rn(a, b, c); }
 
 // Paired node record (two children c, c+1), 5 x float4 in shared memory:
 // {Cx0,Cx1,Cy0,Cy1}, {Cz0,Cz1,d0,d1}, {ax0,ax1,ay0,ay1}, {az0,az1,tan0,tan1}, {sec0,sec1,-,-}
@@ -269,8 +267,8 @@ __device__ __forceinline__ void cull2_ns(const float4* rec, f2 Px, f2 Py, f2 Pz,
   const f2 ax = pk2(Cc.x, Cc.y), ay = pk2(Cc.z, Cc.w), az = pk2(D.x, D.y), tn = pk2(D.z, D.w), sc = pk2(E.x, E.y);
   const f2 vx = sub2(Px, cx), vy = sub2(Py, cy), vz = sub2(Pz, cz);
   const f2 s = fma2(vx, ax, fma2(vy, ay, mul2(vz, az)));
-  const f2 ns = mul2(s, pk2(-1.0f, -1.0f));
-  const f2 wx = fma2(ns, ax, vx), wy = fma2(ns, ay, vy), wz = fma2(ns, az, vz);
+  // w = v + s * (-a) = fma(-s, a, v) exactly (negation is exact)
+  const f2 wx = fma2(s, pk2(-Cc.x, -Cc.y), vx), wy = fma2(s, pk2(-Cc.z, -Cc.w), vy), wz = fma2(s, pk2(-D.x, -D.y), vz);
   const f2 w2 = fma2(wx, wx, fma2(wy, wy, mul2(wz, wz)));
   const f2 dr = add2(dd, R);
   float s0, s1;
@@ -287,10 +285,38 @@ __device__ __forceinline__ void cull2_ns(const float4* rec, f2 Px, f2 Py, f2 Pz,
 }  // namespace crsh
 
 namespace crsh {
+// Eq 9 for ONE node (broadcast scalars, traversal layout {C, d} {a, tan}
+// {sec, -, -, -}) against TWO target spheres packed per coordinate (Px =
+// {x_0, x_1}, ...); same operation order as cull_ns for each half. The node
+// scalars enter FFMA2/FADD2 as broadcast operands (w = v + s * (-a) equals
+// fma(-s, a, v) exactly: negation is exact).
+__device__ __forceinline__ void cull_t2_ns(float4 n0, float4 n1, float sc, f2 Px, f2 Py, f2 Pz, f2 R, bool& p0,
+                                           bool& p1) {
+  const f2 vx = sub2(Px, pk2(n0.x, n0.x)), vy = sub2(Py, pk2(n0.y, n0.y)), vz = sub2(Pz, pk2(n0.z, n0.z));
+  const f2 s = fma2(vx, pk2(n1.x, n1.x), fma2(vy, pk2(n1.y, n1.y), mul2(vz, pk2(n1.z, n1.z))));
+  const f2 wx = fma2(s, pk2(-n1.x, -n1.x), vx), wy = fma2(s, pk2(-n1.y, -n1.y), vy), wz = fma2(s, pk2(-n1.z, -n1.z), vz);
+  const f2 w2 = fma2(wx, wx, fma2(wy, wy, mul2(wz, wz)));
+  const f2 dr = add2(pk2(n0.w, n0.w), R);
+  float s0, s1;
+  up2(s, s0, s1);
+  const f2 rhs = fma2(pk2(fmaxf(s0, 0.0f), fmaxf(s1, 0.0f)), pk2(n1.w, n1.w), mul2(dr, pk2(sc, sc)));
+  const f2 rr = mul2(rhs, rhs);
+  float w0, w1, r0, r1, d0, d1;
+  up2(w2, w0, w1);
+  up2(rr, r0, r1);
+  up2(dr, d0, d1);
+  p0 = (s0 >= -d0) & (w0 <= r0);
+  p1 = (s1 >= -d1) & (w1 <= r1);
+}
+
 // Moller-Trumbore (mt_ns, same per-half operation order) for two rays given
 // as a paired record {ox0,ox1,oy0,oy1} {oz0,oz1,tmin0,tmin1}
 // {dx0,dx1,dy0,dy1} {dz0,dz1,tmax0,tmax1} against one triangle; the
 // triangle's scalars enter the packed instructions as broadcast operands.
+// EARLY: leave as soon as both rays failed a barycentric test (a warp of 32
+// lanes almost never takes that exit together, so the branch-free form, which
+// lets independent ray pairs interleave, is the default in the traversal).
+template <bool EARLY = true>
 __device__ __forceinline__ void mt2_ns(float4 A, float4 Bq, float4 Cq, float4 Dq, f3 v0, f3 e1, f3 e2, bool& h0,
                                        float& t0, bool& h1, float& t1) {
   const f2 ox = pk2(A.x, A.y), oy = pk2(A.z, A.w), oz = pk2(Bq.x, Bq.y);
@@ -311,7 +337,7 @@ __device__ __forceinline__ void mt2_ns(float4 A, float4 Bq, float4 Cq, float4 Dq
   bool k0 = (d0 != 0.0f) & (u0 >= 0.0f) & (u0 <= a0v);
   bool k1 = (d1 != 0.0f) & (u1 >= 0.0f) & (u1 <= a1v);
   h0 = h1 = false;
-  if (!(k0 | k1)) return;
+  if (EARLY && !(k0 | k1)) return;
   const f2 qx = fma2(ty, pk2(e1.z, e1.z), mul2(tz, pk2(-e1.y, -e1.y)));
   const f2 qy = fma2(tz, pk2(e1.x, e1.x), mul2(tx, pk2(-e1.z, -e1.z)));
   const f2 qz = fma2(tx, pk2(e1.y, e1.y), mul2(ty, pk2(-e1.x, -e1.x)));
@@ -322,7 +348,7 @@ __device__ __forceinline__ void mt2_ns(float4 A, float4 Bq, float4 Cq, float4 Dq
   up2(s, s0, s1);
   k0 &= (v0f >= 0.0f) & (s0 <= a0v);
   k1 &= (v1f >= 0.0f) & (s1 <= a1v);
-  if (!(k0 | k1)) return;
+  if (EARLY && !(k0 | k1)) return;
   const f2 tt = mul2(fma2(pk2(e2.x, e2.x), qx, fma2(pk2(e2.y, e2.y), qy, mul2(pk2(e2.z, e2.z), qz))),
                      pk2(1.0f / d0, 1.0f / d1));
   up2(tt, t0, t1);

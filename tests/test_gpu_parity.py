@@ -108,6 +108,19 @@ def test_micro_scenes(seed):
     assert np.array_equal(hit[ok], bt)
 
 
+@pytest.mark.parametrize("levels,leaf,branch", [(1, 8, 8), (1, 64, 4), (3, 4, 4), (3, 16, 8), (4, 8, 8), (2, 32, 2),
+                                                (2, 2, 16)])
+def test_option_space_many_triangles(levels, leaf, branch):
+    """cfg2's 70k-triangle scene at 96x96 over the option space: work items
+    of thousands of triangles (several slices per warp, queues refilled and
+    drained many times), both the shared-memory (group <= 512 rays) and the
+    global-memory group paths (span > 512), Lv 1 (top = bundle level) to 4."""
+    w = make_workload(2, width=96, height=96, levels=levels, leaf_size=leaf, branching=branch)
+    tr, hit, t, ref = run_both(w, crsh.F_SORT | crsh.F_MESH_CULL, taps=False)
+    assert np.array_equal(hit, ref["hit_tri"]) and np.array_equal(t.view(np.uint32), ref["t"].view(np.uint32))
+    assert_counts_equal(crsh.stats(tr.scene), ref)
+
+
 @pytest.mark.parametrize("flags", [3, 7])
 def test_cfg2_full_parity(flags):
     """cfg2 (512x512 SH+RE, ~70k tris / 16 meshes, Lv 2) at full size: all
