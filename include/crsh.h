@@ -103,8 +103,12 @@ typedef struct {
  *               power of 2 in [2, 32]; B0*B^(Lv-1) <= 2^22
  *   flags       CRSH_F_* bits
  *   shard_rank, shard_world  hash-range sharding: this call traverses only
- *               its contiguous range of top-node groups;
- *               world 1 = everything. */
+ *               its contiguous range of top-node groups. The
+ *               range is cut on the device at equal WORK (top-level tests
+ *               after the whole-mesh cull, which every rank runs over all
+ *               groups), the same cut on every rank, so the ranks' ranges
+ *               partition the groups and summed counters / min-merged hits
+ *               equal the world-1 result; world 1 = everything. */
 typedef struct {
   int32_t levels, leaf_size, branching;
   uint32_t flags;
@@ -196,7 +200,9 @@ enum {
   CRSH_TAP_SORTED_RAYS = 8,  /* float[8] rays (o.xyz, tmin, d.xyz, tmax) in sorted order */
   CRSH_TAP_TRI_SPHERES = 9,  /* float[4] padded triangle spheres (scene) */
   CRSH_TAP_MESH_SPHERES = 10,/* float[4] padded mesh spheres (scene) */
-  CRSH_TAP_SCENE_CONSTS = 11 /* float[8]: aabb min.xyz, max.xyz, pad, eps_t */
+  CRSH_TAP_SCENE_CONSTS = 11,/* float[8]: aabb min.xyz, max.xyz, pad, eps_t */
+  CRSH_TAP_GROUP_RANGE = 12, /* u32[3]: this rank's groups [g_lo, g_hi) and G (frame-wide) */
+  CRSH_TAP_GROUP_WORK = 13   /* u64[G]: per-group work the cut balanced (shard_world > 1 only) */
 };
 crsh_status crsh_debug_tap(crsh_scene_t scene, int32_t tap, int32_t segment, int32_t level, void* host_dst,
                            size_t cap_bytes, size_t* n_out);

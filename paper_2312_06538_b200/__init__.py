@@ -23,6 +23,7 @@ SHADOW, REFLECT, REFRACT = 1, 2, 4
 F_SORT, F_MESH_CULL, F_ZORDER, F_STAGE_TIMING, F_BRUTE, F_KERNEL_TIMING = 1, 2, 4, 8, 16, 32
 TAP_KEYS, TAP_VALS, TAP_CHUNK_KEYS, TAP_CHUNK_BASE, TAP_SORTED_KEYS, TAP_SORTED_SLOTS = 1, 2, 3, 4, 5, 6
 TAP_NODES, TAP_SORTED_RAYS, TAP_TRI_SPHERES, TAP_MESH_SPHERES, TAP_SCENE_CONSTS = 7, 8, 9, 10, 11
+TAP_GROUP_RANGE, TAP_GROUP_WORK = 12, 13
 STATUS = {0: "OK", 2: "EINVAL", 3: "EIO", 4: "ELIMIT", 5: "ENOMEM", 6: "ECUDA", 7: "ENCCL"}
 STAGES = ["generate+trim", "compress", "sort", "decompress", "build", "mesh-cull+plan", "traverse+final", "output"]
 
@@ -198,7 +199,7 @@ def launch_count(scene: Scene) -> int:
 
 
 _TAP_DTYPE = {TAP_NODES: (np.float32, 8), TAP_SORTED_RAYS: (np.float32, 8), TAP_TRI_SPHERES: (np.float32, 4),
-              TAP_MESH_SPHERES: (np.float32, 4), TAP_SCENE_CONSTS: (np.float32, 1)}
+              TAP_MESH_SPHERES: (np.float32, 4), TAP_SCENE_CONSTS: (np.float32, 1), TAP_GROUP_WORK: (np.uint64, 1)}
 
 
 def debug_tap(scene: Scene, tap: int, segment: int = 0, level: int = 1) -> np.ndarray:

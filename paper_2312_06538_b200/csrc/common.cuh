@@ -29,6 +29,7 @@ struct FrameDesc {
   uint32_t seg_C[MAX_SEG];
   uint32_t sort_tile_start[MAX_SEG + 1];
   uint32_t n_items;                    // traversal work items
+  uint32_t g_lo, g_hi;                 // this rank's traversal groups [g_lo, g_hi) (work-balanced cut, k_cut)
   uint32_t level_n[MAX_LEVELS + 1];    // padded nodes at level k
 };
 

@@ -197,13 +197,13 @@ struct FrameInfo {
 struct crsh_scene {
   int device = 0;
   int64_t M = 0;
-  int32_t n_meshes = 0;
+  int32_t n_meshes = 0, n_nonempty = 0;    // meshes / meshes with at least one triangle
   float box_min[3], box_max[3], box_ext[3], pad = 0, eps_t = 0;
   Buf tri_e, tri_sph, mesh_sph, mesh_first, mesh_count;
   std::vector<float> h_mesh_sph;
   // per-frame arena (grow-only; `gen` counts reallocations, which invalidate the graph)
   Buf rays, keys_c, vals_c, ckey, cbase, k1, v1, k2, v2, pos, first_chunk, sorted_key, sorted_slot, sorted_rays,
-      nodes, trav, masks, items, best, zero, stage_in, stage_out;
+      nodes, trav, masks, gwork, items, best, zero, stage_in, stage_out;
   uint64_t gen = 0;
   unsigned long long* h_counters = nullptr;   // pinned
   FrameDesc* h_fd = nullptr;                   // pinned
@@ -455,22 +455,36 @@ crsh_status enqueue_frame(crsh_scene* sc, const FrameInfo& fi, const crsh_primar
     CK(cudaMemsetAsync(sc->best.p, 0xFF, 8 * (size_t)fi.Np_max, st));
     {
       CullArgs a{};
-      a.fd = fd; a.K = fi.K; a.rank = fi.rank; a.world = fi.world; a.span = fi.span; a.W = W;
+      a.fd = fd; a.K = fi.K; a.W = W;
       a.trav_top = trav + 3 * fi.level_off[Lv];
       a.n_meshes = sc->n_meshes; a.mesh_sph = sc->mesh_sph.as<float4>(); a.mesh_count = sc->mesh_count.as<uint32_t>();
       a.cull_on = (fi.flags & CRSH_F_MESH_CULL) ? 1 : 0;
-      a.masks = sc->masks.as<uint32_t>(); a.counters = counters; a.n_seg = fi.n_seg;
+      a.masks = sc->masks.as<uint32_t>();
       k_mesh_cull<<<cdiv(std::max<uint64_t>(fi.G_max * fi.K * W, 1), 256), 256, 0, st>>>(a);
       CK(cudaGetLastError());
+      ++nl;
+      if (fi.world > 1) {   // work-balanced cut of the groups over the ranks
+        WorkArgs w{};
+        w.fd = fd; w.K = fi.K; w.W = W; w.n_meshes = sc->n_meshes;
+        w.masks = sc->masks.as<uint32_t>(); w.mesh_count = sc->mesh_count.as<uint32_t>();
+        w.work = sc->gwork.as<unsigned long long>();
+        k_group_work<<<cdiv(std::max<uint64_t>(fi.G_max, 1), 256), 256, 0, st>>>(w);
+        CK(cudaGetLastError());
+        ++nl;
+      }
+      k_cut<<<1, CUT_THREADS, 0, st>>>(fd, sc->gwork.as<unsigned long long>(), fi.rank, fi.world);
+      CK(cudaGetLastError());
+      ++nl;
       PlanArgs p{};
-      p.fd = fd; p.rank = fi.rank; p.world = fi.world;
-      p.K = fi.K; p.W = W; p.masks = sc->masks.as<uint32_t>();
+      p.fd = fd; p.K = fi.K; p.W = W; p.masks = sc->masks.as<uint32_t>();
+      p.group_rays = fi.GR; p.n_seg = fi.n_seg; p.trav_top = trav + 3 * fi.level_off[Lv];
+      p.cull_on = a.cull_on; p.n_nonempty = sc->n_nonempty; p.counters = counters;
       p.n_meshes = sc->n_meshes; p.mesh_count = sc->mesh_count.as<uint32_t>(); p.item_tris = ITEM_TRIS;
       p.items = sc->items.as<uint4>();
       p.status = reinterpret_cast<unsigned long long*>(zb + Z.st_plan); p.ticket = tickets + T_PLAN;
       k_plan<<<cdiv(std::max<uint64_t>(fi.G_max, 1), SCAN_TILE), SCAN_THREADS, 0, st>>>(p);
       CK(cudaGetLastError());
-      nl += 2;
+      ++nl;
     }
     CK(mark(6));
     {
@@ -505,7 +519,7 @@ crsh_status enqueue_frame(crsh_scene* sc, const FrameInfo& fi, const crsh_primar
     CK(mark(7));
     {
       UnpackArgs a{};
-      a.fd = fd; a.rank = fi.rank; a.world = fi.world; a.group_rays = fi.GR; a.n_seg = fi.n_seg;
+      a.fd = fd; a.group_rays = fi.GR; a.n_seg = fi.n_seg;
       a.sorted_slot = sc->sorted_slot.as<uint32_t>(); a.best = sc->best.as<unsigned long long>();
       a.out_hit = out_hit; a.out_t = out_t; a.out_packed = out_packed; a.counters = counters;
       k_unpack<<<cdiv(std::max<uint64_t>(fi.Np_max, 1), 256), 256, 0, st>>>(a);
@@ -618,6 +632,7 @@ crsh_status trace_impl(crsh_scene* sc, const crsh_primary_hits* h, const float* 
     CK(grow(sc, sc->nodes, 32 * total_nodes));
     CK(grow(sc, sc->trav, 48 * total_nodes));
     CK(grow(sc, sc->masks, 4 * (size_t)fi.G_max * fi.K * W + 4));
+    CK(grow(sc, sc->gwork, 8 * (size_t)fi.G_max + 8));
     CK(grow(sc, sc->best, 8 * fi.Np_max));
     CK(grow(sc, sc->items, 16 * items_cap));
   }
@@ -766,6 +781,7 @@ crsh_status crsh_scene_create(const float* tris, const int32_t* mesh_ids, int64_
   ck(cudaMemcpy(sc->mesh_sph.p, sc->h_mesh_sph.data(), 16 * (size_t)n_meshes, cudaMemcpyHostToDevice), "copy mesh_sph");
   ck(cudaMemcpy(sc->mesh_first.p, first.data(), 4 * (size_t)n_meshes, cudaMemcpyHostToDevice), "copy first");
   ck(cudaMemcpy(sc->mesh_count.p, count.data(), 4 * (size_t)n_meshes, cudaMemcpyHostToDevice), "copy count");
+  for (int32_t m = 0; m < n_meshes; ++m) sc->n_nonempty += count[m] ? 1 : 0;
   ck(cudaDeviceSynchronize(), "scene prep");
   if (rc != CRSH_OK) return bail(rc);
   *out = sc;
@@ -777,7 +793,7 @@ void crsh_scene_destroy(crsh_scene_t sc) {
   cudaSetDevice(sc->device);
   Buf* bufs[] = {&sc->tri_e, &sc->tri_sph, &sc->mesh_sph, &sc->mesh_first, &sc->mesh_count, &sc->rays, &sc->keys_c,
                  &sc->vals_c, &sc->ckey, &sc->cbase, &sc->k1, &sc->v1, &sc->k2, &sc->v2, &sc->pos, &sc->first_chunk,
-                 &sc->sorted_key, &sc->sorted_slot, &sc->sorted_rays, &sc->nodes, &sc->trav, &sc->masks, &sc->items,
+                 &sc->sorted_key, &sc->sorted_slot, &sc->sorted_rays, &sc->nodes, &sc->trav, &sc->masks, &sc->gwork, &sc->items,
                  &sc->best, &sc->zero, &sc->stage_in, &sc->stage_out};
   for (Buf* b : bufs) b->release();
   if (sc->h_counters) cudaFreeHost(sc->h_counters);
@@ -902,6 +918,17 @@ crsh_status crsh_debug_tap(crsh_scene_t sc, int32_t tap, int32_t seg_type, int32
     if (cap_bytes < sizeof c) return fail(CRSH_EIO, "buffer too small");
     std::memcpy(host_dst, c, sizeof c);
     return CRSH_OK;
+  } else if (tap == CRSH_TAP_GROUP_RANGE || tap == CRSH_TAP_GROUP_WORK) {
+    if (!fi.valid) return fail(CRSH_EINVAL, "no trace yet");
+    if (tap == CRSH_TAP_GROUP_RANGE) {
+      const uint32_t r[3] = {fd.g_lo, fd.g_hi, fd.G};
+      *n_out = 3;
+      if (cap_bytes < sizeof r) return fail(CRSH_EIO, "buffer too small");
+      std::memcpy(host_dst, r, sizeof r);
+      return CRSH_OK;
+    }
+    if (fi.world <= 1 || fi.brute) return CRSH_OK;
+    src = sc->gwork.p; n = fd.G; esz = 8;
   } else {
     if (!fi.valid) return fail(CRSH_EINVAL, "no trace yet");
     int s = -1;

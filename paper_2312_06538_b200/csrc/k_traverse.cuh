@@ -45,10 +45,13 @@ __device__ __forceinline__ unsigned long long pack_hit(float t, uint32_t tri) {
 }
 
 // ============================================================== K7
+// Eq 9 of every top node against every mesh sphere, over ALL groups (every
+// rank runs this cheap pre-pass on the whole frame: the work-balanced cut
+// below needs the work of every group); the mesh tests/hits of
+// this rank's groups are counted in k_plan.
 struct CullArgs {
-  const FrameDesc* fd;         // G, seg_pad_base -> this shard's top-node range
-  int32_t K, rank, world;
-  uint32_t span;
+  const FrameDesc* fd;         // G
+  int32_t K;
   int32_t W;                   // mask words per node = ceil(n_meshes / 32)
   const float4* trav_top;      // level Lv, traversal layout
   int32_t n_meshes;
@@ -56,59 +59,119 @@ struct CullArgs {
   const uint32_t* mesh_count;
   int32_t cull_on;
   uint32_t* masks;             // [n_top_padded][W]
-  unsigned long long* counters;
-  int32_t n_seg;
 };
 
 __global__ void __launch_bounds__(256) k_mesh_cull(const CullArgs a) {
-  __shared__ unsigned long long s_ctr[MAX_SEG][2];
-  if (threadIdx.x < MAX_SEG * 2) (&s_ctr[0][0])[threadIdx.x] = 0ull;
-  __syncthreads();
-  const uint32_t G = a.fd->G;
-  const uint32_t top_lo = (uint32_t)((uint64_t)G * a.rank / a.world) * a.K;
-  const uint32_t top_hi = (uint32_t)((uint64_t)G * (a.rank + 1) / a.world) * a.K;
+  const uint32_t n_top = a.fd->G * (uint32_t)a.K;
   const uint64_t gid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  const uint64_t total = (uint64_t)(top_hi - top_lo) * a.W;
-  if (gid < total) {
-    const uint32_t n = top_lo + (uint32_t)(gid / a.W);
-    const int w = (int)(gid % a.W);
-    const float4 p0 = __ldg(a.trav_top + 3 * (size_t)n), p1 = __ldg(a.trav_top + 3 * (size_t)n + 1),
-                 p2 = __ldg(a.trav_top + 3 * (size_t)n + 2);
-    uint32_t bits = 0, tests = 0, hits = 0;
-    if (p0.w >= 0.0f) {
-      const f3 C = mk3(p0.x, p0.y, p0.z), A = mk3(p1.x, p1.y, p1.z);
-      for (int b = 0; b < 32; ++b) {
-        const int m = w * 32 + b;
-        if (m >= a.n_meshes) break;
-        if (__ldg(a.mesh_count + m) == 0) continue;
-        if (a.cull_on) {
-          ++tests;
-          if (cull_ns(C, p0.w, A, p1.w, p2.x, __ldg(a.mesh_sph + m))) { bits |= 1u << b; ++hits; }
-        } else {
-          bits |= 1u << b;
-        }
+  if (gid >= (uint64_t)n_top * a.W) return;
+  const uint32_t n = (uint32_t)(gid / a.W);
+  const int w = (int)(gid % a.W);
+  const float4 p0 = __ldg(a.trav_top + 3 * (size_t)n), p1 = __ldg(a.trav_top + 3 * (size_t)n + 1),
+               p2 = __ldg(a.trav_top + 3 * (size_t)n + 2);
+  uint32_t bits = 0;
+  if (p0.w >= 0.0f) {   // existing node
+    const f3 C = mk3(p0.x, p0.y, p0.z), A = mk3(p1.x, p1.y, p1.z);
+    for (int b = 0; b < 32; ++b) {
+      const int m = w * 32 + b;
+      if (m >= a.n_meshes) break;
+      if (__ldg(a.mesh_count + m) == 0) continue;
+      if (!a.cull_on || cull_ns(C, p0.w, A, p1.w, p2.x, __ldg(a.mesh_sph + m))) bits |= 1u << b;
+    }
+  }
+  a.masks[(size_t)n * a.W + w] = bits;
+}
+
+// ============================================================== K7a
+// Work-balanced sharding: the work of group g is its number of
+// top-level tests, sum over its K top nodes of the triangles of the meshes
+// the node kept; rank r takes the contiguous groups whose work prefix falls
+// in [total r / world, total (r+1) / world). Every rank derives the same cut
+// from the same data, so the ranks partition the groups with no exchange.
+struct WorkArgs {
+  const FrameDesc* fd;
+  int32_t K, W, n_meshes;
+  const uint32_t* masks;
+  const uint32_t* mesh_count;
+  unsigned long long* work;    // [G]
+};
+
+__global__ void __launch_bounds__(256) k_group_work(const WorkArgs a) {
+  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= a.fd->G) return;
+  unsigned long long t = 0;
+  for (int j = 0; j < a.K; ++j)
+    for (int w = 0; w < a.W; ++w) {
+      uint32_t m = __ldg(a.masks + ((size_t)g * a.K + j) * a.W + w);
+      while (m) {
+        const int b = __ffs(m) - 1;
+        m &= m - 1;
+        t += __ldg(a.mesh_count + w * 32 + b);
       }
     }
-    a.masks[(size_t)n * a.W + w] = bits;
-    if (tests) {
-      int s = 0;
-      for (int q = 1; q < a.n_seg; ++q) s = (n >= a.fd->seg_pad_base[q] / a.span) ? q : s;
-      atomicAdd(&s_ctr[s][0], (unsigned long long)tests);
-      atomicAdd(&s_ctr[s][1], (unsigned long long)hits);
+  a.work[g] = t;
+}
+
+constexpr int CUT_THREADS = 1024;
+// one CTA: prefix of the group work, cut points of ranks rank and rank+1
+__global__ void __launch_bounds__(CUT_THREADS) k_cut(FrameDesc* fd, const unsigned long long* work, int rank, int world) {
+  const uint32_t G = fd->G;
+  if (world <= 1) {
+    if (threadIdx.x == 0) { fd->g_lo = 0u; fd->g_hi = G; }
+    return;
+  }
+  __shared__ unsigned long long s_sum[CUT_THREADS];
+  __shared__ uint32_t s_cut[2];
+  const uint32_t per = (G + CUT_THREADS - 1) / CUT_THREADS;
+  const uint32_t lo = min(G, threadIdx.x * per), hi = min(G, lo + per);
+  unsigned long long t = 0;
+  for (uint32_t g = lo; g < hi; ++g) t += work[g];
+  s_sum[threadIdx.x] = t;
+  if (threadIdx.x < 2) s_cut[threadIdx.x] = (rank + (int)threadIdx.x >= world) ? G : 0u;
+  __syncthreads();
+  for (int o = 1; o < CUT_THREADS; o <<= 1) {   // inclusive scan (Hillis-Steele)
+    const unsigned long long y = threadIdx.x >= (unsigned)o ? s_sum[threadIdx.x - o] : 0ull;
+    __syncthreads();
+    s_sum[threadIdx.x] += y;
+    __syncthreads();
+  }
+  const unsigned long long total = s_sum[CUT_THREADS - 1];
+  unsigned long long pre = threadIdx.x ? s_sum[threadIdx.x - 1] : 0ull;   // work before group lo
+  // cut(q) = min{g : P(g) >= ceil(total q / world)}, P(g) = work of groups
+  // [0, g); cut(0) = 0, cut(world) = G. The group that crosses the boundary
+  // (P(g) < target <= P(g + 1)) is owned by exactly one thread's range.
+  for (int c = 0; c < 2; ++c) {
+    const int qr = rank + c;
+    if (qr <= 0 || qr >= world) continue;
+    const unsigned long long target = (total * (unsigned long long)qr + (unsigned long long)world - 1) / (unsigned long long)world;
+    unsigned long long p = pre;
+    for (uint32_t g = lo; g < hi; ++g) {
+      const unsigned long long w = work[g];
+      if (p < target && p + w >= target) { s_cut[c] = g + 1; break; }
+      p += w;
     }
   }
   __syncthreads();
-  if (threadIdx.x < MAX_SEG * 2) {
-    const unsigned long long v = (&s_ctr[0][0])[threadIdx.x];
-    if (v) atomicAdd(a.counters + (threadIdx.x / 2) * CTR_STRIDE + CTR_MESH_TESTS + (threadIdx.x & 1), v);
+  if (threadIdx.x == 0) {
+    uint32_t c0 = s_cut[0], c1 = s_cut[1];
+    if (total == 0ull) {   // no work anywhere: split by group count
+      c0 = (uint32_t)((uint64_t)G * rank / world);
+      c1 = (uint32_t)((uint64_t)G * (rank + 1) / world);
+    }
+    fd->g_lo = c0;
+    fd->g_hi = max(c0, c1);
   }
 }
 
 // ============================================================== K7b
 struct PlanArgs {
-  FrameDesc* fd;               // G -> this shard's group range; out: n_items
-  int32_t rank, world;
+  FrameDesc* fd;               // g_lo, g_hi: this rank's group range; out: n_items
   int32_t K, W;
+  uint32_t group_rays;
+  int32_t n_seg;
+  const float4* trav_top;      // node existence (radius >= 0) for the mesh-test count
+  int32_t cull_on, n_nonempty; // meshes with triangles
+  unsigned long long* counters;
   const uint32_t* masks;
   int32_t n_meshes;
   const uint32_t* mesh_count;
@@ -124,28 +187,44 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_plan(const PlanArgs a) {
   if (threadIdx.x == 0) s_tile = atomicAdd(a.ticket, 1u);
   __syncthreads();
   const uint32_t tile = s_tile;
-  const uint32_t G = a.fd->G;
-  const uint32_t g_lo = (uint32_t)((uint64_t)G * a.rank / a.world), g_hi = (uint32_t)((uint64_t)G * (a.rank + 1) / a.world);
+  const uint32_t g_lo = a.fd->g_lo, g_hi = a.fd->g_hi;
   const uint32_t n_tiles = (g_hi - g_lo + SCAN_TILE - 1) / SCAN_TILE;
   if (tile >= n_tiles) {   // surplus block; the first one reports "no items" for an empty range
     if (tile == 0 && threadIdx.x == 0) a.fd->n_items = 0u;
     return;
   }
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  __shared__ unsigned long long s_mesh[MAX_SEG][2];
+  if (threadIdx.x < MAX_SEG * 2) (&s_mesh[0][0])[threadIdx.x] = 0ull;
+  uint32_t seg_group_start[MAX_SEG];
+  for (int q = 0; q < a.n_seg; ++q) seg_group_start[q] = a.fd->seg_pad_base[q] / a.group_rays;
+  __syncthreads();
   uint32_t ntri[SCAN_ITEMS], nit[SCAN_ITEMS], wex[SCAN_ITEMS];
 #pragma unroll
   for (int it = 0; it < SCAN_ITEMS; ++it) {
     const uint32_t g = g_lo + tile * SCAN_TILE + it * SCAN_THREADS + threadIdx.x;
     uint32_t T = 0;
     if (g < g_hi) {
+      uint32_t mt = 0, mh = 0;   // whole-mesh tests / passes of the group's top nodes
       for (int w = 0; w < a.W; ++w) {
         uint32_t m = 0;
-        for (int j = 0; j < a.K; ++j) m |= __ldg(a.masks + ((size_t)g * a.K + j) * a.W + w);
+        for (int j = 0; j < a.K; ++j) {
+          const uint32_t mj = __ldg(a.masks + ((size_t)g * a.K + j) * a.W + w);
+          m |= mj;
+          mh += __popc(mj);
+        }
         while (m) {
           const int b = __ffs(m) - 1;
           m &= m - 1;
           T += __ldg(a.mesh_count + w * 32 + b);
         }
+      }
+      if (a.cull_on) {
+        for (int j = 0; j < a.K; ++j) mt += (__ldg(&a.trav_top[3 * ((size_t)g * a.K + j)].w) >= 0.0f) ? (uint32_t)a.n_nonempty : 0u;
+        int sg = 0;
+        for (int q = 1; q < a.n_seg; ++q) sg = (g >= seg_group_start[q]) ? q : sg;
+        if (mt) atomicAdd(&s_mesh[sg][0], (unsigned long long)mt);
+        if (mh) atomicAdd(&s_mesh[sg][1], (unsigned long long)mh);
       }
     }
     const uint32_t ni = (T + a.item_tris - 1) / a.item_tris;
@@ -175,6 +254,10 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_plan(const PlanArgs a) {
     uint32_t t = 0;
     for (int q = 0; q < SCAN_ITEMS * 8; ++q) t += s_cnt[q];
     a.fd->n_items = prefix + t;
+  }
+  if (threadIdx.x < MAX_SEG * 2) {
+    const unsigned long long v = (&s_mesh[0][0])[threadIdx.x];
+    if (v) atomicAdd(a.counters + (threadIdx.x / 2) * CTR_STRIDE + CTR_MESH_TESTS + (threadIdx.x & 1), v);
   }
 }
 
@@ -734,8 +817,7 @@ __global__ void __launch_bounds__(256) k_brute(const BruteArgs a) {
 
 // ============================================================== K9
 struct UnpackArgs {
-  const FrameDesc* fd;          // G, seg_pad_base, seg_n -> this shard's sorted-ray range
-  int32_t rank, world;
+  const FrameDesc* fd;          // g_lo, g_hi, seg_pad_base, seg_n -> this rank's sorted-ray range
   uint32_t group_rays;
   int32_t n_seg;
   const uint32_t* sorted_slot;
@@ -750,9 +832,7 @@ __global__ void __launch_bounds__(256) k_unpack(const UnpackArgs a) {
   __shared__ unsigned long long s_hit[MAX_SEG];
   if (threadIdx.x < MAX_SEG) s_hit[threadIdx.x] = 0ull;
   __syncthreads();
-  const uint32_t G = a.fd->G;
-  const uint32_t r_lo = (uint32_t)((uint64_t)G * a.rank / a.world) * a.group_rays;
-  const uint32_t r_hi = (uint32_t)((uint64_t)G * (a.rank + 1) / a.world) * a.group_rays;
+  const uint32_t r_lo = a.fd->g_lo * a.group_rays, r_hi = a.fd->g_hi * a.group_rays;
   const uint32_t i = r_lo + blockIdx.x * blockDim.x + threadIdx.x;
   if (i < r_hi) {
     int s = 0;

@@ -17,8 +17,34 @@ PACK_MISS = 0x7F800000FFFFFFFF
 
 
 def group_range(G: int, rank: int, world: int):
-    """Contiguous group range of `rank` (same rule as the library)."""
+    """Contiguous group range of `rank` by group COUNT (the library's rule
+    when no group has any work)."""
     return G * rank // world, G * (rank + 1) // world
+
+
+def balanced_cut(work, rank: int, world: int):
+    """Host mirror of k_cut (include/crsh.h, shard_rank/shard_world): the
+    contiguous group range of `rank` cut at equal work. With P(g) the work of
+    groups [0, g) and T = P(G): cut(q) = min{g : P(g) >= ceil(T q / world)},
+    cut(0) = 0, cut(world) = G; rank r owns [cut(r), cut(r+1))."""
+    work = np.asarray(work, dtype=np.uint64)
+    G = len(work)
+    total = int(work.sum())
+    if world <= 1:
+        return 0, G
+    if total == 0:
+        return group_range(G, rank, world)
+    pre = np.concatenate([[0], np.cumsum(work, dtype=np.uint64)]).astype(object)
+
+    def cut(q):
+        if q <= 0:
+            return 0
+        if q >= world:
+            return G
+        target = (total * q + world - 1) // world
+        return next(g for g in range(G + 1) if pre[g] >= target)
+    lo, hi = cut(rank), cut(rank + 1)
+    return lo, max(lo, hi)
 
 
 def merge_packed(packed, group=None):

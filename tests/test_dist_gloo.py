@@ -87,3 +87,22 @@ def test_decode_matches_header_encoding():
     assert p[1] == np.int64(cd.PACK_MISS) and p[2] == cd.PACK_EMPTY and p[3] == cd.PACK_EMPTY
     h2, t2 = cd.decode_packed(p)
     assert h2.tolist() == [5, -1, -2, -2] and t2[0] == 1.5
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_balanced_cut_partitions_and_balances(seed):
+    """The work-balanced cut (host mirror of k_cut): ranges partition the
+    groups in rank order, and each rank's work is within one group's work of
+    an equal share; zero work falls back to the count split."""
+    r = np.random.default_rng(seed)
+    G = int(r.integers(1, 300))
+    work = r.integers(0, 1000, G) * (r.random(G) < 0.7)
+    for world in (1, 2, 3, 5, 8, 64):
+        rng = [cd.balanced_cut(work, q, world) for q in range(world)]
+        assert rng[0][0] == 0 and rng[-1][1] == G
+        assert all(rng[q][1] == rng[q + 1][0] for q in range(world - 1))
+        tot = int(work.sum())
+        for lo, hi in rng:
+            assert int(work[lo:hi].sum()) <= tot / world + int(work.max(initial=0))
+    assert [cd.balanced_cut(np.zeros(10), q, 3) for q in range(3)] == [(0, 3), (3, 6), (6, 10)]
+    assert [cd.balanced_cut([5, 0, 0, 5], q, 2) for q in range(2)] == [(0, 1), (1, 4)]

@@ -16,6 +16,7 @@ if not torch.cuda.is_available():
 import oracle  # noqa: E402
 import paper_2312_06538_b200 as crsh  # noqa: E402
 from paper_2312_06538_b200.api import tracer_for  # noqa: E402
+from paper_2312_06538_b200 import dist as cd  # noqa: E402
 from workloads import make_micro, make_workload  # noqa: E402
 
 SEG = {0: oracle.SH, 1: oracle.RE, 2: oracle.RR}
@@ -185,19 +186,37 @@ def test_sharded_equals_single():
     tr.run()
     hit1, t1 = tr.results()
     st1 = tr.stats()
+    Lv = w.levels
     for world in (2, 3, 8):
         merged = None
         tsum = np.zeros((3, 9), np.uint64)
+        msum = np.zeros(3, np.uint64)
+        top = []
         for rank in range(world):
             trr = tracer_for(w, shard_rank=rank, shard_world=world)
             packed = torch.empty(trr.slots, dtype=torch.int64, device="cuda")
             trr.run_packed(packed)
             merged = packed.clone() if merged is None else torch.minimum(merged, packed)
-            tsum += trr.stats()["tests"]
+            st = trr.stats()
+            tsum += st["tests"]
+            msum += np.asarray(st["mesh_tests"], np.uint64)
+            top.append(int(st["tests"][:, Lv].sum()))
+            # the device cut equals the host mirror on the device's group work,
+            # and a group's work is exactly its top-level test count
+            work = crsh.debug_tap(trr.scene, crsh.TAP_GROUP_WORK)
+            lo, hi, G = crsh.debug_tap(trr.scene, crsh.TAP_GROUP_RANGE).tolist()
+            assert len(work) == G and (lo, hi) == cd.balanced_cut(work, rank, world), (rank, world, lo, hi)
+            assert top[-1] == int(work[lo:hi].sum())
         trr.unpack(merged)
         hit, t = trr.results()
         assert np.array_equal(hit, hit1) and np.array_equal(t, t1)
         assert np.array_equal(tsum, st1["tests"])
+        assert np.array_equal(msum, np.asarray(st1["mesh_tests"], np.uint64))
+        # work-balanced cut: every rank's top-level tests within one group's
+        # worth (K top nodes x the scene) of an equal share
+        share = sum(top) / world
+        assert max(top) <= share + 8 * w.tris.shape[0], (world, top)
+        assert min(top) > 0, (world, top)
 
 
 def test_host_variant_and_determinism():
