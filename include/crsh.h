@@ -165,6 +165,22 @@ crsh_status crsh_trace_secondary(crsh_scene_t scene, const crsh_primary_hits* hi
 crsh_status crsh_trace_secondary_packed(crsh_scene_t scene, const crsh_primary_hits* hits, const float* lights,
                                         int32_t n_lights, uint32_t ray_types, const crsh_opts* opts,
                                         uint64_t* packed, void* stream);
+/* Fused multi-GPU variant ("fused variant"): the epilogue of
+ * each rank stores the packed result (encoding above) of every ray it owns
+ * straight into EVERY destination buffer in dst -- its own and its peers',
+ * e.g. the NVLink peer pointers of a symmetric allocation -- and the empty
+ * sentinel into every slot that has no ray; slots whose ray another rank owns
+ * are not touched. Each slot of each destination is thus written with its
+ * final value by exactly one rank (empty slots: the same value by all), so
+ * once all ranks' calls have completed every destination holds the merged
+ * frame with no reduction step. Ordering is the caller's: a cross-rank
+ * barrier after the calls before reading, and before the next frame writes
+ * into buffers a peer may still be reading.
+ * dst: host array of n_dst (1..8) device pointers, each [slots] uint64,
+ * writable from this scene's device. Errors: EINVAL for a bad dst. */
+crsh_status crsh_trace_secondary_peer(crsh_scene_t scene, const crsh_primary_hits* hits, const float* lights,
+                                      int32_t n_lights, uint32_t ray_types, const crsh_opts* opts,
+                                      uint64_t* const* dst, int32_t n_dst, void* stream);
 /* packed: device [slots]; hit_tri, t: device [slots] outputs. */
 crsh_status crsh_unpack_hits(crsh_scene_t scene, const uint64_t* packed, int64_t slots, int32_t* hit_tri, float* t,
                              void* stream);

@@ -79,6 +79,9 @@ def load():
     L.crsh_trace_secondary_packed.restype = st
     L.crsh_trace_secondary_packed.argtypes = [vp, C.POINTER(PrimaryHits), vp, C.c_int32, C.c_uint32,
                                               C.POINTER(Opts), vp, vp]
+    L.crsh_trace_secondary_peer.restype = st
+    L.crsh_trace_secondary_peer.argtypes = [vp, C.POINTER(PrimaryHits), vp, C.c_int32, C.c_uint32, C.POINTER(Opts),
+                                            C.POINTER(C.c_uint64), C.c_int32, vp]
     L.crsh_unpack_hits.restype = st
     L.crsh_unpack_hits.argtypes = [vp, vp, C.c_int64, vp, vp, vp]
     L.crsh_stats.restype = st
@@ -170,6 +173,15 @@ def trace_secondary_packed(scene: Scene, hits: PrimaryHits, lights, ray_types: i
     arr, n = _lights(lights)
     _check(load().crsh_trace_secondary_packed(scene.handle, C.byref(hits), arr.ctypes.data, n, ray_types,
                                               C.byref(opts), _ptr(packed), stream))
+
+
+def trace_secondary_peer(scene: Scene, hits: PrimaryHits, lights, ray_types: int, opts: Opts, dst_ptrs, stream=0):
+    """crsh_trace_secondary_peer: dst_ptrs = device addresses (ints) of the
+    packed destination buffers (own + peers')."""
+    arr, n = _lights(lights)
+    d = (C.c_uint64 * len(dst_ptrs))(*[int(x) for x in dst_ptrs])
+    _check(load().crsh_trace_secondary_peer(scene.handle, C.byref(hits), arr.ctypes.data, n, ray_types,
+                                            C.byref(opts), d, len(dst_ptrs), stream))
 
 
 def unpack_hits(scene: Scene, packed, slots: int, hit_tri, t, stream=0):

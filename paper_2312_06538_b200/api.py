@@ -7,7 +7,7 @@ import numpy as np
 import torch
 
 from . import (F_MESH_CULL, F_SORT, Scene, launch_count, load, make_hits, make_opts, num_slots, stats,
-               trace_secondary, trace_secondary_host, trace_secondary_packed, unpack_hits)
+               trace_secondary, trace_secondary_host, trace_secondary_packed, trace_secondary_peer, unpack_hits)
 
 
 class Tracer:
@@ -50,6 +50,12 @@ class Tracer:
     def run_packed(self, packed, stream=None):
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         trace_secondary_packed(self.scene, self.hits, self.lights, self.ray_types, self.opts, packed, s.cuda_stream)
+
+    def run_peer(self, dst_ptrs, stream=None):
+        """Fused multi-GPU epilogue: owned results stored into every buffer in
+        dst_ptrs (device addresses; own + NVLink peers')."""
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        trace_secondary_peer(self.scene, self.hits, self.lights, self.ray_types, self.opts, dst_ptrs, s.cuda_stream)
 
     def unpack(self, packed, stream=None):
         s = stream if stream is not None else torch.cuda.current_stream(self.device)

@@ -33,6 +33,17 @@ struct FrameDesc {
   uint32_t level_n[MAX_LEVELS + 1];    // padded nodes at level k
 };
 
+// Fused multi-GPU epilogue (crsh_trace_secondary_peer): destination packed
+// buffers (this rank's and its peers', e.g. NVLink peer pointers); n = 0 off.
+constexpr int MAX_PEERS = 8;
+struct PeerOut {
+  unsigned long long* p[MAX_PEERS];
+  int32_t n;
+  __device__ __forceinline__ void store(size_t slot, unsigned long long v) const {
+    for (int d = 0; d < n; ++d) p[d][slot] = v;
+  }
+};
+
 // k_frame_plan: padded layout from the segment counts (one warp).
 __global__ void k_frame_plan(FrameDesc* fd, int n_seg, uint32_t GR, uint32_t B0, uint32_t B, int Lv) {
   if (threadIdx.x != 0) return;

@@ -285,6 +285,7 @@ constexpr uint32_t ITEM_TRIS = 2048;   // triangles per traversal work item (loa
 // the cached one, the cached CUDA graph is replayed.
 struct CallKey {
   const void *pos, *nrm, *mat, *materials, *out_hit, *out_t, *out_packed;
+  PeerOut peer;
   int32_t W, H, n_mat, n_lights;
   float eye[3], lights[48];
   uint32_t types;
@@ -296,7 +297,7 @@ struct CallKey {
 // number of kernels launched.
 crsh_status enqueue_frame(crsh_scene* sc, const FrameInfo& fi, const crsh_primary_hits* h, const float* lights,
                           int32_t n_lights, int32_t* out_hit, float* out_t, unsigned long long* out_packed,
-                          cudaStream_t st, int64_t* n_launch) {
+                          const PeerOut& peer, cudaStream_t st, int64_t* n_launch) {
   const uint64_t S = fi.S;
   const int Lv = fi.Lv, B0 = fi.B0, B = fi.B;
   const ZeroLayout Z = ZeroLayout::make(S, fi.G_max);
@@ -331,6 +332,7 @@ crsh_status enqueue_frame(crsh_scene* sc, const FrameInfo& fi, const crsh_primar
     for (int s = 0; s <= fi.n_seg; ++s) a.seg_slot_start[s] = fi.seg_slot_start[s];
     a.rays = sc->rays.as<float4>(); a.keys_c = sc->keys_c.as<uint32_t>(); a.vals_c = sc->vals_c.as<uint32_t>();
     a.out_hit = out_packed ? nullptr : out_hit; a.out_t = out_packed ? nullptr : out_t; a.out_packed = out_packed;
+    a.peer = peer;
     a.status = reinterpret_cast<unsigned long long*>(zb + Z.st_rg); a.ticket = tickets + T_RG;
     a.fd = fd;
     k_raygen<<<cdiv(S, SCAN_TILE), SCAN_THREADS, 0, st>>>(a);
@@ -347,7 +349,7 @@ crsh_status enqueue_frame(crsh_scene* sc, const FrameInfo& fi, const crsh_primar
       BruteArgs b{};
       b.fd = fd; b.vals_c = sc->vals_c.as<uint32_t>(); b.rays = sc->rays.as<float4>(); b.tri_e = sc->tri_e.as<float4>();
       b.M = sc->M; b.n_seg = fi.n_seg;
-      b.out_hit = out_hit; b.out_t = out_t; b.out_packed = out_packed; b.counters = counters;
+      b.out_hit = out_hit; b.out_t = out_t; b.out_packed = out_packed; b.peer = peer; b.counters = counters;
       k_brute<<<cdiv(S, 256), 256, 0, st>>>(b);
       CK(cudaGetLastError());
       ++nl;
@@ -521,7 +523,7 @@ crsh_status enqueue_frame(crsh_scene* sc, const FrameInfo& fi, const crsh_primar
       UnpackArgs a{};
       a.fd = fd; a.group_rays = fi.GR; a.n_seg = fi.n_seg;
       a.sorted_slot = sc->sorted_slot.as<uint32_t>(); a.best = sc->best.as<unsigned long long>();
-      a.out_hit = out_hit; a.out_t = out_t; a.out_packed = out_packed; a.counters = counters;
+      a.out_hit = out_hit; a.out_t = out_t; a.out_packed = out_packed; a.peer = peer; a.counters = counters;
       k_unpack<<<cdiv(std::max<uint64_t>(fi.Np_max, 1), 256), 256, 0, st>>>(a);
       CK(cudaGetLastError());
       ++nl;
@@ -536,7 +538,7 @@ crsh_status enqueue_frame(crsh_scene* sc, const FrameInfo& fi, const crsh_primar
 
 crsh_status trace_impl(crsh_scene* sc, const crsh_primary_hits* h, const float* lights, int32_t n_lights,
                        uint32_t types, const crsh_opts* o, int32_t* out_hit, float* out_t,
-                       unsigned long long* out_packed, cudaStream_t st) {
+                       unsigned long long* out_packed, const PeerOut& peer, cudaStream_t st) {
   if (!sc || !h || !o) return fail(CRSH_EINVAL, "null scene / hits / opts");
   if (h->width <= 0 || h->height <= 0) return fail(CRSH_EINVAL, "width/height must be positive");
   const uint64_t P64 = (uint64_t)h->width * (uint64_t)h->height;
@@ -557,7 +559,7 @@ crsh_status trace_impl(crsh_scene* sc, const crsh_primary_hits* h, const float* 
   const int world = std::max(1, o->shard_world), rank = o->shard_rank;
   if (rank < 0 || rank >= world) return fail(CRSH_EINVAL, "bad shard rank/world");
   if ((o->flags & ~63u) != 0) return fail(CRSH_EINVAL, "unknown flags");
-  if (!out_packed && (!out_hit || !out_t)) return fail(CRSH_EINVAL, "null output");
+  if (!peer.n && !out_packed && (!out_hit || !out_t)) return fail(CRSH_EINVAL, "null output");
 
   // ---------------------------------------------------------------- static plan
   FrameInfo fi;
@@ -640,7 +642,7 @@ crsh_status trace_impl(crsh_scene* sc, const crsh_primary_hits* h, const float* 
   // ---------------------------------------------------------------- graph replay or capture
   CallKey key{};
   key.pos = h->pos; key.nrm = h->nrm; key.mat = h->mat; key.materials = h->materials;
-  key.out_hit = out_hit; key.out_t = out_t; key.out_packed = out_packed;
+  key.out_hit = out_hit; key.out_t = out_t; key.out_packed = out_packed; key.peer = peer;
   key.W = h->width; key.H = h->height; key.n_mat = h->n_mat; key.n_lights = n_lights;
   for (int i = 0; i < 3; ++i) key.eye[i] = h->eye[i];
   for (int i = 0; i < 3 * n_lights; ++i) key.lights[i] = lights[i];
@@ -650,7 +652,7 @@ crsh_status trace_impl(crsh_scene* sc, const crsh_primary_hits* h, const float* 
   static const bool use_graph = !std::getenv("CRSH_NO_GRAPH");
   if (!use_graph) {
     int64_t nl = 0;
-    crsh_status rc = enqueue_frame(sc, fi, h, lights, n_lights, out_hit, out_t, out_packed, st, &nl);
+    crsh_status rc = enqueue_frame(sc, fi, h, lights, n_lights, out_hit, out_t, out_packed, peer, st, &nl);
     if (rc != CRSH_OK) return rc;
     sc->launches = nl;
   } else {
@@ -658,7 +660,7 @@ crsh_status trace_impl(crsh_scene* sc, const crsh_primary_hits* h, const float* 
       if (sc->gexec) { cudaGraphExecDestroy(sc->gexec); sc->gexec = nullptr; }
       CK(cudaStreamBeginCapture(sc->gstream, cudaStreamCaptureModeThreadLocal));
       int64_t nl = 0;
-      crsh_status rc = enqueue_frame(sc, fi, h, lights, n_lights, out_hit, out_t, out_packed, sc->gstream, &nl);
+      crsh_status rc = enqueue_frame(sc, fi, h, lights, n_lights, out_hit, out_t, out_packed, peer, sc->gstream, &nl);
       cudaGraph_t g = nullptr;
       cudaError_t e = cudaStreamEndCapture(sc->gstream, &g);
       if (rc != CRSH_OK) { if (g) cudaGraphDestroy(g); return rc; }
@@ -808,7 +810,7 @@ void crsh_scene_destroy(crsh_scene_t sc) {
 
 crsh_status crsh_trace_secondary(crsh_scene_t sc, const crsh_primary_hits* h, const float* lights, int32_t n_lights,
                                  uint32_t types, const crsh_opts* o, int32_t* hit_tri, float* t, void* stream) {
-  return trace_impl(sc, h, lights, n_lights, types, o, hit_tri, t, nullptr, (cudaStream_t)stream);
+  return trace_impl(sc, h, lights, n_lights, types, o, hit_tri, t, nullptr, PeerOut{}, (cudaStream_t)stream);
 }
 
 crsh_status crsh_trace_secondary_packed(crsh_scene_t sc, const crsh_primary_hits* h, const float* lights,
@@ -816,7 +818,20 @@ crsh_status crsh_trace_secondary_packed(crsh_scene_t sc, const crsh_primary_hits
                                         void* stream) {
   if (!packed) return fail(CRSH_EINVAL, "packed is null");
   return trace_impl(sc, h, lights, n_lights, types, o, nullptr, nullptr,
-                    reinterpret_cast<unsigned long long*>(packed), (cudaStream_t)stream);
+                    reinterpret_cast<unsigned long long*>(packed), PeerOut{}, (cudaStream_t)stream);
+}
+
+crsh_status crsh_trace_secondary_peer(crsh_scene_t sc, const crsh_primary_hits* h, const float* lights,
+                                      int32_t n_lights, uint32_t types, const crsh_opts* o, uint64_t* const* dst,
+                                      int32_t n_dst, void* stream) {
+  if (!dst || n_dst < 1 || n_dst > MAX_PEERS) return fail(CRSH_EINVAL, "dst must hold 1..8 device pointers");
+  PeerOut peer{};
+  for (int d = 0; d < n_dst; ++d) {
+    if (!dst[d]) return fail(CRSH_EINVAL, "null destination pointer");
+    peer.p[d] = reinterpret_cast<unsigned long long*>(dst[d]);
+  }
+  peer.n = n_dst;
+  return trace_impl(sc, h, lights, n_lights, types, o, nullptr, nullptr, nullptr, peer, (cudaStream_t)stream);
 }
 
 crsh_status crsh_unpack_hits(crsh_scene_t sc, const uint64_t* packed, int64_t slots, int32_t* hit_tri, float* t,
@@ -855,7 +870,7 @@ crsh_status crsh_trace_secondary_host(crsh_scene_t sc, const crsh_primary_hits* 
   dh.pos = dpos; dh.nrm = dnrm; dh.mat = dmat; dh.materials = dmats;
   int32_t* dhit = sc->stage_out.as<int32_t>();
   float* dt = reinterpret_cast<float*>(dhit + S);
-  crsh_status rc = trace_impl(sc, &dh, lights, n_lights, types, o, dhit, dt, nullptr, st);
+  crsh_status rc = trace_impl(sc, &dh, lights, n_lights, types, o, dhit, dt, nullptr, PeerOut{}, st);
   if (rc != CRSH_OK) return rc;
   CK(cudaMemcpyAsync(hit_tri, dhit, 4 * (size_t)S, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(t, dt, 4 * (size_t)S, cudaMemcpyDeviceToHost, st));

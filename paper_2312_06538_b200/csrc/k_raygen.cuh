@@ -38,6 +38,7 @@ struct RaygenArgs {
   int32_t* out_hit;                   // optional: -2 / +inf for empty slots
   float* out_t;
   unsigned long long* out_packed;     // optional: sentinel for every slot
+  PeerOut peer;                       // optional (n > 0): sentinel for every EMPTY slot, in every destination
   unsigned long long* status;         // look-back, one word per tile
   uint32_t* ticket;
   FrameDesc* fd;                      // out: seg_comp_start[0..n_seg]
@@ -116,6 +117,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_raygen(const RaygenArgs a) {
         a.out_t[slot] = __int_as_float(0x7f800000);
       }
       if (a.out_packed) a.out_packed[slot] = 0x7FFFFFFFFFFFFFFFull;
+      if (a.peer.n && !ok) a.peer.store(slot, 0x7FFFFFFFFFFFFFFFull);   // rayed slots: written by their owner only
     }
     key[it] = k;
     ballot[it] = __ballot_sync(CRSH_FULL, ok);

@@ -756,6 +756,7 @@ struct BruteArgs {
   int32_t* out_hit;
   float* out_t;
   unsigned long long* out_packed;
+  PeerOut peer;
   unsigned long long* counters;
 };
 
@@ -799,7 +800,9 @@ __global__ void __launch_bounds__(256) k_brute(const BruteArgs a) {
     int s = 0;
     for (int q = 1; q < a.n_seg; ++q) s = (i >= a.fd->seg_comp_start[q]) ? q : s;
     const bool hit = best != BEST_NONE;
-    if (a.out_packed) {
+    if (a.peer.n) {
+      a.peer.store(slot, hit ? best : PACK_MISS);
+    } else if (a.out_packed) {
       a.out_packed[slot] = hit ? best : PACK_MISS;
     } else {
       a.out_hit[slot] = hit ? (int32_t)(uint32_t)(best & 0xFFFFFFFFull) : -1;
@@ -825,6 +828,7 @@ struct UnpackArgs {
   int32_t* out_hit;
   float* out_t;
   unsigned long long* out_packed;
+  PeerOut peer;                 // fused multi-GPU epilogue: store owned results into every destination
   unsigned long long* counters;
 };
 
@@ -841,7 +845,9 @@ __global__ void __launch_bounds__(256) k_unpack(const UnpackArgs a) {
       const uint32_t slot = __ldg(a.sorted_slot + i);
       const unsigned long long b = __ldg(a.best + i);
       const bool hit = b != BEST_NONE;
-      if (a.out_packed) {
+      if (a.peer.n) {
+        a.peer.store(slot, hit ? b : PACK_MISS);
+      } else if (a.out_packed) {
         a.out_packed[slot] = hit ? b : PACK_MISS;
       } else {
         a.out_hit[slot] = hit ? (int32_t)(uint32_t)(b & 0xFFFFFFFFull) : -1;

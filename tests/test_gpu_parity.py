@@ -219,6 +219,36 @@ def test_sharded_equals_single():
         assert min(top) > 0, (world, top)
 
 
+def test_peer_store_equals_single():
+    """Fused multi-GPU epilogue (crsh_trace_secondary_peer): each rank stores
+    its owned results into every destination (here two buffers on this GPU
+    standing for the own and a peer's window; the ranks run one after another,
+    none waits on another). Both destinations must equal the single-rank
+    packed frame, though they start as garbage: every slot is written exactly
+    once with its final value, so no reduction is needed."""
+    w = make_workload(2, width=256, height=256)
+    tr = tracer_for(w)
+    ref = torch.empty(tr.slots, dtype=torch.int64, device="cuda")
+    tr.run_packed(ref)   # world 1: every slot owned
+    st1 = tr.stats()
+    for world in (1, 2, 5):
+        dst = [torch.full((tr.slots,), 0x5A5A5A5A5A5A5A5A, dtype=torch.int64, device="cuda") for _ in range(2)]
+        tsum = np.zeros((3, 9), np.uint64)
+        for rank in range(world):
+            trr = tracer_for(w, shard_rank=rank, shard_world=world)
+            trr.run_peer([d.data_ptr() for d in dst])
+            tsum += trr.stats()["tests"]
+        torch.cuda.synchronize()
+        assert torch.equal(dst[0], ref) and torch.equal(dst[1], ref), world
+        assert np.array_equal(tsum, st1["tests"]), world
+    # brute-force engine through the same epilogue
+    trb = tracer_for(w, flags=crsh.F_BRUTE)
+    d = torch.full((trb.slots,), -1, dtype=torch.int64, device="cuda")
+    trb.run_peer([d.data_ptr()])
+    torch.cuda.synchronize()
+    assert torch.equal(d, ref)
+
+
 def test_host_variant_and_determinism():
     w = make_workload(2, width=200, height=150)
     tr = tracer_for(w)
