@@ -174,10 +174,38 @@ def run_crsh(args):
     stream = torch.cuda.current_stream()
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device="cuda")
     packed = torch.empty(max(tr.slots, 1), dtype=torch.int64, device="cuda") if world > 1 else None
+    # N > 1 merge: the fused epilogue stores each rank's owned
+    # results straight into every rank's symmetric window over NVLink
+    # (crsh_trace_secondary_peer), bracketed by device-side barriers; checked
+    # once against the NCCL MIN all-reduce merge, which it replaces (and which
+    # stays the path if the symmetric window is unavailable or disagrees).
+    merge, hdl, ptrs, sbuf = ("none" if world == 1 else "nccl"), None, None, None
+    if world > 1 and not args.nccl_merge:
+        try:
+            import torch.distributed._symmetric_memory as symm_mem
+            sbuf = symm_mem.empty(max(tr.slots, 1), dtype=torch.int64, device=torch.device("cuda", local))
+            hdl = symm_mem.rendezvous(sbuf, dist.group.WORLD)
+            ptrs = [int(hdl.buffer_ptrs[r]) for r in range(world)]
+            hdl.barrier()
+            tr.run_peer(ptrs, stream)
+            hdl.barrier()
+            tr.run_packed(packed, stream)
+            dist.all_reduce(packed, op=dist.ReduceOp.MIN)
+            ok = torch.tensor([1 if torch.equal(sbuf, packed) else 0], dtype=torch.int32, device="cuda")
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            merge = "peer" if int(ok) == 1 else "nccl"
+        except Exception as e:   # no P2P / symmetric memory on this box: keep the NCCL merge
+            print(f"[bench] fused peer merge unavailable ({type(e).__name__}: {e}); NCCL all-reduce merge", file=sys.stderr)
+            merge = "nccl"
 
     def step():
         if world == 1:
             tr.run(stream)
+        elif merge == "peer":
+            hdl.barrier()                      # every rank done reading the previous frame
+            tr.run_peer(ptrs, stream)          # owned results -> every rank's window
+            hdl.barrier()                      # all stores landed
+            tr.unpack(sbuf, stream)
         else:
             tr.run_packed(packed, stream)
             dist.all_reduce(packed, op=dist.ReduceOp.MIN)   # per-slot min-merge over NVLink
@@ -201,7 +229,7 @@ def run_crsh(args):
             ev[i][1].record(stream)
             st = tr.stats()          # synchronises; outside the event bracket
             stage += np.asarray(st["stage_ms"])
-            launches += tr.launches() + (1 if world > 1 else 0)
+            launches += tr.launches() + (1 if world > 1 else 0)   # + the unpack kernel
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -287,6 +315,8 @@ def run_crsh(args):
                    "ray_types": w.ray_types, "lights": int(w.lights.shape[0]), "levels": w.levels,
                    "leaf_size": w.leaf_size, "branching": w.branching, "hash": "zorder" if args.zorder else "R6 (SPEC layout)",
                    "parallelism": f"hash-range shard x{world}" if world > 1 else "single GPU",
+                   "merge": {"none": "none (1 GPU)", "peer": "fused peer stores into symmetric windows (NVLink)",
+                             "nccl": "NCCL MIN all-reduce"}[merge],
                    "l2": "flushed before every timed step (512 MiB write outside the event bracket)"},
         "rays_per_step": rays,
         "tests_per_ray": round((tests_all + final_all) / max(rays, 1), 2),
@@ -427,6 +457,7 @@ def main():
     ap.add_argument("--impl", default="crsh", choices=["crsh", "reference"])
     ap.add_argument("--zorder", action="store_true", help="Z-order hash layout (SURVEY §8(f) NEXT-4)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--nccl-merge", action="store_true", help="N > 1: NCCL MIN all-reduce merge instead of the fused peer stores")
     ap.add_argument("--table4", action="store_true", help="CRSH vs RAH vs N x M report (not the contract line)")
     ap.add_argument("--sweep", action="store_true", help="cfg5 depth/bundle sweep (not the contract line)")
     args = ap.parse_args()
