@@ -143,6 +143,17 @@ __device__ __forceinline__ uint32_t tile_scan_lookback(const uint32_t* s_cnt, ui
   return total;
 }
 
+// Per-segment counter add from a whole warp: lane values are summed per
+// segment with one warp reduction each and added by lane 0 -- one 64-bit
+// shared atomic per (warp, segment) instead of one contended CAS loop per
+// thread (64-bit shared atomics are CAS loops). Call with all 32 lanes.
+__device__ __forceinline__ void warp_seg_add(unsigned long long* base, int stride, int n_seg, int seg, uint32_t v) {
+  for (int q = 0; q < n_seg; ++q) {
+    const uint32_t sq = __reduce_add_sync(CRSH_FULL, seg == q ? v : 0u);
+    if (sq && (threadIdx.x & 31) == 0) atomicAdd(base + q * stride, (unsigned long long)sq);
+  }
+}
+
 // Block-wide exclusive scan of one uint32 per thread (blockDim.x == 256).
 __device__ __forceinline__ uint32_t block_excl_scan_256(uint32_t v, uint32_t* s_warp /*8*/, uint32_t* total) {
   const int lane = (int)lane_id(), warp = threadIdx.x >> 5;

@@ -203,7 +203,7 @@ struct crsh_scene {
   std::vector<float> h_mesh_sph;
   // per-frame arena (grow-only; `gen` counts reallocations, which invalidate the graph)
   Buf rays, keys_c, vals_c, ckey, cbase, k1, v1, k2, v2, pos, first_chunk, sorted_key, sorted_slot, sorted_rays,
-      nodes, trav, masks, gwork, items, best, zero, stage_in, stage_out;
+      nodes, trav, masks, gwork, gstat, items, best, zero, stage_in, stage_out;
   uint64_t gen = 0;
   unsigned long long* h_counters = nullptr;   // pinned
   FrameDesc* h_fd = nullptr;                   // pinned
@@ -465,23 +465,26 @@ crsh_status enqueue_frame(crsh_scene* sc, const FrameInfo& fi, const crsh_primar
       k_mesh_cull<<<cdiv(std::max<uint64_t>(fi.G_max * fi.K * W, 1), 256), 256, 0, st>>>(a);
       CK(cudaGetLastError());
       ++nl;
-      if (fi.world > 1) {   // work-balanced cut of the groups over the ranks (SURVEY 8(e))
+      {   // per-group triangles / mesh counters / work (one warp per group)
         WorkArgs w{};
         w.fd = fd; w.K = fi.K; w.W = W; w.n_meshes = sc->n_meshes;
         w.masks = sc->masks.as<uint32_t>(); w.mesh_count = sc->mesh_count.as<uint32_t>();
-        w.work = sc->gwork.as<unsigned long long>();
-        k_group_work<<<cdiv(std::max<uint64_t>(fi.G_max, 1), 256), 256, 0, st>>>(w);
+        w.trav_top = trav + 3 * fi.level_off[Lv]; w.cull_on = a.cull_on; w.n_nonempty = sc->n_nonempty;
+        w.work = sc->gwork.as<unsigned long long>(); w.gstat = sc->gstat.as<uint4>();
+        k_group_work<<<cdiv(std::max<uint64_t>(fi.G_max, 1), 8), 256, 0, st>>>(w);
         CK(cudaGetLastError());
         ++nl;
       }
-      k_cut<<<1, CUT_THREADS, 0, st>>>(fd, sc->gwork.as<unsigned long long>(), fi.rank, fi.world);
+      if (fi.world > 1) {   // work-balanced cut of the groups over the ranks (SURVEY 8(e))
+        k_cut<<<1, CUT_THREADS, 0, st>>>(fd, sc->gwork.as<unsigned long long>(), fi.rank, fi.world);
+      } else {
+        k_cut<<<1, 32, 0, st>>>(fd, nullptr, 0, 1);
+      }
       CK(cudaGetLastError());
       ++nl;
       PlanArgs p{};
-      p.fd = fd; p.K = fi.K; p.W = W; p.masks = sc->masks.as<uint32_t>();
-      p.group_rays = fi.GR; p.n_seg = fi.n_seg; p.trav_top = trav + 3 * fi.level_off[Lv];
-      p.cull_on = a.cull_on; p.n_nonempty = sc->n_nonempty; p.counters = counters;
-      p.n_meshes = sc->n_meshes; p.mesh_count = sc->mesh_count.as<uint32_t>(); p.item_tris = ITEM_TRIS;
+      p.fd = fd; p.group_rays = fi.GR; p.n_seg = fi.n_seg; p.gstat = sc->gstat.as<uint4>(); p.counters = counters;
+      p.item_tris = ITEM_TRIS;
       p.items = sc->items.as<uint4>();
       p.status = reinterpret_cast<unsigned long long*>(zb + Z.st_plan); p.ticket = tickets + T_PLAN;
       k_plan<<<cdiv(std::max<uint64_t>(fi.G_max, 1), SCAN_TILE), SCAN_THREADS, 0, st>>>(p);
@@ -635,6 +638,7 @@ crsh_status trace_impl(crsh_scene* sc, const crsh_primary_hits* h, const float* 
     CK(grow(sc, sc->trav, 48 * total_nodes));
     CK(grow(sc, sc->masks, 4 * (size_t)fi.G_max * fi.K * W + 4));
     CK(grow(sc, sc->gwork, 8 * (size_t)fi.G_max + 8));
+    CK(grow(sc, sc->gstat, 16 * (size_t)fi.G_max + 16));
     CK(grow(sc, sc->best, 8 * fi.Np_max));
     CK(grow(sc, sc->items, 16 * items_cap));
   }
@@ -795,7 +799,7 @@ void crsh_scene_destroy(crsh_scene_t sc) {
   cudaSetDevice(sc->device);
   Buf* bufs[] = {&sc->tri_e, &sc->tri_sph, &sc->mesh_sph, &sc->mesh_first, &sc->mesh_count, &sc->rays, &sc->keys_c,
                  &sc->vals_c, &sc->ckey, &sc->cbase, &sc->k1, &sc->v1, &sc->k2, &sc->v2, &sc->pos, &sc->first_chunk,
-                 &sc->sorted_key, &sc->sorted_slot, &sc->sorted_rays, &sc->nodes, &sc->trav, &sc->masks, &sc->gwork, &sc->items,
+                 &sc->sorted_key, &sc->sorted_slot, &sc->sorted_rays, &sc->nodes, &sc->trav, &sc->masks, &sc->gwork, &sc->gstat, &sc->items,
                  &sc->best, &sc->zero, &sc->stage_in, &sc->stage_out};
   for (Buf* b : bufs) b->release();
   if (sc->h_counters) cudaFreeHost(sc->h_counters);

@@ -93,23 +93,47 @@ struct WorkArgs {
   int32_t K, W, n_meshes;
   const uint32_t* masks;
   const uint32_t* mesh_count;
-  unsigned long long* work;    // [G]
+  const float4* trav_top;      // node existence (radius >= 0)
+  int32_t cull_on, n_nonempty;
+  unsigned long long* work;    // [G] top-level tests of the group (the cut's work)
+  uint4* gstat;                // [G] {triangles of the meshes any node kept, mesh tests, mesh passes, 0}
 };
 
+// one warp per group, lane j = top node j (K <= 32): the per-node masks are
+// combined with warp votes/reductions, so no thread walks a group serially
 __global__ void __launch_bounds__(256) k_group_work(const WorkArgs a) {
-  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= a.fd->G) return;
-  unsigned long long t = 0;
-  for (int j = 0; j < a.K; ++j)
-    for (int w = 0; w < a.W; ++w) {
-      uint32_t m = __ldg(a.masks + ((size_t)g * a.K + j) * a.W + w);
-      while (m) {
-        const int b = __ffs(m) - 1;
-        m &= m - 1;
-        t += __ldg(a.mesh_count + w * 32 + b);
-      }
+  const uint32_t g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = lane_id();
+  if (g >= a.fd->G) return;   // warp-uniform
+  const bool in = (int)lane < a.K;
+  unsigned long long work = 0;
+  uint32_t T = 0, mh = 0;
+  for (int w = 0; w < a.W; ++w) {
+    const uint32_t mj = in ? __ldg(a.masks + ((size_t)g * a.K + lane) * a.W + w) : 0u;
+    mh += __popc(mj);
+    const uint32_t u = __reduce_or_sync(CRSH_FULL, mj);   // meshes any node kept
+    uint32_t nb = 0;                                     // lane b: nodes that kept mesh w*32+b
+#pragma unroll 4
+    for (int b = 0; b < 32; ++b) {
+      const uint32_t c = __popc(__ballot_sync(CRSH_FULL, (mj >> b) & 1u));
+      nb = ((int)lane == b) ? c : nb;
     }
-  a.work[g] = t;
+    const int m = w * 32 + (int)lane;
+    const uint32_t cnt = (m < a.n_meshes) ? __ldg(a.mesh_count + m) : 0u;
+    T += ((u >> lane) & 1u) ? cnt : 0u;
+    work += (unsigned long long)nb * cnt;
+  }
+  const uint32_t ex = (in && __ldg(&a.trav_top[3 * ((size_t)g * a.K + lane)].w) >= 0.0f) ? 1u : 0u;
+  T = __reduce_add_sync(CRSH_FULL, T);
+  mh = __reduce_add_sync(CRSH_FULL, mh);
+  const uint32_t n_ex = __reduce_add_sync(CRSH_FULL, ex);
+  // 64-bit work: two 32-bit halves reduced separately
+  const uint32_t lo = __reduce_add_sync(CRSH_FULL, (uint32_t)(work & 0xFFFFu)),
+                 hi = __reduce_add_sync(CRSH_FULL, (uint32_t)(work >> 16));
+  if (lane == 0) {
+    a.work[g] = ((unsigned long long)hi << 16) + lo;
+    a.gstat[g] = make_uint4(T, a.cull_on ? n_ex * (uint32_t)a.n_nonempty : 0u, a.cull_on ? mh : 0u, 0u);
+  }
 }
 
 constexpr int CUT_THREADS = 1024;
@@ -166,15 +190,10 @@ __global__ void __launch_bounds__(CUT_THREADS) k_cut(FrameDesc* fd, const unsign
 // ============================================================== K7b
 struct PlanArgs {
   FrameDesc* fd;               // g_lo, g_hi: this rank's group range; out: n_items
-  int32_t K, W;
   uint32_t group_rays;
   int32_t n_seg;
-  const float4* trav_top;      // node existence (radius >= 0) for the mesh-test count
-  int32_t cull_on, n_nonempty; // meshes with triangles
+  const uint4* gstat;          // k_group_work: {triangles, mesh tests, mesh passes, 0} per group
   unsigned long long* counters;
-  const uint32_t* masks;
-  int32_t n_meshes;
-  const uint32_t* mesh_count;
   uint32_t item_tris;
   uint4* items;                // (group, v_begin, v_end, 0)
   unsigned long long* status;
@@ -200,31 +219,19 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_plan(const PlanArgs a) {
   for (int q = 0; q < a.n_seg; ++q) seg_group_start[q] = a.fd->seg_pad_base[q] / a.group_rays;
   __syncthreads();
   uint32_t ntri[SCAN_ITEMS], nit[SCAN_ITEMS], wex[SCAN_ITEMS];
+  uint32_t mt[MAX_SEG] = {0u, 0u, 0u}, mh[MAX_SEG] = {0u, 0u, 0u};
 #pragma unroll
   for (int it = 0; it < SCAN_ITEMS; ++it) {
     const uint32_t g = g_lo + tile * SCAN_TILE + it * SCAN_THREADS + threadIdx.x;
     uint32_t T = 0;
     if (g < g_hi) {
-      uint32_t mt = 0, mh = 0;   // whole-mesh tests / passes of the group's top nodes
-      for (int w = 0; w < a.W; ++w) {
-        uint32_t m = 0;
-        for (int j = 0; j < a.K; ++j) {
-          const uint32_t mj = __ldg(a.masks + ((size_t)g * a.K + j) * a.W + w);
-          m |= mj;
-          mh += __popc(mj);
-        }
-        while (m) {
-          const int b = __ffs(m) - 1;
-          m &= m - 1;
-          T += __ldg(a.mesh_count + w * 32 + b);
-        }
-      }
-      if (a.cull_on) {
-        for (int j = 0; j < a.K; ++j) mt += (__ldg(&a.trav_top[3 * ((size_t)g * a.K + j)].w) >= 0.0f) ? (uint32_t)a.n_nonempty : 0u;
-        int sg = 0;
-        for (int q = 1; q < a.n_seg; ++q) sg = (g >= seg_group_start[q]) ? q : sg;
-        if (mt) atomicAdd(&s_mesh[sg][0], (unsigned long long)mt);
-        if (mh) atomicAdd(&s_mesh[sg][1], (unsigned long long)mh);
+      const uint4 st = __ldg(a.gstat + g);   // whole-mesh tests / passes of the group's top nodes
+      T = st.x;
+      int sg = 0;
+      for (int q = 1; q < a.n_seg; ++q) sg = (g >= seg_group_start[q]) ? q : sg;
+      for (int q = 0; q < MAX_SEG; ++q) {
+        mt[q] += (sg == q) ? st.y : 0u;
+        mh[q] += (sg == q) ? st.z : 0u;
       }
     }
     const uint32_t ni = (T + a.item_tris - 1) / a.item_tris;
@@ -238,6 +245,10 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_plan(const PlanArgs a) {
     nit[it] = ni;
     wex[it] = incl - ni;
     if (lane == 31) s_cnt[it * 8 + warp] = incl;
+  }
+  for (int q = 0; q < a.n_seg; ++q) {
+    warp_seg_add(&s_mesh[0][0], 2, a.n_seg, q, mt[q]);
+    warp_seg_add(&s_mesh[0][1], 2, a.n_seg, q, mh[q]);
   }
   __syncthreads();
   if (warp == 0) tile_scan_lookback(s_cnt, s_excl, &s_prefix, a.status, (int)tile);
@@ -780,6 +791,8 @@ __global__ void __launch_bounds__(256) k_brute(const BruteArgs a) {
   }
   const f3 o = mk3(r0.x, r0.y, r0.z), d = mk3(r1.x, r1.y, r1.z);
   unsigned long long best = BEST_NONE;
+  int seg = 0;
+  uint32_t hv = 0;
   for (int64_t t0 = 0; t0 < a.M; t0 += 256) {
     __syncthreads();
     const int nt = (int)((a.M - t0) < 256 ? (a.M - t0) : 256);
@@ -808,13 +821,16 @@ __global__ void __launch_bounds__(256) k_brute(const BruteArgs a) {
       a.out_hit[slot] = hit ? (int32_t)(uint32_t)(best & 0xFFFFFFFFull) : -1;
       a.out_t[slot] = hit ? __uint_as_float((uint32_t)(best >> 32)) : __int_as_float(0x7f800000);
     }
-    if (hit) atomicAdd(&s_hit[s], 1ull);
-    atomicAdd(&s_tests[s], (unsigned long long)a.M);
+    seg = s;
+    hv = hit ? 1u : 0u;
   }
+  warp_seg_add(s_hit, 1, a.n_seg, seg, hv);
+  warp_seg_add(s_tests, 1, a.n_seg, seg, ok ? 1u : 0u);   // rays x M below
   __syncthreads();
   if (threadIdx.x < MAX_SEG) {
     if (s_hit[threadIdx.x]) atomicAdd(a.counters + threadIdx.x * CTR_STRIDE + CTR_RAYS_HIT, s_hit[threadIdx.x]);
-    if (s_tests[threadIdx.x]) atomicAdd(a.counters + threadIdx.x * CTR_STRIDE + CTR_FINAL_TESTS, s_tests[threadIdx.x]);
+    if (s_tests[threadIdx.x])
+      atomicAdd(a.counters + threadIdx.x * CTR_STRIDE + CTR_FINAL_TESTS, s_tests[threadIdx.x] * (unsigned long long)a.M);
   }
 }
 
@@ -838,8 +854,10 @@ __global__ void __launch_bounds__(256) k_unpack(const UnpackArgs a) {
   __syncthreads();
   const uint32_t r_lo = a.fd->g_lo * a.group_rays, r_hi = a.fd->g_hi * a.group_rays;
   const uint32_t i = r_lo + blockIdx.x * blockDim.x + threadIdx.x;
+  if (r_lo + blockIdx.x * blockDim.x >= r_hi) return;   // surplus block (uniform)
+  int s = 0;
+  uint32_t hv = 0;
   if (i < r_hi) {
-    int s = 0;
     for (int q = 1; q < a.n_seg; ++q) s = (i >= a.fd->seg_pad_base[q]) ? q : s;
     if (i - a.fd->seg_pad_base[s] < a.fd->seg_n[s]) {
       const uint32_t slot = __ldg(a.sorted_slot + i);
@@ -853,9 +871,10 @@ __global__ void __launch_bounds__(256) k_unpack(const UnpackArgs a) {
         a.out_hit[slot] = hit ? (int32_t)(uint32_t)(b & 0xFFFFFFFFull) : -1;
         a.out_t[slot] = hit ? __uint_as_float((uint32_t)(b >> 32)) : __int_as_float(0x7f800000);
       }
-      if (hit) atomicAdd(&s_hit[s], 1ull);
+      hv = hit ? 1u : 0u;
     }
   }
+  warp_seg_add(s_hit, 1, a.n_seg, s, hv);
   __syncthreads();
   if (threadIdx.x < MAX_SEG && s_hit[threadIdx.x]) atomicAdd(a.counters + threadIdx.x * CTR_STRIDE + CTR_RAYS_HIT, s_hit[threadIdx.x]);
 }
