@@ -83,8 +83,13 @@ void crsh_scene_destroy(crsh_scene_t scene);
  *   mat       [P] int32 material index, -1 = no primary hit
  *   materials [n_mat][3] float32: reflectivity, transmissivity, ior
  *   eye       camera position (view vector for reflection/refraction)
+ *   dir       optional [3][P] float32 SoA incident directions (unit), used
+ *             instead of norm(pos - eye) as the view vector i of RE/RR rays:
+ *             the vertices of a later Whitted bounce, whose incident rays
+ *             are the previous bounce's secondary rays. NULL =
+ *             the camera at `eye` (the primary G-buffer).
  * For crsh_trace_secondary these are device pointers; for
- * crsh_trace_secondary_host they are host pointers. */
+ * crsh_trace_secondary_host they are host pointers (dir must be NULL). */
 typedef struct {
   int32_t width, height;
   const float* pos;
@@ -93,6 +98,7 @@ typedef struct {
   const float* materials;
   int32_t n_mat;
   float eye[3];
+  const float* dir;
 } crsh_primary_hits;
 
 /* Hierarchy and run options.

@@ -61,8 +61,14 @@ def lib():
         L.or_scene_prep.restype = C.c_int
         L.or_scene_prep.argtypes = [vp, vp, C.c_int64, C.c_int32, vp, vp, vp, vp, vp]
         L.or_generate.restype = C.c_int64
-        L.or_generate.argtypes = [C.c_int32, vp, vp, vp, vp, C.c_int32, vp, vp, C.c_int32, C.c_uint32, vp, vp,
+        L.or_generate.argtypes = [C.c_int32, vp, vp, vp, vp, C.c_int32, vp, vp, vp, C.c_int32, C.c_uint32, vp, vp,
                                   C.c_float, C.c_uint32, vp, vp, vp]
+        L.or_shade.restype = None
+        L.or_shade.argtypes = [C.c_int32, vp, vp, vp, vp, C.c_int32, vp, vp, vp, C.c_int32, vp, vp]
+        L.or_spawn.restype = C.c_int64
+        L.or_spawn.argtypes = [C.c_int32, C.c_int32, C.c_uint32, vp, vp, vp, vp, vp, C.c_int64, vp, vp, vp, vp, vp, vp]
+        L.or_backprop.restype = None
+        L.or_backprop.argtypes = [C.c_int32, vp, vp, C.c_int32, vp, vp, vp, vp, vp]
         L.or_trim.restype = C.c_int64
         L.or_trim.argtypes = [C.c_int64, vp, vp, vp, vp, vp]
         L.or_compress.restype = C.c_int64
@@ -202,7 +208,8 @@ def generate(w, prep: ScenePrep, flags: int = 0):
     keys = np.zeros(S, np.uint32)
     empty = np.zeros(S, np.uint32)
     lib().or_generate(P, _p(_f32(w.pos)), _p(_f32(w.nrm)), _p(np.ascontiguousarray(w.mat, np.int32)),
-                      _p(_f32(w.materials)), w.materials.shape[0], _p(_f32(w.eye)), _p(_f32(w.lights)), L,
+                      _p(_f32(w.materials)), w.materials.shape[0], _p(_f32(w.eye)),
+                      _p(_f32(w.dir)) if getattr(w, "dir", None) is not None else None, _p(_f32(w.lights)), L,
                       w.ray_types, _p(prep.box_min), _p(prep.box_ext), prep.eps_t, flags, _p(rays), _p(keys), _p(empty))
     return rays, keys, empty
 
@@ -342,3 +349,71 @@ def trace(w, prep: ScenePrep | None = None, flags: int = F_SORT | F_MESH_CULL, n
     if taps:
         out["taps"] = tap
     return out
+
+
+# --------------------------------------------------------------------------
+# multi-bounce Whitted loop
+
+def whitted(w, depth: int, prep: ScenePrep | None = None, flags: int = F_SORT | F_MESH_CULL, n_threads=None):
+    """Radiance per pixel after `depth` reflection/refraction bounces.
+    Bounce d traces the vertex set V_d (V_0 = the G-buffer) with the secondary
+    pass -- shadow rays for the direct term, RE/RR rays while d < depth -- the
+    RE/RR closest hits become V_{d+1}, and L(v) = direct(v) + refl L(re child)
+    + trans L(rr child) is assembled from the deepest bounce up (or_shade,
+    or_spawn, or_backprop in oracle.cpp). Returns dict(image[P], vertices[d],
+    rays[d], stats[d])."""
+    import dataclasses
+    prep = prep or ScenePrep(w.tris, w.mesh_ids)
+    tri_mat = np.ascontiguousarray(w.tri_mat, np.int32)
+    L = w.lights.shape[0]
+    mats = _f32(w.materials)
+    n_mat = mats.shape[0]
+    cur = dict(P=w.P, pos=_f32(w.pos).reshape(3, -1), nrm=_f32(w.nrm).reshape(3, -1),
+               mat=np.ascontiguousarray(w.mat, np.int32).reshape(-1), dir=None)
+    per = []   # (mat, direct, c_re, c_rr) per bounce
+    verts, nrays, stats = [], [], []
+    for d in range(depth + 1):
+        P = cur["P"]
+        verts.append(P)
+        types = (SH if L > 0 else 0) | ((RE | RR) if d < depth else 0)
+        if P == 0 or types == 0:
+            per.append((cur["mat"], np.zeros(P, np.float32), None, None))
+            nrays.append(0); stats.append(None)
+            break
+        wd = dataclasses.replace(w, width=P, height=1, pos=cur["pos"], nrm=cur["nrm"], mat=cur["mat"],
+                                 dir=cur["dir"], ray_types=types)
+        out = trace(wd, prep, flags=flags, n_threads=n_threads)
+        nrays.append(int(sum(out["stats"]["rays"])))
+        stats.append(out["stats"])
+        hit = np.ascontiguousarray(out["hit_tri"], np.int32)
+        direct = np.zeros(P, np.float32)
+        dirp = _p(cur["dir"]) if cur["dir"] is not None else None
+        if types & SH:
+            lib().or_shade(P, _p(cur["pos"]), _p(cur["nrm"]), _p(cur["mat"]), _p(mats), n_mat, _p(_f32(w.eye)), dirp,
+                           _p(_f32(w.lights)), L, _p(hit), _p(direct))
+        if d == depth:
+            per.append((cur["mat"], direct, None, None))
+            break
+        cap = 2 * P
+        npos, nnrm, ndir = (np.zeros((3, max(cap, 1)), np.float32) for _ in range(3))
+        nmat = np.zeros(max(cap, 1), np.int32)
+        c_re, c_rr = np.zeros(P, np.int32), np.zeros(P, np.int32)
+        k = lib().or_spawn(P, L, types, _p(_f32(out["rays"])), _p(hit), _p(np.ascontiguousarray(out["t"], np.float32)),
+                           _p(prep.tri_e), _p(tri_mat), cap, _p(npos), _p(nnrm), _p(nmat), _p(ndir), _p(c_re),
+                           _p(c_rr))
+        per.append((cur["mat"], direct, c_re, c_rr))
+        # or_spawn writes SoA planes of stride k into the front of each buffer
+        cur = dict(P=int(k), pos=npos.reshape(-1)[:3 * k].reshape(3, k).copy(),
+                   nrm=nnrm.reshape(-1)[:3 * k].reshape(3, k).copy(), mat=nmat[:k].copy(),
+                   dir=ndir.reshape(-1)[:3 * k].reshape(3, k).copy())
+    # radiance, deepest bounce first
+    Lnext = np.zeros(1, np.float32)
+    for mat, direct, c_re, c_rr in reversed(per):
+        P = len(direct)
+        Lcur = np.zeros(max(P, 1), np.float32)
+        if P:
+            lib().or_backprop(P, _p(np.ascontiguousarray(mat, np.int32)), _p(mats), n_mat, _p(direct),
+                              _p(c_re) if c_re is not None else None, _p(c_rr) if c_rr is not None else None,
+                              _p(Lnext), _p(Lcur))
+        Lnext = Lcur
+    return dict(image=Lnext[:w.P].copy(), vertices=verts, rays=nrays, stats=stats)

@@ -491,9 +491,10 @@ EXPORT int or_scene_prep(const float* tris, const int32_t* mesh_ids, int64_t M, 
  * Outputs per slot: ray8 (o, tmin, d, tmax), key, empty flag (1 = no ray:
  * P:91 "a 0 or a 1, indicating if there is a ray or not, respectively"). */
 EXPORT int64_t or_generate(int32_t P, const float* pos, const float* nrm, const int32_t* mat,
-                           const float* materials, int32_t n_mat, const float* eye, const float* lights,
-                           int32_t n_lights, uint32_t types, const float* box_min, const float* box_ext,
-                           float eps_t, uint32_t flags, float* rays, uint32_t* keys, uint32_t* empty) {
+                           const float* materials, int32_t n_mat, const float* eye, const float* dir,
+                           const float* lights, int32_t n_lights, uint32_t types, const float* box_min,
+                           const float* box_ext, float eps_t, uint32_t flags, float* rays, uint32_t* keys,
+                           uint32_t* empty) {
   const bool zorder = (flags & 4u) != 0;   // CRSH_F_ZORDER
   int64_t slot = 0;
   auto fragment = [&](int32_t p) { return v3(pos[p], pos[P + p], pos[2 * (int64_t)P + p]); };
@@ -523,7 +524,9 @@ EXPORT int64_t or_generate(int32_t P, const float* pos, const float* nrm, const 
       if (mat[p] < 0 || mat[p] >= n_mat) continue;
       const float* mt = materials + 3 * mat[p];
       V3 x = fragment(p);
-      V3 i = norm3(sub(x, v3(eye[0], eye[1], eye[2])));
+      // view vector: from the camera (primary G-buffer), or the given incident
+      // direction of a later Whitted bounce
+      V3 i = dir ? v3(dir[p], dir[P + p], dir[2 * (int64_t)P + p]) : norm3(sub(x, v3(eye[0], eye[1], eye[2])));
       V3 n = normal(p);
       V3 d;
       if (type == 2) {   // reflection (mirror), emitted iff reflectivity > 0
@@ -760,4 +763,90 @@ EXPORT void or_brute(int64_t n_rays, const float* rays, int64_t M, const float* 
   for (int i = 1; i < n_threads; ++i) th.emplace_back(worker);
   worker();
   for (auto& t : th) t.join();
+}
+
+/* ---------------------------------------------------------------------------
+ * Multi-bounce Whitted loop ("accumulate
+ * shading ... output another set of secondary rays onto the ray array ... and
+ * continue"; SPEC S:514-522 shade_and_spawn, [Whi80]). A bounce is a set of
+ * VERTICES laid out like a G-buffer (pos, winding normal, material, incident
+ * direction); tracing it with crsh's secondary pass gives the shadow-ray
+ * visibility of every light and the closest hits of the reflection and
+ * refraction rays, which become the next bounce's vertices. Radiance is then
+ * assembled bottom-up:  L(v) = direct(v) + refl(v) L(re child) + trans(v) L(rr child).
+ * Readings (W1-W4): white lights of intensity 1/n_lights;
+ * diffuse weight kd = max(0, 1 - refl - trans); Lambert with the normal turned
+ * toward the incoming ray; background (miss) radiance 0.
+ * ------------------------------------------------------------------------- */
+
+/* direct term per vertex from the shadow rays of this bounce (slots l*P + v):
+ * a light counts iff its shadow ray found no occluder (hit_tri == -1). */
+EXPORT void or_shade(int32_t P, const float* pos, const float* nrm, const int32_t* mat, const float* materials,
+                     int32_t n_mat, const float* eye, const float* dir, const float* lights, int32_t n_lights,
+                     const int32_t* hit_tri, float* direct) {
+  for (int32_t v = 0; v < P; ++v) {
+    direct[v] = 0.0f;
+    if (mat[v] < 0 || mat[v] >= n_mat || n_lights <= 0) continue;
+    const float* mt = materials + 3 * mat[v];
+    const float kd = fmaxf(0.0f, (1.0f - mt[0]) - mt[1]);
+    V3 x = v3(pos[v], pos[P + v], pos[2 * (int64_t)P + v]);
+    V3 n = v3(nrm[v], nrm[P + v], nrm[2 * (int64_t)P + v]);
+    V3 i = dir ? v3(dir[v], dir[P + v], dir[2 * (int64_t)P + v]) : norm3(sub(x, v3(eye[0], eye[1], eye[2])));
+    if (dot3(i, n) > 0.0f) n = neg(n);   // face the incoming side
+    float acc = 0.0f;
+    for (int32_t l = 0; l < n_lights; ++l) {
+      if (hit_tri[(int64_t)l * P + v] != -1) continue;   // occluded
+      V3 lv = sub(v3(lights[3 * l], lights[3 * l + 1], lights[3 * l + 2]), x);
+      const float len = len3(lv);
+      const float c = dot3(n, lv);
+      if (c > 0.0f && len > 0.0f) acc = acc + c / len;
+    }
+    direct[v] = (kd * acc) * (1.0f / (float)n_lights);
+  }
+}
+
+/* next bounce's vertices from this bounce's RE / RR closest hits, in vertex
+ * order (RE child before RR child): pos = o + t d (fma per axis), normal =
+ * norm(e1 x e2) of the hit triangle, material of the triangle, incident
+ * direction d. c_re / c_rr: child index or -1. Returns the vertex count. */
+EXPORT int64_t or_spawn(int32_t P, int32_t n_lights, uint32_t types, const float* rays, const int32_t* hit_tri,
+                        const float* t, const float* tri_e, const int32_t* tri_mat, int64_t cap, float* npos,
+                        float* nnrm, int32_t* nmat, float* ndir, int32_t* c_re, int32_t* c_rr) {
+  const int64_t sh = (types & 1u) ? (int64_t)n_lights * P : 0;
+  const int64_t re0 = sh, rr0 = sh + ((types & 2u) ? P : 0);
+  int64_t k = 0;
+  std::vector<int64_t> src;   // slot of each child
+  for (int32_t v = 0; v < P; ++v) {
+    c_re[v] = c_rr[v] = -1;
+    if ((types & 2u) && hit_tri[re0 + v] >= 0) { c_re[v] = (int32_t)k++; src.push_back(re0 + v); }
+    if ((types & 4u) && hit_tri[rr0 + v] >= 0) { c_rr[v] = (int32_t)k++; src.push_back(rr0 + v); }
+  }
+  if (k > cap) return -1;
+  for (int64_t c = 0; c < k; ++c) {
+    const int64_t s = src[c];
+    const float* r = rays + 8 * s;
+    const float th = t[s];
+    const int32_t tri = hit_tri[s];
+    const float* te = tri_e + 9 * (int64_t)tri;
+    V3 nn = norm3(cross3(v3(te[3], te[4], te[5]), v3(te[6], te[7], te[8])));
+    npos[c] = fmaf(th, r[4], r[0]); npos[k + c] = fmaf(th, r[5], r[1]); npos[2 * k + c] = fmaf(th, r[6], r[2]);
+    nnrm[c] = nn.x; nnrm[k + c] = nn.y; nnrm[2 * k + c] = nn.z;
+    ndir[c] = r[4]; ndir[k + c] = r[5]; ndir[2 * k + c] = r[6];
+    nmat[c] = tri_mat[tri];
+  }
+  return k;
+}
+
+/* L(v) = direct(v), then + refl L(re child), then + trans L(rr child) (fma). */
+EXPORT void or_backprop(int32_t P, const int32_t* mat, const float* materials, int32_t n_mat, const float* direct,
+                        const int32_t* c_re, const int32_t* c_rr, const float* L_next, float* L) {
+  for (int32_t v = 0; v < P; ++v) {
+    float r = direct[v];
+    if (mat[v] >= 0 && mat[v] < n_mat) {
+      const float* mt = materials + 3 * mat[v];
+      if (c_re && c_re[v] >= 0) r = fmaf(mt[0], L_next[c_re[v]], r);
+      if (c_rr && c_rr[v] >= 0) r = fmaf(mt[1], L_next[c_rr[v]], r);
+    }
+    L[v] = r;
+  }
 }

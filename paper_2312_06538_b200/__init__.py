@@ -36,7 +36,8 @@ class CrshError(RuntimeError):
 
 class PrimaryHits(C.Structure):
     _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("pos", C.c_void_p), ("nrm", C.c_void_p),
-                ("mat", C.c_void_p), ("materials", C.c_void_p), ("n_mat", C.c_int32), ("eye", C.c_float * 3)]
+                ("mat", C.c_void_p), ("materials", C.c_void_p), ("n_mat", C.c_int32), ("eye", C.c_float * 3),
+                ("dir", C.c_void_p)]
 
 
 class Opts(C.Structure):
@@ -140,12 +141,13 @@ class Scene:
             pass
 
 
-def make_hits(width, height, pos, nrm, mat, materials, n_mat, eye) -> PrimaryHits:
+def make_hits(width, height, pos, nrm, mat, materials, n_mat, eye, dir=None) -> PrimaryHits:
     h = PrimaryHits()
     h.width, h.height = width, height
     h.pos, h.nrm, h.mat, h.materials = _ptr(pos), _ptr(nrm), _ptr(mat), _ptr(materials)
     h.n_mat = n_mat
     h.eye = (C.c_float * 3)(*[float(x) for x in eye])
+    h.dir = _ptr(dir) if dir is not None else None
     return h
 
 

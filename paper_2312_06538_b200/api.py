@@ -22,7 +22,7 @@ class Tracer:
         self.M = int(t.shape[0])
         self.gbuf = None
 
-    def set_gbuffer(self, width, height, pos, nrm, mat, materials, eye):
+    def set_gbuffer(self, width, height, pos, nrm, mat, materials, eye, dir=None):
         d = self.device
         self.width, self.height = width, height
         self.pos = torch.as_tensor(np.ascontiguousarray(pos, np.float32)).to(d)
@@ -30,8 +30,9 @@ class Tracer:
         self.mat = torch.as_tensor(np.ascontiguousarray(mat, np.int32)).to(d)
         self.materials = torch.as_tensor(np.ascontiguousarray(materials, np.float32)).to(d)
         self.eye = [float(x) for x in eye]
+        self.dir = None if dir is None else torch.as_tensor(np.ascontiguousarray(dir, np.float32)).to(d)
         self.hits = make_hits(width, height, self.pos, self.nrm, self.mat, self.materials,
-                              int(self.materials.shape[0]), self.eye)
+                              int(self.materials.shape[0]), self.eye, self.dir)
 
     def configure(self, lights, ray_types, levels=2, leaf_size=8, branching=8, flags=F_SORT | F_MESH_CULL,
                   shard_rank=0, shard_world=1):
@@ -81,6 +82,6 @@ class Tracer:
 def tracer_for(w, device: int = 0, flags=F_SORT | F_MESH_CULL, **kw) -> Tracer:
     """Tracer set up from a workloads.Workload."""
     tr = Tracer(w.tris, w.mesh_ids, device)
-    tr.set_gbuffer(w.width, w.height, w.pos, w.nrm, w.mat, w.materials, w.eye)
+    tr.set_gbuffer(w.width, w.height, w.pos, w.nrm, w.mat, w.materials, w.eye, getattr(w, "dir", None))
     tr.configure(w.lights, w.ray_types, w.levels, w.leaf_size, w.branching, flags, **kw)
     return tr

@@ -284,7 +284,7 @@ constexpr uint32_t ITEM_TRIS = 2048;   // triangles per traversal work item (loa
 // Everything a frame's launch sequence depends on: if the key of a call equals
 // the cached one, the cached CUDA graph is replayed.
 struct CallKey {
-  const void *pos, *nrm, *mat, *materials, *out_hit, *out_t, *out_packed;
+  const void *pos, *nrm, *mat, *materials, *dir, *out_hit, *out_t, *out_packed;
   PeerOut peer;
   int32_t W, H, n_mat, n_lights;
   float eye[3], lights[48];
@@ -324,6 +324,7 @@ crsh_status enqueue_frame(crsh_scene* sc, const FrameInfo& fi, const crsh_primar
     a.P = h->width * h->height; a.pos = h->pos; a.nrm = h->nrm; a.mat = h->mat; a.materials = h->materials;
     a.n_mat = h->n_mat;
     for (int i = 0; i < 3; ++i) a.eye[i] = h->eye[i];
+    a.dir = h->dir;
     for (int i = 0; i < 3 * n_lights; ++i) a.lights[i] = lights[i];
     a.n_lights = n_lights; a.zorder = (fi.flags & CRSH_F_ZORDER) ? 1 : 0;
     for (int i = 0; i < 3; ++i) { a.box_min[i] = sc->box_min[i]; a.box_ext[i] = sc->box_ext[i]; }
@@ -645,7 +646,7 @@ crsh_status trace_impl(crsh_scene* sc, const crsh_primary_hits* h, const float* 
 
   // ---------------------------------------------------------------- graph replay or capture
   CallKey key{};
-  key.pos = h->pos; key.nrm = h->nrm; key.mat = h->mat; key.materials = h->materials;
+  key.pos = h->pos; key.nrm = h->nrm; key.mat = h->mat; key.materials = h->materials; key.dir = h->dir;
   key.out_hit = out_hit; key.out_t = out_t; key.out_packed = out_packed; key.peer = peer;
   key.W = h->width; key.H = h->height; key.n_mat = h->n_mat; key.n_lights = n_lights;
   for (int i = 0; i < 3; ++i) key.eye[i] = h->eye[i];
@@ -858,6 +859,7 @@ crsh_status crsh_trace_secondary_host(crsh_scene_t sc, const crsh_primary_hits* 
   const size_t P = (size_t)h->width * h->height;
   const int64_t S = crsh_num_slots((int32_t)P, n_lights, types);
   cudaStream_t st = (cudaStream_t)stream;
+  if (h->dir) return fail(CRSH_EINVAL, "dir must be NULL for crsh_trace_secondary_host");
   const size_t in_bytes = 28 * P + 12 * (size_t)std::max(h->n_mat, 0);
   CK(ensure(sc->stage_in, in_bytes + 64));
   CK(ensure(sc->stage_out, 8 * (size_t)std::max<int64_t>(S, 1)));

@@ -23,6 +23,7 @@ struct RaygenArgs {
   const float* materials;
   int32_t n_mat;
   float eye[3];
+  const float* dir;                   // optional [3][P] incident directions (Whitted bounce > 0)
   float lights[16 * 3];
   int32_t n_lights;
   int32_t zorder;
@@ -69,7 +70,8 @@ __device__ __forceinline__ bool gen_ray(const RaygenArgs& a, uint32_t slot, floa
     return true;
   }
   const float refl = __ldg(a.materials + 3 * m), trans = __ldg(a.materials + 3 * m + 1);
-  const f3 i = norm3(x - mk3(a.eye[0], a.eye[1], a.eye[2]));
+  const f3 i = a.dir ? mk3(__ldg(a.dir + p), __ldg(a.dir + P + p), __ldg(a.dir + 2 * P + p))
+                     : norm3(x - mk3(a.eye[0], a.eye[1], a.eye[2]));
   f3 n = mk3(__ldg(a.nrm + p), __ldg(a.nrm + P + p), __ldg(a.nrm + 2 * P + p));
   f3 d;
   if (type == 1) {   // reflection, iff reflectivity > 0

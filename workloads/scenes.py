@@ -64,6 +64,7 @@ class Workload:
     leaf_size: int = 8
     branching: int = 8
     meta: dict = field(default_factory=dict)
+    dir: np.ndarray | None = None   # [3, P] float32 incident directions (Whitted bounce > 0), None = from eye
 
     @property
     def P(self) -> int:
