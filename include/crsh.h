@@ -187,6 +187,38 @@ crsh_status crsh_trace_secondary_packed(crsh_scene_t scene, const crsh_primary_h
 crsh_status crsh_trace_secondary_peer(crsh_scene_t scene, const crsh_primary_hits* hits, const float* lights,
                                       int32_t n_lights, uint32_t ray_types, const crsh_opts* opts,
                                       uint64_t* const* dst, int32_t n_dst, void* stream);
+/* Multi-bounce Whitted rendering on top of the secondary pass (SURVEY §8(f)
+ * NEXT-2; "accumulate shading ... output another set of secondary
+ * rays onto the ray array that we used initially and continue"; [Whi80]).
+ * Bounce d traces a vertex set V_d (V_0 = gbuf) with crsh_trace_secondary's
+ * pipeline: shadow rays to every light give the direct term, and while
+ * d < depth the reflection / refraction rays' closest hits become V_{d+1}
+ * (hit point o + t d, winding normal of the hit triangle, its material,
+ * incident direction d -- the `dir` field of the next bounce's buffer). The
+ * radiance is then assembled from the deepest bounce up:
+ *   L(v) = kd sum_l vis_l max(0, n.l_hat) / n_lights
+ *          + refl L(reflection child) + trans L(refraction child),
+ *   kd = max(0, 1 - refl - trans), n turned toward the incoming ray,
+ *   white lights, background 0 (readings W1-W4).
+ *   gbuf      device G-buffer of the pixels (bounce 0), as crsh_trace_secondary
+ *   tri_mat   device [M] int32 material index of every triangle
+ *   depth     reflection/refraction bounces, 0..8 (0 = direct light only)
+ *   opts      hierarchy options and flags (one rank; no CRSH_F_BRUTE)
+ *   image     device [P] float32 out: radiance per pixel (0 where mat < 0)
+ *   stats     optional host out: per-bounce vertices, rays, tests
+ * Synchronises `stream` once per bounce (the next vertex count). */
+#define CRSH_MAX_BOUNCES 8
+typedef struct {
+  int32_t bounces, reserved;
+  int64_t vertices[CRSH_MAX_BOUNCES + 1];     /* vertices of bounce d */
+  int64_t rays[CRSH_MAX_BOUNCES + 1];         /* non-empty rays traced at bounce d */
+  uint64_t tests[CRSH_MAX_BOUNCES + 1];       /* ray-node tests (all levels) at bounce d */
+  uint64_t final_tests[CRSH_MAX_BOUNCES + 1]; /* Moller-Trumbore tests at bounce d */
+} crsh_whitted_stats_t;
+crsh_status crsh_render_whitted(crsh_scene_t scene, const crsh_primary_hits* gbuf, const float* lights,
+                                int32_t n_lights, const int32_t* tri_mat, int32_t depth, const crsh_opts* opts,
+                                float* image, crsh_whitted_stats_t* stats, void* stream);
+
 /* packed: device [slots]; hit_tri, t: device [slots] outputs. */
 crsh_status crsh_unpack_hits(crsh_scene_t scene, const uint64_t* packed, int64_t slots, int32_t* hit_tri, float* t,
                              void* stream);

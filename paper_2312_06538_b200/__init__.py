@@ -40,6 +40,11 @@ class PrimaryHits(C.Structure):
                 ("dir", C.c_void_p)]
 
 
+class WhittedStats(C.Structure):
+    _fields_ = [("bounces", C.c_int32), ("reserved", C.c_int32), ("vertices", C.c_int64 * 9), ("rays", C.c_int64 * 9),
+                ("tests", C.c_uint64 * 9), ("final_tests", C.c_uint64 * 9)]
+
+
 class Opts(C.Structure):
     _fields_ = [("levels", C.c_int32), ("leaf_size", C.c_int32), ("branching", C.c_int32), ("flags", C.c_uint32),
                 ("shard_rank", C.c_int32), ("shard_world", C.c_int32)]
@@ -83,6 +88,9 @@ def load():
     L.crsh_trace_secondary_peer.restype = st
     L.crsh_trace_secondary_peer.argtypes = [vp, C.POINTER(PrimaryHits), vp, C.c_int32, C.c_uint32, C.POINTER(Opts),
                                             C.POINTER(C.c_uint64), C.c_int32, vp]
+    L.crsh_render_whitted.restype = st
+    L.crsh_render_whitted.argtypes = [vp, C.POINTER(PrimaryHits), vp, C.c_int32, vp, C.c_int32, C.POINTER(Opts), vp,
+                                      C.POINTER(WhittedStats), vp]
     L.crsh_unpack_hits.restype = st
     L.crsh_unpack_hits.argtypes = [vp, vp, C.c_int64, vp, vp, vp]
     L.crsh_stats.restype = st
@@ -184,6 +192,18 @@ def trace_secondary_peer(scene: Scene, hits: PrimaryHits, lights, ray_types: int
     d = (C.c_uint64 * len(dst_ptrs))(*[int(x) for x in dst_ptrs])
     _check(load().crsh_trace_secondary_peer(scene.handle, C.byref(hits), arr.ctypes.data, n, ray_types,
                                             C.byref(opts), d, len(dst_ptrs), stream))
+
+
+def render_whitted(scene: Scene, hits: PrimaryHits, lights, tri_mat, depth: int, opts: Opts, image, stream=0) -> dict:
+    """crsh_render_whitted: radiance per pixel after `depth` bounces into the
+    device buffer `image` [P] float32; returns the per-bounce stats."""
+    arr, n = _lights(lights)
+    ws = WhittedStats()
+    _check(load().crsh_render_whitted(scene.handle, C.byref(hits), arr.ctypes.data, n, _ptr(tri_mat), depth,
+                                      C.byref(opts), _ptr(image), C.byref(ws), stream))
+    d = ws.bounces
+    return dict(vertices=list(ws.vertices)[:d + 1], rays=list(ws.rays)[:d + 1], tests=list(ws.tests)[:d + 1],
+                final_tests=list(ws.final_tests)[:d + 1])
 
 
 def unpack_hits(scene: Scene, packed, slots: int, hit_tri, t, stream=0):

@@ -7,7 +7,8 @@ import numpy as np
 import torch
 
 from . import (F_MESH_CULL, F_SORT, Scene, launch_count, load, make_hits, make_opts, num_slots, stats,
-               trace_secondary, trace_secondary_host, trace_secondary_packed, trace_secondary_peer, unpack_hits)
+               render_whitted, trace_secondary, trace_secondary_host, trace_secondary_packed, trace_secondary_peer,
+               unpack_hits)
 
 
 class Tracer:
@@ -57,6 +58,18 @@ class Tracer:
         dst_ptrs (device addresses; own + NVLink peers')."""
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         trace_secondary_peer(self.scene, self.hits, self.lights, self.ray_types, self.opts, dst_ptrs, s.cuda_stream)
+
+    def render(self, tri_mat, depth: int, stream=None):
+        """Multi-bounce Whitted image (crsh_render_whitted) of the G-buffer set
+        by set_gbuffer, with the lights / options of configure; returns
+        (image [P] float32 tensor, per-bounce stats)."""
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        if getattr(self, "_tri_mat_src", None) is not tri_mat:
+            self._tri_mat = torch.as_tensor(np.ascontiguousarray(tri_mat, np.int32)).to(self.device)
+            self._tri_mat_src = tri_mat
+        img = torch.empty(max(self.width * self.height, 1), dtype=torch.float32, device=self.device)
+        st = render_whitted(self.scene, self.hits, self.lights, self._tri_mat, depth, self.opts, img, s.cuda_stream)
+        return img, st
 
     def unpack(self, packed, stream=None):
         s = stream if stream is not None else torch.cuda.current_stream(self.device)

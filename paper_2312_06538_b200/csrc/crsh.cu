@@ -19,6 +19,7 @@
 #include "k_raygen.cuh"
 #include "k_sort.cuh"
 #include "k_traverse.cuh"
+#include "k_whitted.cuh"
 
 using namespace crsh;
 
@@ -217,6 +218,9 @@ struct crsh_scene {
   std::vector<unsigned char> gkey;
   int64_t graph_launches = 0;                  // kernels inside the cached graph
   int sm_count = 148;
+  // multi-bounce Whitted loop (crsh_render_whitted): per-bounce vertex sets and terms
+  std::vector<std::array<Buf, 8>> wb;   // pos, nrm, dir, mat, direct, c_re, c_rr, L
+  Buf w_hit, w_t, w_zero;
 };
 
 namespace {
@@ -293,6 +297,24 @@ struct CallKey {
   uint64_t gen;
 };
 
+// The ray-definition part of K1's arguments (G-buffer, lights, slot layout);
+// also used by the Whitted loop to regenerate a traced ray bit for bit.
+RaygenArgs raygen_def(const crsh_scene* sc, const FrameInfo& fi, const crsh_primary_hits* h, const float* lights,
+                      int32_t n_lights) {
+  RaygenArgs a{};
+  a.P = h->width * h->height; a.pos = h->pos; a.nrm = h->nrm; a.mat = h->mat; a.materials = h->materials;
+  a.n_mat = h->n_mat;
+  for (int i = 0; i < 3; ++i) a.eye[i] = h->eye[i];
+  a.dir = h->dir;
+  for (int i = 0; i < 3 * n_lights; ++i) a.lights[i] = lights[i];
+  a.n_lights = n_lights; a.zorder = (fi.flags & CRSH_F_ZORDER) ? 1 : 0;
+  for (int i = 0; i < 3; ++i) { a.box_min[i] = sc->box_min[i]; a.box_ext[i] = sc->box_ext[i]; }
+  a.eps_t = sc->eps_t; a.n_slots = (uint32_t)fi.S; a.n_seg = fi.n_seg;
+  for (int s = 0; s < fi.n_seg; ++s) a.seg_type[s] = fi.seg_type[s];
+  for (int s = 0; s <= fi.n_seg; ++s) a.seg_slot_start[s] = fi.seg_slot_start[s];
+  return a;
+}
+
 // Enqueue one frame on `st` (directly or under graph capture). Returns the
 // number of kernels launched.
 crsh_status enqueue_frame(crsh_scene* sc, const FrameInfo& fi, const crsh_primary_hits* h, const float* lights,
@@ -320,17 +342,7 @@ crsh_status enqueue_frame(crsh_scene* sc, const FrameInfo& fi, const crsh_primar
 
   // ---------------------------------------------------------------- K1: generate + hash + trim
   {
-    RaygenArgs a{};
-    a.P = h->width * h->height; a.pos = h->pos; a.nrm = h->nrm; a.mat = h->mat; a.materials = h->materials;
-    a.n_mat = h->n_mat;
-    for (int i = 0; i < 3; ++i) a.eye[i] = h->eye[i];
-    a.dir = h->dir;
-    for (int i = 0; i < 3 * n_lights; ++i) a.lights[i] = lights[i];
-    a.n_lights = n_lights; a.zorder = (fi.flags & CRSH_F_ZORDER) ? 1 : 0;
-    for (int i = 0; i < 3; ++i) { a.box_min[i] = sc->box_min[i]; a.box_ext[i] = sc->box_ext[i]; }
-    a.eps_t = sc->eps_t; a.n_slots = (uint32_t)S; a.n_seg = fi.n_seg;
-    for (int s = 0; s < fi.n_seg; ++s) a.seg_type[s] = fi.seg_type[s];
-    for (int s = 0; s <= fi.n_seg; ++s) a.seg_slot_start[s] = fi.seg_slot_start[s];
+    RaygenArgs a = raygen_def(sc, fi, h, lights, n_lights);
     a.rays = sc->rays.as<float4>(); a.keys_c = sc->keys_c.as<uint32_t>(); a.vals_c = sc->vals_c.as<uint32_t>();
     a.out_hit = out_packed ? nullptr : out_hit; a.out_t = out_packed ? nullptr : out_t; a.out_packed = out_packed;
     a.peer = peer;
@@ -542,7 +554,7 @@ crsh_status enqueue_frame(crsh_scene* sc, const FrameInfo& fi, const crsh_primar
 
 crsh_status trace_impl(crsh_scene* sc, const crsh_primary_hits* h, const float* lights, int32_t n_lights,
                        uint32_t types, const crsh_opts* o, int32_t* out_hit, float* out_t,
-                       unsigned long long* out_packed, const PeerOut& peer, cudaStream_t st) {
+                       unsigned long long* out_packed, const PeerOut& peer, cudaStream_t st, bool graph_ok = true) {
   if (!sc || !h || !o) return fail(CRSH_EINVAL, "null scene / hits / opts");
   if (h->width <= 0 || h->height <= 0) return fail(CRSH_EINVAL, "width/height must be positive");
   const uint64_t P64 = (uint64_t)h->width * (uint64_t)h->height;
@@ -655,7 +667,7 @@ crsh_status trace_impl(crsh_scene* sc, const crsh_primary_hits* h, const float* 
   std::vector<unsigned char> kb(sizeof(CallKey));
   std::memcpy(kb.data(), &key, sizeof(CallKey));
   static const bool use_graph = !std::getenv("CRSH_NO_GRAPH");
-  if (!use_graph) {
+  if (!use_graph || !graph_ok) {
     int64_t nl = 0;
     crsh_status rc = enqueue_frame(sc, fi, h, lights, n_lights, out_hit, out_t, out_packed, peer, st, &nl);
     if (rc != CRSH_OK) return rc;
@@ -803,6 +815,8 @@ void crsh_scene_destroy(crsh_scene_t sc) {
                  &sc->sorted_key, &sc->sorted_slot, &sc->sorted_rays, &sc->nodes, &sc->trav, &sc->masks, &sc->gwork, &sc->gstat, &sc->items,
                  &sc->best, &sc->zero, &sc->stage_in, &sc->stage_out};
   for (Buf* b : bufs) b->release();
+  for (auto& w : sc->wb) for (auto& b : w) b.release();
+  sc->w_hit.release(); sc->w_t.release(); sc->w_zero.release();
   if (sc->h_counters) cudaFreeHost(sc->h_counters);
   if (sc->h_fd) cudaFreeHost(sc->h_fd);
   if (sc->gexec) cudaGraphExecDestroy(sc->gexec);
@@ -837,6 +851,109 @@ crsh_status crsh_trace_secondary_peer(crsh_scene_t sc, const crsh_primary_hits* 
   }
   peer.n = n_dst;
   return trace_impl(sc, h, lights, n_lights, types, o, nullptr, nullptr, nullptr, peer, (cudaStream_t)stream);
+}
+
+crsh_status crsh_render_whitted(crsh_scene_t sc, const crsh_primary_hits* gbuf, const float* lights, int32_t n_lights,
+                                const int32_t* tri_mat, int32_t depth, const crsh_opts* o, float* image,
+                                crsh_whitted_stats_t* wst, void* stream) {
+  if (!sc || !gbuf || !o || !image || !tri_mat) return fail(CRSH_EINVAL, "null argument");
+  if (depth < 0 || depth > CRSH_MAX_BOUNCES) return fail(CRSH_EINVAL, "depth must be in [0, 8]");
+  if (o->shard_world > 1) return fail(CRSH_EINVAL, "crsh_render_whitted runs on one rank");
+  if (o->flags & CRSH_F_BRUTE) return fail(CRSH_EINVAL, "crsh_render_whitted traces with the hierarchy");
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaSetDevice(sc->device));
+  if (wst) { std::memset(wst, 0, sizeof(*wst)); wst->bounces = depth; }
+  if ((int)sc->wb.size() < depth + 1) sc->wb.resize(depth + 1);
+  crsh_primary_hits cur = *gbuf;
+  std::vector<int64_t> Pd;
+  int last = -1;
+  int64_t launches = 0;
+  for (int d = 0; d <= depth; ++d) {
+    const int64_t P = (int64_t)cur.width * cur.height;
+    Pd.push_back(P);
+    last = d;
+    auto& B = sc->wb[d];
+    for (int i = 4; i < 8; ++i) CK(ensure(B[i], 4 * (size_t)std::max<int64_t>(P, 1)));
+    if (wst) wst->vertices[d] = P;
+    if (P == 0) break;
+    const uint32_t types = (n_lights > 0 ? (uint32_t)CRSH_SHADOW : 0u) |
+                           (d < depth ? (uint32_t)(CRSH_REFLECT | CRSH_REFRACT) : 0u);
+    if (types == 0) {   // no lights at the last bounce: no direct term, no children
+      CK(cudaMemsetAsync(B[4].p, 0, 4 * (size_t)P, st));
+      break;
+    }
+    const int64_t S = crsh_num_slots((int32_t)P, n_lights, types);
+    CK(ensure(sc->w_hit, 4 * (size_t)S));
+    CK(ensure(sc->w_t, 4 * (size_t)S));
+    int32_t* hit = sc->w_hit.as<int32_t>();
+    float* tt = sc->w_t.as<float>();
+    crsh_status rc = trace_impl(sc, &cur, lights, n_lights, types, o, hit, tt, nullptr, PeerOut{}, st, false);
+    if (rc != CRSH_OK) return rc;
+    launches += sc->launches;
+    const FrameInfo fi = sc->fi;
+    if (wst) {
+      crsh_stats_t bs;
+      rc = crsh_stats(sc, &bs);
+      if (rc != CRSH_OK) return rc;
+      for (int q = 0; q < 3; ++q) {
+        wst->rays[d] += (int64_t)bs.rays[q];
+        for (int k = 1; k <= MAX_LEVELS; ++k) wst->tests[d] += bs.tests[q][k];
+        wst->final_tests[d] += bs.final_tests[q];
+      }
+    }
+    // KW1: direct term + child placement
+    const uint32_t tiles = cdiv((uint64_t)P, SCAN_TILE);
+    CK(ensure(sc->w_zero, 8 * ((size_t)tiles + 2)));
+    CK(cudaMemsetAsync(sc->w_zero.p, 0, 8 * ((size_t)tiles + 2), st));
+    ShadeArgs a{};
+    a.rg = raygen_def(sc, fi, &cur, lights, n_lights);
+    a.hit_tri = hit;
+    a.sh_slots = (types & CRSH_SHADOW) ? n_lights * (int32_t)P : 0;
+    a.re0 = (types & CRSH_REFLECT) ? a.sh_slots : -1;
+    a.rr0 = (types & CRSH_REFRACT) ? a.sh_slots + (int32_t)P : -1;
+    a.spawn = d < depth ? 1 : 0;
+    a.direct = B[4].as<float>(); a.c_re = B[5].as<int32_t>(); a.c_rr = B[6].as<int32_t>();
+    a.count = sc->w_zero.as<uint32_t>();
+    a.ticket = sc->w_zero.as<uint32_t>() + 1;
+    a.status = sc->w_zero.as<unsigned long long>() + 1;
+    k_shade<<<tiles, SCAN_THREADS, 0, st>>>(a);
+    CK(cudaGetLastError());
+    ++launches;
+    if (d == depth) break;
+    uint32_t k = 0;
+    CK(cudaMemcpyAsync(&k, a.count, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (k == 0) break;   // no reflection / refraction hit: the last bounce
+    // KW2: the children become the next bounce's vertex set
+    auto& N = sc->wb[d + 1];
+    for (int i = 0; i < 3; ++i) CK(ensure(N[i], 12 * (size_t)k));
+    CK(ensure(N[3], 4 * (size_t)k));
+    SpawnArgs sp{};
+    sp.rg = a.rg; sp.hit_tri = hit; sp.t = tt; sp.re0 = a.re0; sp.rr0 = a.rr0;
+    sp.c_re = a.c_re; sp.c_rr = a.c_rr; sp.tri_e = sc->tri_e.as<float4>(); sp.tri_mat = tri_mat; sp.k = k;
+    sp.npos = N[0].as<float>(); sp.nnrm = N[1].as<float>(); sp.ndir = N[2].as<float>(); sp.nmat = N[3].as<int32_t>();
+    k_spawn<<<cdiv((uint64_t)P, 256), 256, 0, st>>>(sp);
+    CK(cudaGetLastError());
+    ++launches;
+    cur.width = (int32_t)k; cur.height = 1;
+    cur.pos = sp.npos; cur.nrm = sp.nnrm; cur.mat = sp.nmat; cur.dir = sp.ndir;
+  }
+  // KW3: radiance from the deepest bounce up; bounce 0 writes the image
+  for (int d = last; d >= 0; --d) {
+    const int64_t P = Pd[d];
+    if (P == 0) continue;
+    auto& B = sc->wb[d];
+    const bool has_next = d < last && Pd[d + 1] > 0;
+    const int32_t* mat = d == 0 ? gbuf->mat : sc->wb[d][3].as<int32_t>();
+    k_backprop<<<cdiv((uint64_t)P, 256), 256, 0, st>>>(
+        (int32_t)P, mat, gbuf->materials, gbuf->n_mat, B[4].as<float>(), has_next ? B[5].as<int32_t>() : nullptr,
+        has_next ? B[6].as<int32_t>() : nullptr, has_next ? sc->wb[d + 1][7].as<float>() : nullptr,
+        d == 0 ? image : B[7].as<float>());
+    CK(cudaGetLastError());
+    ++launches;
+  }
+  sc->launches = launches;
+  return CRSH_OK;
 }
 
 crsh_status crsh_unpack_hits(crsh_scene_t sc, const uint64_t* packed, int64_t slots, int32_t* hit_tri, float* t,
