@@ -448,6 +448,57 @@ def run_sweep(args):
             del tr
 
 
+def run_whitted(args):
+    """Multi-bounce Whitted loop (crsh_render_whitted) on
+    the chosen config: rays of all bounces per second, with the oracle's loop
+    timed beside it on a band of rows (not the contract line)."""
+    import torch
+
+    import oracle
+    from paper_2312_06538_b200.api import tracer_for
+    from workloads import make_workload
+    w = make_workload(args.config)
+    flags = 7 if args.zorder else 3
+    tr = tracer_for(w, flags=flags)
+    stream = torch.cuda.current_stream()
+    for _ in range(max(3, args.warmup)):
+        img, st = tr.render(w.tri_mat, args.whitted)
+    torch.cuda.synchronize()
+    ms = []
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+    for _ in range(max(1, args.steps)):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        img, st = tr.render(w.tri_mat, args.whitted)
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms.append(a.elapsed_time(b))
+    rays = int(sum(st["rays"]))
+    t = float(np.median(ms))
+    line = {"mode": "whitted", "metric": "secondary Mrays/s, all bounces of the Whitted loop", "unit": "Mrays/s",
+            "value": round(rays / (t * 1e-3) / 1e6, 3), "ms_per_frame": round(t, 3), "depth": args.whitted,
+            "hash": "zorder" if args.zorder else "R6", "workload": w.name, "vertices": st["vertices"],
+            "rays": st["rays"], "tests": [int(x) for x in st["tests"]], "final_tests": [int(x) for x in st["final_tests"]],
+            "image_mean": float(img[:w.P].mean())}
+    if not args.no_cpu_baseline:
+        import dataclasses
+        rows = max(1, w.height // 32)
+        r0 = (w.height - rows) // 2
+        P = w.width
+        band = dataclasses.replace(w, height=rows,
+                                   pos=np.ascontiguousarray(w.pos.reshape(3, w.height, P)[:, r0:r0 + rows].reshape(3, -1)),
+                                   nrm=np.ascontiguousarray(w.nrm.reshape(3, w.height, P)[:, r0:r0 + rows].reshape(3, -1)),
+                                   mat=np.ascontiguousarray(w.mat.reshape(w.height, P)[r0:r0 + rows].reshape(-1)))
+        t0 = time.perf_counter()
+        ref = oracle.whitted(band, args.whitted, flags=flags)
+        dt = time.perf_counter() - t0
+        line["cpu_baseline"] = {"value": round(sum(ref["rays"]) / dt / 1e6, 5), "unit": "Mrays/s",
+                                "cores": oracle.default_threads(), "kind": "oracle",
+                                "sample": f"{rows} of {w.height} image rows (centre band), {sum(ref['rays'])} rays, {dt:.1f} s"}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -460,7 +511,11 @@ def main():
     ap.add_argument("--nccl-merge", action="store_true", help="N > 1: NCCL MIN all-reduce merge instead of the fused peer stores")
     ap.add_argument("--table4", action="store_true", help="CRSH vs RAH vs N x M report (not the contract line)")
     ap.add_argument("--sweep", action="store_true", help="cfg5 depth/bundle sweep (not the contract line)")
+    ap.add_argument("--whitted", type=int, default=None, metavar="D",
+                    help="multi-bounce Whitted loop of depth D (NEXT-2; not the contract line)")
     args = ap.parse_args()
+    if args.whitted is not None:
+        return run_whitted(args)
     if args.table4:
         return run_table4(args)
     if args.sweep:
