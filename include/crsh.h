@@ -187,6 +187,39 @@ crsh_status crsh_trace_secondary_packed(crsh_scene_t scene, const crsh_primary_h
 crsh_status crsh_trace_secondary_peer(crsh_scene_t scene, const crsh_primary_hits* hits, const float* lights,
                                       int32_t n_lights, uint32_t ray_types, const crsh_opts* opts,
                                       uint64_t* const* dst, int32_t n_dst, void* stream);
+/* Trace an arbitrary batch of rays through the same pipeline (hash of the
+ * bounce-ray layout, compress, sort, decompress, hierarchy, cull, traverse,
+ * closest hit): the re-entry point the paper describes for the next set of
+ * rays ("output these rays onto the ray array ... and continue from the
+ * ray-sorting step") and the engine of the GPU primary pass.
+ *   rays     device [n][8] float32: o.xyz, tmin, d.xyz (unit), tmax; a ray
+ *            with !(tmax > tmin) is an empty slot (hit -2)
+ *   hit_tri, t  device [n] outputs as crsh_trace_secondary
+ * Counters go to segment 1 (the bounce-ray segment) of crsh_stats. */
+crsh_status crsh_trace_rays(crsh_scene_t scene, const float* rays, int64_t n, const crsh_opts* opts, int32_t* hit_tri,
+                            float* t, void* stream);
+
+/* Pinhole camera of the GPU primary pass: orthonormal basis (right, up, fwd),
+ * tan_half_vfov = tan(vertical field of view / 2). Pixel (i, j), j = 0 at the
+ * top, p = j*width + i, ray through the pixel centre:
+ *   u = ((2i+1)/W - 1) * tan_half_vfov * (W/H),  v = (1 - (2j+1)/H) * tan_half_vfov,
+ *   d = norm(fma(u, right, fma(v, up, fwd))),  o = eye, tmin = 0, tmax = +inf. */
+typedef struct {
+  float eye[3], right[3], up[3], fwd[3];
+  float tan_half_vfov;
+} crsh_camera;
+
+/* GPU primary pass (the G-buffer the paper rasterises,
+ * P:67-71, produced in the library instead): camera rays traced with
+ * crsh_trace_rays; per pixel pos = fma(t, d, o), nrm = norm(e1 x e2) of the
+ * hit triangle turned toward the camera, mat = tri_mat[hit]; a miss gives
+ * pos = nrm = 0, mat = -1. The outputs are a crsh_primary_hits-compatible
+ * G-buffer (device SoA [3][P] pos / nrm, [P] mat) plus the primary hit_tri / t
+ * (device [P]). tri_mat: device [M] int32. One rank. */
+crsh_status crsh_primary_gbuffer(crsh_scene_t scene, const crsh_camera* cam, int32_t width, int32_t height,
+                                 const int32_t* tri_mat, const crsh_opts* opts, float* pos, float* nrm, int32_t* mat,
+                                 int32_t* hit_tri, float* t, void* stream);
+
 /* Multi-bounce Whitted rendering on top of the secondary pass (SURVEY §8(f)
  * NEXT-2; "accumulate shading ... output another set of secondary
  * rays onto the ray array that we used initially and continue"; [Whi80]).

@@ -69,6 +69,12 @@ def lib():
         L.or_spawn.argtypes = [C.c_int32, C.c_int32, C.c_uint32, vp, vp, vp, vp, vp, C.c_int64, vp, vp, vp, vp, vp, vp]
         L.or_backprop.restype = None
         L.or_backprop.argtypes = [C.c_int32, vp, vp, C.c_int32, vp, vp, vp, vp, vp]
+        L.or_camera_rays.restype = None
+        L.or_camera_rays.argtypes = [vp, C.c_int32, C.c_int32, vp]
+        L.or_keys_given.restype = None
+        L.or_keys_given.argtypes = [C.c_int64, vp, vp, vp, C.c_uint32, vp, vp]
+        L.or_gbuffer.restype = None
+        L.or_gbuffer.argtypes = [C.c_int64, vp, vp, vp, vp, vp, vp, vp, vp]
         L.or_trim.restype = C.c_int64
         L.or_trim.argtypes = [C.c_int64, vp, vp, vp, vp, vp]
         L.or_compress.restype = C.c_int64
@@ -298,9 +304,47 @@ def trace(w, prep: ScenePrep | None = None, flags: int = F_SORT | F_MESH_CULL, n
     """Returns dict(hit_tri[slots], t[slots], stats, [taps]).  hit_tri = -2 for
     an empty slot, -1 for a miss (SURVEY §8(c) output convention)."""
     prep = prep or ScenePrep(w.tris, w.mesh_ids)
-    Lv, B0, B = w.levels, w.leaf_size, w.branching
-    P, L = w.P, w.lights.shape[0]
     rays, keys, empty = generate(w, prep, flags)
+    return _trace_core(rays, keys, empty, segments(w.P, w.lights.shape[0], w.ray_types), prep, w.levels, w.leaf_size,
+                       w.branching, flags, n_threads, taps)
+
+
+def trace_rays(rays, prep: ScenePrep, levels=2, leaf_size=8, branching=8, flags: int = F_SORT | F_MESH_CULL,
+               n_threads=None, taps=False):
+    """A given ray batch ([n, 8]: o, tmin, d, tmax) through the same stages
+    (crsh_trace_rays): bounce-ray hash keys, one segment reported as 1."""
+    rays = _f32(rays).reshape(-1, 8)
+    n = rays.shape[0]
+    keys = np.zeros(n, np.uint32)
+    empty = np.zeros(n, np.uint32)
+    lib().or_keys_given(n, _p(rays), _p(prep.box_min), _p(prep.box_ext), flags, _p(keys), _p(empty))
+    return _trace_core(rays, keys, empty, [(1, 0, n)], prep, levels, leaf_size, branching, flags, n_threads, taps)
+
+
+def camera_rays(cam13, W: int, H: int):
+    rays = np.zeros((W * H, 8), np.float32)
+    lib().or_camera_rays(_p(_f32(cam13)), W, H, _p(rays))
+    return rays
+
+
+def primary_gbuffer(tris, mesh_ids, tri_mat, cam13, W: int, H: int, levels=2, leaf_size=8, branching=8,
+                    flags: int = F_SORT | F_MESH_CULL, prep: ScenePrep | None = None):
+    """GPU primary pass mirror (NEXT-3): camera rays traced with the pipeline,
+    then the G-buffer of the closest hits. Returns (pos[3,P], nrm[3,P],
+    mat[P], hit_tri[P], t[P], stats)."""
+    prep = prep or ScenePrep(tris, mesh_ids)
+    rays = camera_rays(cam13, W, H)
+    out = trace_rays(rays, prep, levels, leaf_size, branching, flags)
+    P = W * H
+    pos, nrm = np.zeros((3, P), np.float32), np.zeros((3, P), np.float32)
+    mat = np.zeros(P, np.int32)
+    lib().or_gbuffer(P, _p(rays), _p(np.ascontiguousarray(out["hit_tri"], np.int32)),
+                     _p(np.ascontiguousarray(out["t"], np.float32)), _p(prep.tri_e),
+                     _p(np.ascontiguousarray(tri_mat, np.int32)), _p(pos), _p(nrm), _p(mat))
+    return pos, nrm, mat, out["hit_tri"], out["t"], out["stats"]
+
+
+def _trace_core(rays, keys, empty, segs, prep: ScenePrep, Lv, B0, B, flags, n_threads, taps):
     S = rays.shape[0]
     hit_tri = np.full(S, -2, np.int32)
     t_out = np.full(S, np.inf, np.float32)
@@ -311,7 +355,7 @@ def trace(w, prep: ScenePrep | None = None, flags: int = F_SORT | F_MESH_CULL, n
     # trimming over the whole slot array keeps slot order, so each
     # segment's survivors stay contiguous.
     keys_c, vals_c = trim(empty, keys, np.arange(S, dtype=np.uint32))
-    for seg, s0, ns in segments(P, L, w.ray_types):
+    for seg, s0, ns in segs:
         sel = (vals_c >= s0) & (vals_c < s0 + ns)
         k, v = keys_c[sel], vals_c[sel]
         stats["slots"][seg] = ns

@@ -850,3 +850,59 @@ EXPORT void or_backprop(int32_t P, const int32_t* mat, const float* materials, i
     L[v] = r;
   }
 }
+
+/* ---------------------------------------------------------------------------
+ * GPU primary pass mirror. cam = eye[3],
+ * right[3], up[3], fwd[3], tan_half_vfov (13 floats); pixel (i, j), j = 0 at
+ * the top, ray through the pixel centre.
+ * ------------------------------------------------------------------------- */
+EXPORT void or_camera_rays(const float* cam, int32_t W, int32_t H, float* rays) {
+  const float ax = cam[12] * ((float)W / (float)H);
+  for (int32_t j = 0; j < H; ++j)
+    for (int32_t i = 0; i < W; ++i) {
+      const float u = ((float)(2 * i + 1) / (float)W - 1.0f) * ax;
+      const float v = (1.0f - (float)(2 * j + 1) / (float)H) * cam[12];
+      V3 dd = v3(fmaf(u, cam[3], fmaf(v, cam[6], cam[9])), fmaf(u, cam[4], fmaf(v, cam[7], cam[10])),
+                 fmaf(u, cam[5], fmaf(v, cam[8], cam[11])));
+      V3 d = norm3(dd);
+      float* r = rays + 8 * ((int64_t)j * W + i);
+      r[0] = cam[0]; r[1] = cam[1]; r[2] = cam[2]; r[3] = 0.0f;
+      r[4] = d.x; r[5] = d.y; r[6] = d.z; r[7] = INFINITY;
+    }
+}
+
+/* keys / empty flags of a given ray batch: the bounce-ray hash of (o, d);
+ * a ray with !(tmax > tmin) is an empty slot. */
+EXPORT void or_keys_given(int64_t n, const float* rays, const float* box_min, const float* box_ext, uint32_t flags,
+                          uint32_t* keys, uint32_t* empty) {
+  const bool zorder = (flags & 4u) != 0;
+  for (int64_t s = 0; s < n; ++s) {
+    const float* r = rays + 8 * s;
+    if (!(r[7] > r[3])) { empty[s] = 1; keys[s] = 0; continue; }
+    keys[s] = hash_bounce(v3(r[0], r[1], r[2]), v3(r[4], r[5], r[6]), box_min, box_ext, zorder);
+    empty[s] = 0;
+  }
+}
+
+/* G-buffer from the primary hits: pos = fma(t, d, o), n = norm(e1 x e2)
+ * turned toward the camera, material of the triangle; miss -> 0, 0, -1. */
+EXPORT void or_gbuffer(int64_t P, const float* rays, const int32_t* hit_tri, const float* t, const float* tri_e,
+                       const int32_t* tri_mat, float* pos, float* nrm, int32_t* mat) {
+  for (int64_t p = 0; p < P; ++p) {
+    const int32_t h = hit_tri[p];
+    if (h < 0) {
+      pos[p] = pos[P + p] = pos[2 * P + p] = 0.0f;
+      nrm[p] = nrm[P + p] = nrm[2 * P + p] = 0.0f;
+      mat[p] = -1;
+      continue;
+    }
+    const float* r = rays + 8 * p;
+    const float* te = tri_e + 9 * (int64_t)h;
+    V3 n = norm3(cross3(v3(te[3], te[4], te[5]), v3(te[6], te[7], te[8])));
+    V3 d = v3(r[4], r[5], r[6]);
+    if (dot3(d, n) > 0.0f) n = neg(n);
+    pos[p] = fmaf(t[p], r[4], r[0]); pos[P + p] = fmaf(t[p], r[5], r[1]); pos[2 * P + p] = fmaf(t[p], r[6], r[2]);
+    nrm[p] = n.x; nrm[P + p] = n.y; nrm[2 * P + p] = n.z;
+    mat[p] = tri_mat[h];
+  }
+}

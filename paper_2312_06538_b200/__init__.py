@@ -45,6 +45,20 @@ class WhittedStats(C.Structure):
                 ("tests", C.c_uint64 * 9), ("final_tests", C.c_uint64 * 9)]
 
 
+class Camera(C.Structure):
+    _fields_ = [("eye", C.c_float * 3), ("right", C.c_float * 3), ("up", C.c_float * 3), ("fwd", C.c_float * 3),
+                ("tan_half_vfov", C.c_float)]
+
+
+def make_camera(cam13) -> Camera:
+    """crsh_camera from 13 floats: eye, right, up, fwd, tan(vfov/2)."""
+    c = Camera()
+    v = [float(x) for x in cam13]
+    c.eye = (C.c_float * 3)(*v[0:3]); c.right = (C.c_float * 3)(*v[3:6])
+    c.up = (C.c_float * 3)(*v[6:9]); c.fwd = (C.c_float * 3)(*v[9:12]); c.tan_half_vfov = v[12]
+    return c
+
+
 class Opts(C.Structure):
     _fields_ = [("levels", C.c_int32), ("leaf_size", C.c_int32), ("branching", C.c_int32), ("flags", C.c_uint32),
                 ("shard_rank", C.c_int32), ("shard_world", C.c_int32)]
@@ -88,6 +102,11 @@ def load():
     L.crsh_trace_secondary_peer.restype = st
     L.crsh_trace_secondary_peer.argtypes = [vp, C.POINTER(PrimaryHits), vp, C.c_int32, C.c_uint32, C.POINTER(Opts),
                                             C.POINTER(C.c_uint64), C.c_int32, vp]
+    L.crsh_trace_rays.restype = st
+    L.crsh_trace_rays.argtypes = [vp, vp, C.c_int64, C.POINTER(Opts), vp, vp, vp]
+    L.crsh_primary_gbuffer.restype = st
+    L.crsh_primary_gbuffer.argtypes = [vp, C.POINTER(Camera), C.c_int32, C.c_int32, vp, C.POINTER(Opts), vp, vp, vp,
+                                       vp, vp, vp]
     L.crsh_render_whitted.restype = st
     L.crsh_render_whitted.argtypes = [vp, C.POINTER(PrimaryHits), vp, C.c_int32, vp, C.c_int32, C.POINTER(Opts), vp,
                                       C.POINTER(WhittedStats), vp]
@@ -192,6 +211,19 @@ def trace_secondary_peer(scene: Scene, hits: PrimaryHits, lights, ray_types: int
     d = (C.c_uint64 * len(dst_ptrs))(*[int(x) for x in dst_ptrs])
     _check(load().crsh_trace_secondary_peer(scene.handle, C.byref(hits), arr.ctypes.data, n, ray_types,
                                             C.byref(opts), d, len(dst_ptrs), stream))
+
+
+def trace_rays(scene: Scene, rays, n: int, opts: Opts, hit_tri, t, stream=0):
+    """crsh_trace_rays: device rays [n][8] (o, tmin, d, tmax) -> hit_tri, t."""
+    _check(load().crsh_trace_rays(scene.handle, _ptr(rays), n, C.byref(opts), _ptr(hit_tri), _ptr(t), stream))
+
+
+def primary_gbuffer(scene: Scene, cam13, width: int, height: int, tri_mat, opts: Opts, pos, nrm, mat, hit_tri, t,
+                    stream=0):
+    """crsh_primary_gbuffer: the GPU primary pass into device G-buffer tensors."""
+    c = make_camera(cam13)
+    _check(load().crsh_primary_gbuffer(scene.handle, C.byref(c), width, height, _ptr(tri_mat), C.byref(opts),
+                                       _ptr(pos), _ptr(nrm), _ptr(mat), _ptr(hit_tri), _ptr(t), stream))
 
 
 def render_whitted(scene: Scene, hits: PrimaryHits, lights, tri_mat, depth: int, opts: Opts, image, stream=0) -> dict:

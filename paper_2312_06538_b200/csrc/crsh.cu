@@ -20,6 +20,7 @@
 #include "k_sort.cuh"
 #include "k_traverse.cuh"
 #include "k_whitted.cuh"
+#include "k_primary.cuh"
 
 using namespace crsh;
 
@@ -191,6 +192,7 @@ struct FrameInfo {
   uint32_t flags = 0;
   int rank = 0, world = 1;
   bool sorted = false, timed = false, ktimed = false, brute = false;
+  const float4* in_rays = nullptr;          // ray-batch mode (crsh_trace_rays)
   FrameDesc fd{};                           // host copy of the device counts (refreshed lazily)
   bool fd_fresh = false;
 };
@@ -221,6 +223,7 @@ struct crsh_scene {
   // multi-bounce Whitted loop (crsh_render_whitted): per-bounce vertex sets and terms
   std::vector<std::array<Buf, 8>> wb;   // pos, nrm, dir, mat, direct, c_re, c_rr, L
   Buf w_hit, w_t, w_zero;
+  Buf prim_rays;                        // crsh_primary_gbuffer camera rays
 };
 
 namespace {
@@ -306,6 +309,7 @@ RaygenArgs raygen_def(const crsh_scene* sc, const FrameInfo& fi, const crsh_prim
   a.n_mat = h->n_mat;
   for (int i = 0; i < 3; ++i) a.eye[i] = h->eye[i];
   a.dir = h->dir;
+  a.in_rays = fi.in_rays;
   for (int i = 0; i < 3 * n_lights; ++i) a.lights[i] = lights[i];
   a.n_lights = n_lights; a.zorder = (fi.flags & CRSH_F_ZORDER) ? 1 : 0;
   for (int i = 0; i < 3; ++i) { a.box_min[i] = sc->box_min[i]; a.box_ext[i] = sc->box_ext[i]; }
@@ -554,7 +558,8 @@ crsh_status enqueue_frame(crsh_scene* sc, const FrameInfo& fi, const crsh_primar
 
 crsh_status trace_impl(crsh_scene* sc, const crsh_primary_hits* h, const float* lights, int32_t n_lights,
                        uint32_t types, const crsh_opts* o, int32_t* out_hit, float* out_t,
-                       unsigned long long* out_packed, const PeerOut& peer, cudaStream_t st, bool graph_ok = true) {
+                       unsigned long long* out_packed, const PeerOut& peer, cudaStream_t st, bool graph_ok = true,
+                       const float4* in_rays = nullptr) {
   if (!sc || !h || !o) return fail(CRSH_EINVAL, "null scene / hits / opts");
   if (h->width <= 0 || h->height <= 0) return fail(CRSH_EINVAL, "width/height must be positive");
   const uint64_t P64 = (uint64_t)h->width * (uint64_t)h->height;
@@ -589,6 +594,7 @@ crsh_status trace_impl(crsh_scene* sc, const crsh_primary_hits* h, const float* 
   fi.ktimed = (o->flags & CRSH_F_KERNEL_TIMING) != 0;
   fi.brute = (o->flags & CRSH_F_BRUTE) != 0;
   fi.rank = rank; fi.world = world;
+  fi.in_rays = in_rays;
   uint64_t S = 0;
   const int type_bits[3] = {1, 2, 4};
   for (int t = 0; t < 3; ++t) {
@@ -816,7 +822,7 @@ void crsh_scene_destroy(crsh_scene_t sc) {
                  &sc->best, &sc->zero, &sc->stage_in, &sc->stage_out};
   for (Buf* b : bufs) b->release();
   for (auto& w : sc->wb) for (auto& b : w) b.release();
-  sc->w_hit.release(); sc->w_t.release(); sc->w_zero.release();
+  sc->w_hit.release(); sc->w_t.release(); sc->w_zero.release(); sc->prim_rays.release();
   if (sc->h_counters) cudaFreeHost(sc->h_counters);
   if (sc->h_fd) cudaFreeHost(sc->h_fd);
   if (sc->gexec) cudaGraphExecDestroy(sc->gexec);
@@ -851,6 +857,49 @@ crsh_status crsh_trace_secondary_peer(crsh_scene_t sc, const crsh_primary_hits* 
   }
   peer.n = n_dst;
   return trace_impl(sc, h, lights, n_lights, types, o, nullptr, nullptr, nullptr, peer, (cudaStream_t)stream);
+}
+
+crsh_status crsh_trace_rays(crsh_scene_t sc, const float* rays, int64_t n, const crsh_opts* o, int32_t* hit_tri,
+                            float* t, void* stream) {
+  if (!sc || !o || !hit_tri || !t || (n > 0 && !rays)) return fail(CRSH_EINVAL, "null argument");
+  if (n < 0 || n >= (1ll << 30)) return fail(CRSH_ELIMIT, "n must be in [0, 2^30)");
+  if (n == 0) return CRSH_OK;
+  // a one-segment frame (the bounce-type segment, slot i = ray i) whose K1
+  // reads the given rays instead of generating them from a G-buffer
+  crsh_primary_hits h{};
+  h.width = (int32_t)n; h.height = 1;
+  h.pos = rays; h.nrm = rays; h.mat = reinterpret_cast<const int32_t*>(rays);
+  h.n_mat = 0;
+  return trace_impl(sc, &h, nullptr, 0, CRSH_REFLECT, o, hit_tri, t, nullptr, PeerOut{}, (cudaStream_t)stream, true,
+                    reinterpret_cast<const float4*>(rays));
+}
+
+crsh_status crsh_primary_gbuffer(crsh_scene_t sc, const crsh_camera* cam, int32_t width, int32_t height,
+                                 const int32_t* tri_mat, const crsh_opts* o, float* pos, float* nrm, int32_t* mat,
+                                 int32_t* hit_tri, float* t, void* stream) {
+  if (!sc || !cam || !tri_mat || !o || !pos || !nrm || !mat || !hit_tri || !t) return fail(CRSH_EINVAL, "null argument");
+  if (width <= 0 || height <= 0 || (int64_t)width * height >= (1ll << 30)) return fail(CRSH_ELIMIT, "bad image size");
+  if (o->shard_world > 1) return fail(CRSH_EINVAL, "the primary pass runs on one rank");
+  const int64_t P = (int64_t)width * height;
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaSetDevice(sc->device));
+  CK(ensure(sc->prim_rays, 32 * (size_t)P));
+  CameraArgs c{};
+  for (int k = 0; k < 3; ++k) {
+    c.eye[k] = cam->eye[k]; c.right[k] = cam->right[k]; c.up[k] = cam->up[k]; c.fwd[k] = cam->fwd[k];
+  }
+  c.tan_half = cam->tan_half_vfov; c.W = width; c.H = height; c.rays = sc->prim_rays.as<float4>();
+  k_camera_rays<<<cdiv((uint64_t)P, 256), 256, 0, st>>>(c);
+  CK(cudaGetLastError());
+  crsh_status rc = crsh_trace_rays(sc, sc->prim_rays.as<float>(), P, o, hit_tri, t, stream);
+  if (rc != CRSH_OK) return rc;
+  GbufArgs g{};
+  g.P = P; g.rays = c.rays; g.hit_tri = hit_tri; g.t = t; g.tri_e = sc->tri_e.as<float4>(); g.tri_mat = tri_mat;
+  g.pos = pos; g.nrm = nrm; g.mat = mat;
+  k_gbuffer<<<cdiv((uint64_t)P, 256), 256, 0, st>>>(g);
+  CK(cudaGetLastError());
+  sc->launches += 2;
+  return CRSH_OK;
 }
 
 crsh_status crsh_render_whitted(crsh_scene_t sc, const crsh_primary_hits* gbuf, const float* lights, int32_t n_lights,

@@ -24,6 +24,7 @@ struct RaygenArgs {
   int32_t n_mat;
   float eye[3];
   const float* dir;                   // optional [3][P] incident directions (Whitted bounce > 0)
+  const float4* in_rays;              // ray-batch mode (crsh_trace_rays): slot i = {o, tmin}, {d, tmax}
   float lights[16 * 3];
   int32_t n_lights;
   int32_t zorder;
@@ -46,6 +47,13 @@ struct RaygenArgs {
 };
 
 __device__ __forceinline__ bool gen_ray(const RaygenArgs& a, uint32_t slot, float4& r0, float4& r1, uint32_t& key) {
+  if (a.in_rays) {   // given rays (primary pass, external batches): bounce-type hash, empty iff !(tmax > tmin)
+    r0 = __ldg(a.in_rays + 2 * (size_t)slot);
+    r1 = __ldg(a.in_rays + 2 * (size_t)slot + 1);
+    if (!(r1.w > r0.w)) return false;
+    key = hash_bounce_ns(mk3(r0.x, r0.y, r0.z), mk3(r1.x, r1.y, r1.z), a.box_min, a.box_ext, a.zorder != 0);
+    return true;
+  }
   int s = 0;
   while (s + 1 < a.n_seg && slot >= a.seg_slot_start[s + 1]) ++s;
   const uint32_t local = slot - a.seg_slot_start[s];

@@ -309,3 +309,59 @@ def test_incident_directions_parity():
     tr, hit, t, ref = run_both(w, crsh.F_SORT | crsh.F_MESH_CULL, taps=False)
     assert np.array_equal(hit, ref["hit_tri"]) and np.array_equal(t.view(np.uint32), ref["t"].view(np.uint32))
     assert_counts_equal(crsh.stats(tr.scene), ref)
+
+
+@pytest.mark.parametrize("cfg,W,H,flags", [(1, 128, 96, 3), (2, 256, 256, 3), (2, 200, 150, 7)])
+def test_primary_gbuffer_parity(cfg, W, H, flags):
+    """GPU primary pass (NEXT-3, crsh_primary_gbuffer): camera rays traced
+    through the pipeline; G-buffer, primary hits and counters bit-exact vs the
+    oracle."""
+    from workloads import make_camera
+    w = make_workload(cfg, width=16, height=16)
+    cam = make_camera()
+    scene = crsh.Scene(torch.as_tensor(w.tris).cuda(), torch.as_tensor(w.mesh_ids).cuda())
+    P = W * H
+    pos = torch.empty(3 * P, dtype=torch.float32, device="cuda")
+    nrm = torch.empty(3 * P, dtype=torch.float32, device="cuda")
+    mat = torch.empty(P, dtype=torch.int32, device="cuda")
+    hit = torch.empty(P, dtype=torch.int32, device="cuda")
+    t = torch.empty(P, dtype=torch.float32, device="cuda")
+    tm = torch.as_tensor(w.tri_mat).cuda()
+    opts = crsh.make_opts(w.levels, w.leaf_size, w.branching, flags)
+    crsh.primary_gbuffer(scene, cam, W, H, tm, opts, pos, nrm, mat, hit, t)
+    torch.cuda.synchronize()
+    rpos, rnrm, rmat, rhit, rt, rst = oracle.primary_gbuffer(w.tris, w.mesh_ids, w.tri_mat, cam, W, H, w.levels,
+                                                             w.leaf_size, w.branching, flags)
+    assert np.array_equal(hit.cpu().numpy(), rhit) and np.array_equal(t.cpu().numpy().view(np.uint32), rt.view(np.uint32))
+    assert np.array_equal(mat.cpu().numpy(), rmat)
+    assert np.array_equal(pos.cpu().numpy().reshape(3, P).view(np.uint32), rpos.view(np.uint32))
+    assert np.array_equal(nrm.cpu().numpy().reshape(3, P).view(np.uint32), rnrm.view(np.uint32))
+    st = crsh.stats(scene)
+    assert np.array_equal(st["tests"][1], rst["tests"][1]) and st["final_tests"][1] == rst["final_tests"][1]
+
+
+def test_trace_rays_parity():
+    """crsh_trace_rays on a batch of random rays (some empty, some reversed
+    intervals): hits and counters bit-exact vs the oracle and equal to brute force."""
+    w = make_workload(2, width=16, height=16)
+    r = np.random.default_rng(5)
+    n = 20000
+    o = r.uniform(0.5, 9.5, size=(n, 3)).astype(np.float32)
+    d = r.normal(size=(n, 3))
+    d = (d / np.linalg.norm(d, axis=1, keepdims=True)).astype(np.float32)
+    tmin = np.full(n, 1e-3, np.float32)
+    tmax = np.where(r.random(n) < 0.1, -1.0, np.where(r.random(n) < 0.5, 4.0, np.inf)).astype(np.float32)
+    rays = np.concatenate([o, tmin[:, None], d, tmax[:, None]], axis=1).astype(np.float32)
+    scene = crsh.Scene(torch.as_tensor(w.tris).cuda(), torch.as_tensor(w.mesh_ids).cuda())
+    hit = torch.empty(n, dtype=torch.int32, device="cuda")
+    t = torch.empty(n, dtype=torch.float32, device="cuda")
+    crsh.trace_rays(scene, torch.as_tensor(rays).cuda(), n, crsh.make_opts(2, 8, 8, 3), hit, t)
+    torch.cuda.synchronize()
+    prep = oracle.ScenePrep(w.tris, w.mesh_ids)
+    ref = oracle.trace_rays(rays, prep, 2, 8, 8, 3)
+    assert np.array_equal(hit.cpu().numpy(), ref["hit_tri"])
+    assert np.array_equal(t.cpu().numpy().view(np.uint32), ref["t"].view(np.uint32))
+    assert_counts_equal(crsh.stats(scene), ref)
+    ok = ref["hit_tri"] != -2
+    bt, _ = oracle.unpack(oracle.brute(rays[ok], prep))
+    assert np.array_equal(ref["hit_tri"][ok], bt)

@@ -101,6 +101,19 @@ def _lib():
     return _raster
 
 
+def make_camera(eye=EYE, fwd=FWD, up=UP, vfov=VFOV) -> np.ndarray:
+    """Pinhole camera of the GPU primary pass (include/crsh.h crsh_camera):
+    eye, right, up, fwd, tan(vfov/2) as 13 float32 -- the same orthonormal
+    basis raster.c builds (right = fwd x up, up' = right x fwd), in float64
+    then rounded. Input generation only (no method arithmetic)."""
+    f = np.asarray(fwd, np.float64)
+    f = f / np.linalg.norm(f)
+    r = np.cross(f, np.asarray(up, np.float64))
+    r = r / np.linalg.norm(r)
+    u = np.cross(r, f)
+    return np.concatenate([np.asarray(eye, np.float64), r, u, f, [np.tan(np.radians(vfov) / 2)]]).astype(np.float32)
+
+
 def rasterize(tris, tri_mat, width, height, eye=EYE, fwd=FWD, up=UP, vfov=VFOV):
     tris = np.ascontiguousarray(tris, dtype=np.float32)
     tri_mat = np.ascontiguousarray(tri_mat, dtype=np.int32)
