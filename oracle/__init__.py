@@ -59,7 +59,13 @@ def lib():
         L.or_miniball.restype = C.c_int
         L.or_miniball.argtypes = [vp, C.c_int64, vp]
         L.or_scene_prep.restype = C.c_int
-        L.or_scene_prep.argtypes = [vp, vp, C.c_int64, C.c_int32, vp, vp, vp, vp, vp]
+        L.or_scene_prep.argtypes = [vp, vp, C.c_int64, C.c_int32, vp, vp, vp, vp, vp, C.c_float, C.c_float, vp]
+        L.or_transform.restype = None
+        L.or_transform.argtypes = [vp, vp, C.c_int64, vp, vp]
+        L.or_sigma_max.restype = C.c_double
+        L.or_sigma_max.argtypes = [vp]
+        L.or_update_sphere.restype = None
+        L.or_update_sphere.argtypes = [vp, vp, vp]
         L.or_generate.restype = C.c_int64
         L.or_generate.argtypes = [C.c_int32, vp, vp, vp, vp, C.c_int32, vp, vp, vp, C.c_int32, C.c_uint32, vp, vp,
                                   C.c_float, C.c_uint32, vp, vp, vp]
@@ -169,7 +175,7 @@ def miniball(points):
 
 
 class ScenePrep:
-    def __init__(self, tris, mesh_ids):
+    def __init__(self, tris, mesh_ids, pad=None, eps_t=None, mesh_sph=None):
         tris = _f32(tris).reshape(-1, 9)
         mesh_ids = np.ascontiguousarray(mesh_ids, np.int32)
         M = tris.shape[0]
@@ -180,8 +186,11 @@ class ScenePrep:
         self.mesh_sph = np.zeros((max(n_meshes, 1), 4), np.float32)
         self.mesh_range = np.zeros((max(n_meshes, 1), 2), np.int64)
         self.consts = np.zeros(8, np.float32)
+        ms_in = _f32(mesh_sph).reshape(-1, 4) if mesh_sph is not None else None
         rc = lib().or_scene_prep(_p(tris), _p(mesh_ids), M, n_meshes, _p(self.tri_e), _p(self.tri_sph),
-                                 _p(self.mesh_sph), _p(self.mesh_range), _p(self.consts))
+                                 _p(self.mesh_sph), _p(self.mesh_range), _p(self.consts),
+                                 -1.0 if pad is None else float(pad), 0.0 if eps_t is None else float(eps_t),
+                                 _p(ms_in) if ms_in is not None else None)
         if rc != 0:
             raise ValueError("mesh ids must be non-decreasing and dense from 0")
         self.box_min = self.consts[0:3].copy()
@@ -461,3 +470,38 @@ def whitted(w, depth: int, prep: ScenePrep | None = None, flags: int = F_SORT | 
                               _p(Lnext), _p(Lcur))
         Lnext = Lcur
     return dict(image=Lnext[:w.P].copy(), vertices=verts, rays=nrays, stats=stats)
+
+
+# --------------------------------------------------------------------------
+# dynamic scenes (§3.3.1)
+
+def transform_tris(tris, mesh_ids, xforms):
+    """creation-time vertices -> per-mesh affine transform ([n_meshes, 12] =
+    [A | b] row-major), per axis fma(a0, x, fma(a1, y, fma(a2, z, b)))."""
+    tris = _f32(tris).reshape(-1, 9)
+    out = np.zeros_like(tris)
+    lib().or_transform(_p(tris), _p(np.ascontiguousarray(mesh_ids, np.int32)), tris.shape[0],
+                       _p(_f32(xforms).reshape(-1, 12)), _p(out))
+    return out
+
+
+def sigma_max(xf12) -> float:
+    return float(lib().or_sigma_max(_p(_f32(xf12))))
+
+
+def update_sphere(sph4, xf12):
+    out = np.zeros(4, np.float32)
+    lib().or_update_sphere(_p(_f32(sph4)), _p(_f32(xf12)), _p(out))
+    return out
+
+
+def transformed_prep(prep0: ScenePrep, tris0, mesh_ids, xforms):
+    """The scene after crsh_scene_transform: transformed vertices, triangle
+    data recomputed with the creation pad, mesh spheres UPDATED from the
+    creation spheres (not recomputed), AABB of the transformed vertices,
+    creation eps_t. Returns (prep, transformed tris)."""
+    xforms = _f32(xforms).reshape(-1, 12)
+    tris = transform_tris(tris0, mesh_ids, xforms)
+    ms = np.stack([update_sphere(prep0.mesh_sph[m], xforms[m]) for m in range(prep0.n_meshes)]) \
+        if prep0.n_meshes else np.zeros((1, 4), np.float32)
+    return ScenePrep(tris, mesh_ids, pad=prep0.pad, eps_t=prep0.eps_t, mesh_sph=ms), tris

@@ -440,7 +440,8 @@ EXPORT int or_miniball(const float* pts, int64_t n, float* out4) {
  * [min.xyz, max.xyz, pad, eps_t]. */
 EXPORT int or_scene_prep(const float* tris, const int32_t* mesh_ids, int64_t M, int32_t n_meshes,
                          float* tri_e /*M*9*/, float* tri_sph /*M*4*/, float* mesh_sph /*n*4*/,
-                         int64_t* mesh_range /*n*2*/, float* consts /*8*/) {
+                         int64_t* mesh_range /*n*2*/, float* consts /*8*/, float pad_in, float eps_in,
+                         const float* mesh_sph_in) {
   float mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
   for (int64_t t = 0; t < M; ++t)
     for (int v = 0; v < 3; ++v)
@@ -451,7 +452,8 @@ EXPORT int or_scene_prep(const float* tris, const int32_t* mesh_ids, int64_t M, 
   double diag = 0.0;
   for (int k = 0; k < 3; ++k) { double e = (double)mx[k] - (double)mn[k]; diag += e * e; }
   diag = std::sqrt(diag);
-  const float pad = (float)(1e-5 * diag), eps_t = (float)(1e-4 * diag);
+  // a transformed scene keeps the creation-time pad and eps_t (pad_in >= 0)
+  const float pad = pad_in >= 0.0f ? pad_in : (float)(1e-5 * diag), eps_t = pad_in >= 0.0f ? eps_in : (float)(1e-4 * diag);
   for (int k = 0; k < 3; ++k) { consts[k] = mn[k]; consts[3 + k] = mx[k]; }
   consts[6] = pad; consts[7] = eps_t;
   for (int64_t t = 0; t < M; ++t) {
@@ -473,7 +475,9 @@ EXPORT int or_scene_prep(const float* tris, const int32_t* mesh_ids, int64_t M, 
     int64_t t1 = t0;
     while (t1 < M && mesh_ids[t1] == m) ++t1;
     mesh_range[2 * m] = t0; mesh_range[2 * m + 1] = t1;
-    if (t1 > t0) {
+    if (mesh_sph_in) {   // bounding-volume update result: no recomputation
+      for (int k = 0; k < 4; ++k) mesh_sph[4 * m + k] = mesh_sph_in[4 * m + k];
+    } else if (t1 > t0) {
       or_miniball(tris + 9 * t0, 3 * (t1 - t0), mesh_sph + 4 * m);
       mesh_sph[4 * m + 3] += pad;
     } else {
@@ -905,4 +909,62 @@ EXPORT void or_gbuffer(int64_t P, const float* rays, const int32_t* hit_tri, con
     nrm[p] = n.x; nrm[P + p] = n.y; nrm[2 * P + p] = n.z;
     mat[p] = tri_mat[h];
   }
+}
+
+/* ---------------------------------------------------------------------------
+ * Dynamic scenes (§3.3.1 Bounding Volume Update, P:75-77;
+ * S:226-234): per-mesh affine transforms xf = [A | b] (3x4 row-major) applied
+ * to the creation-time vertices; the mesh spheres are UPDATED, not recomputed
+ * ("we only update the center and the radius"): c' = A c + b, r' = r sigma_max(A)
+ * (largest singular value, conservative), rounded up.
+ * ------------------------------------------------------------------------- */
+static inline float xf_axis(const float* xf, int row, float x, float y, float z) {
+  return fmaf(xf[4 * row], x, fmaf(xf[4 * row + 1], y, fmaf(xf[4 * row + 2], z, xf[4 * row + 3])));
+}
+
+EXPORT void or_transform(const float* tris, const int32_t* mesh_ids, int64_t M, const float* xf, float* out) {
+  for (int64_t t = 0; t < M; ++t) {
+    const float* a = xf + 12 * mesh_ids[t];
+    for (int v = 0; v < 3; ++v) {
+      const float* p = tris + 9 * t + 3 * v;
+      for (int r = 0; r < 3; ++r) out[9 * t + 3 * v + r] = xf_axis(a, r, p[0], p[1], p[2]);
+    }
+  }
+}
+
+/* sigma_max(A) = sqrt(largest eigenvalue of A^T A), closed form for the
+ * symmetric 3x3 (trigonometric method), double precision. */
+EXPORT double or_sigma_max(const float* xf) {
+  double A[3][3], S[3][3];
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) A[r][c] = (double)xf[4 * r + c];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) S[i][j] = A[0][i] * A[0][j] + A[1][i] * A[1][j] + A[2][i] * A[2][j];
+  const double p1 = S[0][1] * S[0][1] + S[0][2] * S[0][2] + S[1][2] * S[1][2];
+  double lam;
+  if (p1 == 0.0) {
+    lam = std::max(S[0][0], std::max(S[1][1], S[2][2]));
+  } else {
+    const double q = (S[0][0] + S[1][1] + S[2][2]) / 3.0;
+    const double p2 = (S[0][0] - q) * (S[0][0] - q) + (S[1][1] - q) * (S[1][1] - q) + (S[2][2] - q) * (S[2][2] - q) + 2.0 * p1;
+    const double p = std::sqrt(p2 / 6.0);
+    double B[3][3];
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) B[i][j] = (S[i][j] - (i == j ? q : 0.0)) / p;
+    const double det = B[0][0] * (B[1][1] * B[2][2] - B[1][2] * B[2][1]) - B[0][1] * (B[1][0] * B[2][2] - B[1][2] * B[2][0]) +
+                       B[0][2] * (B[1][0] * B[2][1] - B[1][1] * B[2][0]);
+    const double r = det / 2.0;
+    const double phi = r <= -1.0 ? M_PI / 3.0 : (r >= 1.0 ? 0.0 : std::acos(r) / 3.0);
+    lam = q + 2.0 * p * std::cos(phi);
+  }
+  return std::sqrt(std::max(lam, 0.0));
+}
+
+EXPORT void or_update_sphere(const float* sph, const float* xf, float* out) {
+  if (sph[3] < 0.0f) { for (int k = 0; k < 4; ++k) out[k] = sph[k]; return; }   // empty mesh
+  for (int r = 0; r < 3; ++r) out[r] = xf_axis(xf, r, sph[0], sph[1], sph[2]);
+  const double want = (double)sph[3] * or_sigma_max(xf);
+  float rf = (float)want;
+  if ((double)rf < want) rf = std::nextafter(rf, INFINITY);
+  out[3] = rf;
 }
