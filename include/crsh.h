@@ -187,6 +187,19 @@ crsh_status crsh_trace_secondary_packed(crsh_scene_t scene, const crsh_primary_h
 crsh_status crsh_trace_secondary_peer(crsh_scene_t scene, const crsh_primary_hits* hits, const float* lights,
                                       int32_t n_lights, uint32_t ray_types, const crsh_opts* opts,
                                       uint64_t* const* dst, int32_t n_dst, void* stream);
+/* Dynamic scenes (§3.3.1 Bounding Volume Update,
+ * P:75-77): move every mesh by an affine transform of its
+ * CREATION-time vertices. xforms: host [n_meshes][12] float32, row-major
+ * [A | b] (3x4); vertex' = (fma(a00, x, fma(a01, y, fma(a02, z, b0))), ...).
+ * Triangle data (e1, e2, minimal spheres) is rebuilt from the moved vertices
+ * with the creation pad; the mesh spheres are UPDATED, not recomputed
+ * ("since we only update the center and the radius there is no need to
+ * recalculate the bounding spheres"): c' = A c + b (same fma order),
+ * r' = r * sigma_max(A) rounded up (conservative; rigid motions keep r);
+ * the hash box becomes the moved vertices' AABB; eps_t stays. Synchronous.
+ * Errors: EINVAL for a null pointer or a non-finite entry. */
+crsh_status crsh_scene_transform(crsh_scene_t scene, const float* xforms);
+
 /* Trace an arbitrary batch of rays through the same pipeline (hash of the
  * bounce-ray layout, compress, sort, decompress, hierarchy, cull, traverse,
  * closest hit): the re-entry point the paper describes for the next set of

@@ -102,6 +102,8 @@ def load():
     L.crsh_trace_secondary_peer.restype = st
     L.crsh_trace_secondary_peer.argtypes = [vp, C.POINTER(PrimaryHits), vp, C.c_int32, C.c_uint32, C.POINTER(Opts),
                                             C.POINTER(C.c_uint64), C.c_int32, vp]
+    L.crsh_scene_transform.restype = st
+    L.crsh_scene_transform.argtypes = [vp, vp]
     L.crsh_trace_rays.restype = st
     L.crsh_trace_rays.argtypes = [vp, vp, C.c_int64, C.POINTER(Opts), vp, vp, vp]
     L.crsh_primary_gbuffer.restype = st
@@ -211,6 +213,13 @@ def trace_secondary_peer(scene: Scene, hits: PrimaryHits, lights, ray_types: int
     d = (C.c_uint64 * len(dst_ptrs))(*[int(x) for x in dst_ptrs])
     _check(load().crsh_trace_secondary_peer(scene.handle, C.byref(hits), arr.ctypes.data, n, ray_types,
                                             C.byref(opts), d, len(dst_ptrs), stream))
+
+
+def scene_transform(scene: Scene, xforms):
+    """crsh_scene_transform: host [n_meshes, 12] float32 affine [A | b] per mesh,
+    applied to the creation-time vertices."""
+    x = np.ascontiguousarray(np.asarray(xforms, np.float32).reshape(-1, 12))
+    _check(load().crsh_scene_transform(scene.handle, x.ctypes.data))
 
 
 def trace_rays(scene: Scene, rays, n: int, opts: Opts, hit_tri, t, stream=0):

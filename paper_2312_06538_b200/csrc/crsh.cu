@@ -224,6 +224,9 @@ struct crsh_scene {
   std::vector<std::array<Buf, 8>> wb;   // pos, nrm, dir, mat, direct, c_re, c_rr, L
   Buf w_hit, w_t, w_zero;
   Buf prim_rays;                        // crsh_primary_gbuffer camera rays
+  // dynamic scenes (crsh_scene_transform): creation-time geometry and spheres
+  Buf tris0, mesh_ids, tris_cur, xf, boxk;
+  std::vector<float> h_mesh_sph0;
 };
 
 namespace {
@@ -804,6 +807,13 @@ crsh_status crsh_scene_create(const float* tris, const int32_t* mesh_ids, int64_
     mesh_sphere(ht.data(), first[m], first[m] + count[m], sc->pad, &sc->h_mesh_sph[4 * m]);
   }
   ck(cudaMemcpy(sc->mesh_sph.p, sc->h_mesh_sph.data(), 16 * (size_t)n_meshes, cudaMemcpyHostToDevice), "copy mesh_sph");
+  sc->h_mesh_sph0 = sc->h_mesh_sph;
+  ck(ensure(sc->tris0, 36 * (size_t)M), "alloc tris0");
+  ck(ensure(sc->mesh_ids, 4 * (size_t)M), "alloc mesh_ids");
+  if (rc == CRSH_OK) {
+    ck(cudaMemcpy(sc->tris0.p, tris, 36 * (size_t)M, cudaMemcpyDeviceToDevice), "copy tris0");
+    ck(cudaMemcpy(sc->mesh_ids.p, mesh_ids, 4 * (size_t)M, cudaMemcpyDeviceToDevice), "copy mesh ids");
+  }
   ck(cudaMemcpy(sc->mesh_first.p, first.data(), 4 * (size_t)n_meshes, cudaMemcpyHostToDevice), "copy first");
   ck(cudaMemcpy(sc->mesh_count.p, count.data(), 4 * (size_t)n_meshes, cudaMemcpyHostToDevice), "copy count");
   for (int32_t m = 0; m < n_meshes; ++m) sc->n_nonempty += count[m] ? 1 : 0;
@@ -823,6 +833,7 @@ void crsh_scene_destroy(crsh_scene_t sc) {
   for (Buf* b : bufs) b->release();
   for (auto& w : sc->wb) for (auto& b : w) b.release();
   sc->w_hit.release(); sc->w_t.release(); sc->w_zero.release(); sc->prim_rays.release();
+  sc->tris0.release(); sc->mesh_ids.release(); sc->tris_cur.release(); sc->xf.release(); sc->boxk.release();
   if (sc->h_counters) cudaFreeHost(sc->h_counters);
   if (sc->h_fd) cudaFreeHost(sc->h_fd);
   if (sc->gexec) cudaGraphExecDestroy(sc->gexec);
@@ -857,6 +868,88 @@ crsh_status crsh_trace_secondary_peer(crsh_scene_t sc, const crsh_primary_hits* 
   }
   peer.n = n_dst;
   return trace_impl(sc, h, lights, n_lights, types, o, nullptr, nullptr, nullptr, peer, (cudaStream_t)stream);
+}
+
+}  // extern "C"
+
+namespace {
+// largest singular value of the 3x3 part of a row-major [A | b]: sqrt of the
+// largest eigenvalue of A^T A by the closed trigonometric form (double)
+double sigma_max3(const float* x) {
+  double A[3][3], S[3][3];
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) A[r][c] = (double)x[4 * r + c];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) S[i][j] = A[0][i] * A[0][j] + A[1][i] * A[1][j] + A[2][i] * A[2][j];
+  const double off = S[0][1] * S[0][1] + S[0][2] * S[0][2] + S[1][2] * S[1][2];
+  double lam;
+  if (off == 0.0) {
+    lam = std::max(S[0][0], std::max(S[1][1], S[2][2]));
+  } else {
+    const double q = (S[0][0] + S[1][1] + S[2][2]) / 3.0;
+    const double p2 = (S[0][0] - q) * (S[0][0] - q) + (S[1][1] - q) * (S[1][1] - q) + (S[2][2] - q) * (S[2][2] - q) + 2.0 * off;
+    const double p = std::sqrt(p2 / 6.0);
+    double Bm[3][3];
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) Bm[i][j] = (S[i][j] - (i == j ? q : 0.0)) / p;
+    const double det = Bm[0][0] * (Bm[1][1] * Bm[2][2] - Bm[1][2] * Bm[2][1]) -
+                       Bm[0][1] * (Bm[1][0] * Bm[2][2] - Bm[1][2] * Bm[2][0]) +
+                       Bm[0][2] * (Bm[1][0] * Bm[2][1] - Bm[1][1] * Bm[2][0]);
+    const double r = det / 2.0;
+    const double phi = r <= -1.0 ? M_PI / 3.0 : (r >= 1.0 ? 0.0 : std::acos(r) / 3.0);
+    lam = q + 2.0 * p * std::cos(phi);
+  }
+  return std::sqrt(std::max(lam, 0.0));
+}
+inline int float_key(float f) { const int i = __builtin_bit_cast(int, f); return i >= 0 ? i : (i ^ 0x7FFFFFFF); }
+inline float key_float(int k) { return __builtin_bit_cast(float, k >= 0 ? k : (k ^ 0x7FFFFFFF)); }
+}  // namespace
+
+extern "C" {
+
+crsh_status crsh_scene_transform(crsh_scene_t sc, const float* xforms) {
+  if (!sc || !xforms) return fail(CRSH_EINVAL, "null argument");
+  CK(cudaSetDevice(sc->device));
+  const int n = sc->n_meshes;
+  for (int i = 0; i < 12 * n; ++i)
+    if (!std::isfinite(xforms[i])) return fail(CRSH_EINVAL, "non-finite transform");
+  CK(ensure(sc->tris_cur, 36 * (size_t)sc->M));
+  CK(ensure(sc->xf, 48 * (size_t)n));
+  CK(ensure(sc->boxk, 32));
+  CK(cudaMemcpy(sc->xf.p, xforms, 48 * (size_t)n, cudaMemcpyHostToDevice));
+  const int init[6] = {float_key(INFINITY), float_key(INFINITY), float_key(INFINITY),
+                       float_key(-INFINITY), float_key(-INFINITY), float_key(-INFINITY)};
+  CK(cudaMemcpy(sc->boxk.p, init, sizeof init, cudaMemcpyHostToDevice));
+  const int grid = (int)std::min<int64_t>((sc->M + 255) / 256, 8 * sc->sm_count);
+  k_transform<<<grid, 256>>>(sc->tris0.as<float>(), sc->mesh_ids.as<int32_t>(), sc->M, sc->xf.as<float>(),
+                             sc->tris_cur.as<float>(), sc->boxk.as<float>());
+  CK(cudaGetLastError());
+  k_tri_prep<<<grid, 256>>>(sc->tris_cur.as<float>(), sc->M, sc->pad, sc->tri_e.as<float4>(), sc->tri_sph.as<float4>());
+  CK(cudaGetLastError());
+  int box[6];
+  CK(cudaMemcpy(box, sc->boxk.p, sizeof box, cudaMemcpyDeviceToHost));
+  for (int k = 0; k < 3; ++k) {
+    sc->box_min[k] = key_float(box[k]);
+    sc->box_max[k] = key_float(box[3 + k]);
+    sc->box_ext[k] = sc->box_max[k] - sc->box_min[k];
+  }
+  // bounding-volume update: centre transformed, radius scaled by
+  // sigma_max and rounded up -- the creation-time spheres are not recomputed
+  for (int m = 0; m < n; ++m) {
+    const float* s0 = &sc->h_mesh_sph0[4 * m];
+    float* s1 = &sc->h_mesh_sph[4 * m];
+    if (s0[3] < 0.0f) { for (int k = 0; k < 4; ++k) s1[k] = s0[k]; continue; }
+    const float* a = xforms + 12 * m;
+    for (int r = 0; r < 3; ++r)
+      s1[r] = std::fmaf(a[4 * r], s0[0], std::fmaf(a[4 * r + 1], s0[1], std::fmaf(a[4 * r + 2], s0[2], a[4 * r + 3])));
+    const double want = (double)s0[3] * sigma_max3(a);
+    float rf = (float)want;
+    if ((double)rf < want) rf = std::nextafter(rf, INFINITY);
+    s1[3] = rf;
+  }
+  CK(cudaMemcpy(sc->mesh_sph.p, sc->h_mesh_sph.data(), 16 * (size_t)n, cudaMemcpyHostToDevice));
+  ++sc->gen;   // scene constants changed: recapture the frame graph
+  return CRSH_OK;
 }
 
 crsh_status crsh_trace_rays(crsh_scene_t sc, const float* rays, int64_t n, const crsh_opts* o, int32_t* hit_tri,

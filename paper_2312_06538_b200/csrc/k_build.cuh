@@ -185,4 +185,42 @@ __global__ void __launch_bounds__(128) k_upper(const UpperArgs a) {
   store_node(a.nodes, a.trav, j, st[0]);
 }
 
+// ---------------------------------------------------------------- dynamic scenes
+// (§3.3.1): creation-time vertices -> per-mesh
+// affine transform [A | b] (row-major 3x4), per axis
+// fma(a0, x, fma(a1, y, fma(a2, z, b))); AABB of the result.
+__global__ void k_transform(const float* __restrict__ tris0, const int32_t* __restrict__ mesh_ids, int64_t M,
+                            const float* __restrict__ xf, float* __restrict__ tris, float* __restrict__ box /*6*/) {
+  float mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < M; t += (int64_t)gridDim.x * blockDim.x) {
+    const float* a = xf + 12 * __ldg(mesh_ids + t);
+    for (int v = 0; v < 3; ++v) {
+      const float x = tris0[9 * t + 3 * v], y = tris0[9 * t + 3 * v + 1], z = tris0[9 * t + 3 * v + 2];
+      for (int r = 0; r < 3; ++r) {
+        const float o = __fmaf_rn(a[4 * r], x, __fmaf_rn(a[4 * r + 1], y, __fmaf_rn(a[4 * r + 2], z, a[4 * r + 3])));
+        tris[9 * t + 3 * v + r] = o;
+        mn[r] = fminf(mn[r], o);
+        mx[r] = fmaxf(mx[r], o);
+      }
+    }
+  }
+  // min / max are exact and order-free: warp reduce, then one atomic per warp
+  // on the float bits ordered as integers (monotone map of IEEE floats)
+  for (int r = 0; r < 3; ++r) {
+    float lo = mn[r], hi = mx[r];
+    for (int o = 16; o > 0; o >>= 1) {
+      lo = fminf(lo, __shfl_xor_sync(CRSH_FULL, lo, o));
+      hi = fmaxf(hi, __shfl_xor_sync(CRSH_FULL, hi, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+      auto key = [](float f) {   // order-preserving float -> int
+        const int i = __float_as_int(f);
+        return i >= 0 ? i : (int)(i ^ 0x7FFFFFFF);
+      };
+      atomicMin(reinterpret_cast<int*>(box) + r, key(lo));
+      atomicMax(reinterpret_cast<int*>(box) + 3 + r, key(hi));
+    }
+  }
+}
+
 }  // namespace crsh

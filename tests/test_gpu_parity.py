@@ -365,3 +365,64 @@ def test_trace_rays_parity():
     ok = ref["hit_tri"] != -2
     bt, _ = oracle.unpack(oracle.brute(rays[ok], prep))
     assert np.array_equal(ref["hit_tri"][ok], bt)
+
+
+def _random_motion(n_meshes, seed, fixed=6):
+    r = np.random.default_rng(seed)
+    X = []
+    for m in range(n_meshes):
+        if m < fixed:
+            X.append(np.array([1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1, 0], np.float32))
+            continue
+        q, _ = np.linalg.qr(r.normal(size=(3, 3)))
+        q *= np.sign(np.linalg.det(q))
+        A = q @ np.diag(r.uniform(0.7, 1.3, 3))
+        X.append(np.concatenate([A, r.uniform(-1, 1, 3)[:, None]], axis=1).astype(np.float32).reshape(12))
+    return np.stack(X)
+
+
+@pytest.mark.parametrize("cfg,seed", [(1, 0), (2, 1)])
+def test_dynamic_scene_parity(cfg, seed):
+    """Dynamic scenes (NEXT-3, crsh_scene_transform): after moving the meshes
+    the scene constants, triangle spheres and updated mesh spheres are
+    bit-exact vs the oracle, and a primary pass + secondary frame of the moved
+    scene is bit-exact too; a second transform starts again from the
+    creation-time vertices."""
+    from workloads import make_camera
+    import dataclasses
+    w = make_workload(cfg, width=96, height=96)
+    prep0 = oracle.ScenePrep(w.tris, w.mesh_ids)
+    scene = crsh.Scene(torch.as_tensor(w.tris).cuda(), torch.as_tensor(w.mesh_ids).cuda())
+    tm = torch.as_tensor(w.tri_mat).cuda()
+    cam = make_camera()
+    W = H = 96
+    P = W * H
+    for k in range(2):
+        X = _random_motion(prep0.n_meshes, seed + 10 * k)
+        crsh.scene_transform(scene, X)
+        prep, tris = oracle.transformed_prep(prep0, w.tris, w.mesh_ids, X)
+        assert np.array_equal(crsh.debug_tap(scene, crsh.TAP_SCENE_CONSTS), prep.consts)
+        assert np.array_equal(crsh.debug_tap(scene, crsh.TAP_TRI_SPHERES).view(np.uint32), prep.tri_sph.view(np.uint32))
+        assert np.array_equal(crsh.debug_tap(scene, crsh.TAP_MESH_SPHERES), prep.mesh_sph[:prep.n_meshes])
+        # primary pass on the moved scene, then its secondary frame
+        opts = crsh.make_opts(w.levels, w.leaf_size, w.branching, 3)
+        pos = torch.empty(3 * P, dtype=torch.float32, device="cuda")
+        nrm = torch.empty(3 * P, dtype=torch.float32, device="cuda")
+        mat = torch.empty(P, dtype=torch.int32, device="cuda")
+        ph = torch.empty(P, dtype=torch.int32, device="cuda")
+        pt = torch.empty(P, dtype=torch.float32, device="cuda")
+        crsh.primary_gbuffer(scene, cam, W, H, tm, opts, pos, nrm, mat, ph, pt)
+        rpos, rnrm, rmat, rhit, rt, _ = oracle.primary_gbuffer(tris, w.mesh_ids, w.tri_mat, cam, W, H, w.levels,
+                                                               w.leaf_size, w.branching, 3, prep=prep)
+        assert np.array_equal(ph.cpu().numpy(), rhit) and np.array_equal(mat.cpu().numpy(), rmat)
+        wm = dataclasses.replace(w, tris=tris, width=W, height=H, pos=rpos, nrm=rnrm, mat=rmat)
+        hits = crsh.make_hits(W, H, pos, nrm, mat, torch.as_tensor(w.materials).cuda(), w.materials.shape[0], w.eye)
+        slots = crsh.num_slots(P, w.lights.shape[0], w.ray_types)
+        hit = torch.empty(slots, dtype=torch.int32, device="cuda")
+        t = torch.empty(slots, dtype=torch.float32, device="cuda")
+        crsh.trace_secondary(scene, hits, w.lights, w.ray_types, opts, hit, t)
+        torch.cuda.synchronize()
+        ref = oracle.trace(wm, prep)
+        assert np.array_equal(hit.cpu().numpy(), ref["hit_tri"])
+        assert np.array_equal(t.cpu().numpy().view(np.uint32), ref["t"].view(np.uint32))
+        assert_counts_equal(crsh.stats(scene), ref)
