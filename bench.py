@@ -499,6 +499,76 @@ def run_whitted(args):
     print(json.dumps(line), flush=True)
 
 
+def run_animate(args):
+    """Animated scene (the paper's multi-frame averages,
+    P:307): every frame moves the object meshes (crsh_scene_transform: a
+    rotation about each object's vertical axis plus a bob), renders the
+    G-buffer with the GPU primary pass (crsh_primary_gbuffer) and traces the
+    secondary rays; the frame time is averaged over the animation (not the
+    contract line)."""
+    import torch
+
+    import paper_2312_06538_b200 as crsh
+    from workloads import make_camera, make_workload
+    w = make_workload(args.config)
+    flags = 7 if args.zorder else 3
+    scene = crsh.Scene(torch.as_tensor(w.tris).cuda(), torch.as_tensor(w.mesh_ids).cuda())
+    tm = torch.as_tensor(w.tri_mat).cuda()
+    mats = torch.as_tensor(w.materials).cuda()
+    cam = make_camera()
+    W, H, P = w.width, w.height, w.width * w.height
+    opts = crsh.make_opts(w.levels, w.leaf_size, w.branching, flags)
+    pos = torch.empty(3 * P, dtype=torch.float32, device="cuda")
+    nrm = torch.empty(3 * P, dtype=torch.float32, device="cuda")
+    mat = torch.empty(P, dtype=torch.int32, device="cuda")
+    ph = torch.empty(P, dtype=torch.int32, device="cuda")
+    pt = torch.empty(P, dtype=torch.float32, device="cuda")
+    slots = crsh.num_slots(P, w.lights.shape[0], w.ray_types)
+    hit = torch.empty(slots, dtype=torch.int32, device="cuda")
+    t = torch.empty(slots, dtype=torch.float32, device="cuda")
+    hits = crsh.make_hits(W, H, pos, nrm, mat, mats, w.materials.shape[0], w.eye)
+    n_m = int(w.mesh_ids.max()) + 1
+    tris = w.tris.reshape(-1, 3, 3).astype(np.float64)
+    centres = np.stack([tris[w.mesh_ids == m].reshape(-1, 3).mean(0) for m in range(n_m)])
+    n_walls = 6
+
+    def xforms(f):
+        X = np.zeros((n_m, 12), np.float32)
+        for m in range(n_m):
+            a = 0.0 if m < n_walls else 2 * np.pi * f / max(1, args.animate) * (1 + m % 3)
+            c, s_ = np.cos(a), np.sin(a)
+            R = np.array([[c, 0, s_], [0, 1, 0], [-s_, 0, c]])
+            b = centres[m] - R @ centres[m] + (0 if m < n_walls else np.array([0, 0.2 * np.sin(a), 0]))
+            X[m] = np.concatenate([R, b[:, None]], axis=1).reshape(12)
+        return X
+
+    stream = torch.cuda.current_stream()
+    ms, rays, tms = [], 0, []
+    for f in range(args.animate + 3):
+        X = xforms(f)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        crsh.scene_transform(scene, X)
+        t1 = time.perf_counter()
+        a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a_.record(stream)
+        crsh.primary_gbuffer(scene, cam, W, H, tm, opts, pos, nrm, mat, ph, pt, stream.cuda_stream)
+        crsh.trace_secondary(scene, hits, w.lights, w.ray_types, opts, hit, t, stream.cuda_stream)
+        b_.record(stream)
+        torch.cuda.synchronize()
+        if f >= 3:
+            ms.append(a_.elapsed_time(b_))
+            tms.append((t1 - t0) * 1e3)
+            rays += int(sum(crsh.stats(scene)["rays"]))
+    line = {"mode": "animate", "metric": "secondary Mrays/s averaged over an animation (moving meshes, GPU primary pass)",
+            "unit": "Mrays/s", "value": round(rays / (sum(ms) * 1e-3) / 1e6, 3), "frames": args.animate,
+            "ms_per_frame_primary_plus_secondary": round(float(np.mean(ms)), 3),
+            "ms_per_frame_transform_host_wall": round(float(np.mean(tms)), 3), "primary_rays_per_frame": P,
+            "secondary_rays_per_frame": rays // max(1, len(ms)), "hash": "zorder" if args.zorder else "R6",
+            "workload": w.name}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -513,7 +583,11 @@ def main():
     ap.add_argument("--sweep", action="store_true", help="cfg5 depth/bundle sweep (not the contract line)")
     ap.add_argument("--whitted", type=int, default=None, metavar="D",
                     help="multi-bounce Whitted loop of depth D (NEXT-2; not the contract line)")
+    ap.add_argument("--animate", type=int, default=None, metavar="F",
+                    help="F animated frames: moving meshes + GPU primary pass + secondary trace (NEXT-3)")
     args = ap.parse_args()
+    if args.animate is not None:
+        return run_animate(args)
     if args.whitted is not None:
         return run_whitted(args)
     if args.table4:
