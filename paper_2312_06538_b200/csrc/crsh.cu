@@ -289,7 +289,10 @@ cudaError_t dispatch_b(int B, F&& f) {
   return cudaErrorInvalidValue;
 }
 
-constexpr uint32_t ITEM_TRIS = 2048;   // triangles per traversal work item (load balance)
+#ifndef CRSH_ITEM_TRIS
+#define CRSH_ITEM_TRIS 2048
+#endif
+constexpr uint32_t ITEM_TRIS = CRSH_ITEM_TRIS;   // triangles per traversal work item (load balance)
 
 // Everything a frame's launch sequence depends on: if the key of a call equals
 // the cached one, the cached CUDA graph is replayed.
