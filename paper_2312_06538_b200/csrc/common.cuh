@@ -154,8 +154,17 @@ __device__ __forceinline__ void warp_seg_add(unsigned long long* base, int strid
   }
 }
 
+// Block-wide exclusive scan of one uint32 per thread (blockDim.x == 32 NW).
+template <int NW>
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp /*NW*/, uint32_t* total);
+
 // Block-wide exclusive scan of one uint32 per thread (blockDim.x == 256).
 __device__ __forceinline__ uint32_t block_excl_scan_256(uint32_t v, uint32_t* s_warp /*8*/, uint32_t* total) {
+  return block_excl_scan<8>(v, s_warp, total);
+}
+
+template <int NW>
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp /*NW*/, uint32_t* total) {
   const int lane = (int)lane_id(), warp = threadIdx.x >> 5;
   uint32_t incl = v;
 #pragma unroll
@@ -167,7 +176,7 @@ __device__ __forceinline__ uint32_t block_excl_scan_256(uint32_t v, uint32_t* s_
   __syncthreads();
   uint32_t wpre = 0, tot = 0;
 #pragma unroll
-  for (int w = 0; w < 8; ++w) {
+  for (int w = 0; w < NW; ++w) {
     const uint32_t x = s_warp[w];
     wpre += (w < warp) ? x : 0u;
     tot += x;

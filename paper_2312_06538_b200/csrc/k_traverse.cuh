@@ -286,7 +286,10 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_plan(const PlanArgs a) {
 //    is taken from the LOWEST level that has a full step, so the queues stay
 //    bounded and persist across slices; the rest is drained at the item end.
 // No block barrier is executed inside the hot loop.
-constexpr int TRAV_THREADS = 256;
+#ifndef CRSH_TRAV_THREADS
+#define CRSH_TRAV_THREADS 256
+#endif
+constexpr int TRAV_THREADS = CRSH_TRAV_THREADS;
 constexpr int TRAV_WARPS = TRAV_THREADS / 32;
 constexpr uint32_t SMALL_GROUP_RAYS = 512;   // groups up to this size live in shared memory
 constexpr int LOWQ = 64;                     // capacity of a warp queue below level Lv-1
@@ -374,7 +377,7 @@ __global__ void __launch_bounds__(TRAV_THREADS, CRSH_TRAV_MINB) k_traverse(const
   float4* s_pairs = reinterpret_cast<float4*>(smraw + L.off_pairs);
   float4* s_tpairs = reinterpret_cast<float4*>(smraw + L.off_tpairs);
   __shared__ uint32_t s_item, s_cur_g, s_n_act, s_carry, s_carry_c;
-  __shared__ uint32_t s_warp[8];
+  __shared__ uint32_t s_warp[TRAV_WARPS];
   __shared__ unsigned long long s_ctr[MAX_SEG * CTR_STRIDE];
   __shared__ uint32_t s_qlen[TRAV_WARPS][MAX_LEVELS + 1];
   // per-level tables copied out of the kernel parameters: a runtime index into
@@ -506,8 +509,8 @@ __global__ void __launch_bounds__(TRAV_THREADS, CRSH_TRAV_MINB) k_traverse(const
         }
         const uint32_t act = nm ? 1u : 0u;
         uint32_t tot_a, tot_c;
-        const uint32_t ea = block_excl_scan_256(act, s_warp, &tot_a);
-        const uint32_t ec = block_excl_scan_256(cnt, s_warp, &tot_c);
+        const uint32_t ea = block_excl_scan<TRAV_WARPS>(act, s_warp, &tot_a);
+        const uint32_t ec = block_excl_scan<TRAV_WARPS>(cnt, s_warp, &tot_c);
         const uint32_t base_a = s_carry, base_c = s_carry_c;
         if (act) {
           s_act_nmask[base_a + ea] = nm;
