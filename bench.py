@@ -309,7 +309,7 @@ def run_crsh(args):
     out = {
         "metric": METRIC, "value": round(mrays, 3), "unit": "Mrays/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
-        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f32",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded procedural scene + rasterised G-buffer, workloads/)",
         "config": {"workload": w.name, "pixels": w.width * w.height, "triangles": tr.M, "meshes": int(w.n_meshes),
                    "ray_types": w.ray_types, "lights": int(w.lights.shape[0]), "levels": w.levels,
@@ -365,7 +365,7 @@ def run_reference(args):
     v = rays / sum(times) / 1e6
     out = {"metric": METRIC, "value": round(v, 5), "unit": "Mrays/s", "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": round(1e3 * sum(times) / len(times), 2), "higher_is_better": True,
-           "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
+           "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
            "config": {"workload": w.name},
            "cpu_baseline": {"value": round(v, 5), "unit": "Mrays/s", "cores": oracle.default_threads(),
                             "kind": "oracle", "sample": f"{rows_probe} of {w.height} image rows per step"},
