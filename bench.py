@@ -181,9 +181,19 @@ def run_crsh(args):
     # stays the path if the symmetric window is unavailable or disagrees).
     merge, hdl, ptrs, sbuf = ("none" if world == 1 else "nccl"), None, None, None
     if world > 1 and not args.nccl_merge:
+        # every rank allocates first and the ranks agree before the collective
+        # rendezvous, so one rank's failure cannot leave the others waiting in it
         try:
             import torch.distributed._symmetric_memory as symm_mem
             sbuf = symm_mem.empty(max(tr.slots, 1), dtype=torch.int64, device=torch.device("cuda", local))
+            ok_alloc = 1
+        except Exception as e:
+            print(f"[bench] symmetric allocation failed ({type(e).__name__}: {e})", file=sys.stderr)
+            ok_alloc = 0
+        flag = torch.tensor([ok_alloc], dtype=torch.int32, device="cuda")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    if world > 1 and not args.nccl_merge and int(flag) == 1:
+        try:
             hdl = symm_mem.rendezvous(sbuf, dist.group.WORLD)
             ptrs = [int(hdl.buffer_ptrs[r]) for r in range(world)]
             hdl.barrier()
