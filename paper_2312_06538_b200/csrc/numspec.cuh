@@ -285,30 +285,6 @@ __device__ __forceinline__ void cull2_ns(const float4* rec, f2 Px, f2 Py, f2 Pz,
 }  // namespace crsh
 
 namespace crsh {
-// Eq 9 for ONE node (broadcast scalars, traversal layout {C, d} {a, tan}
-// {sec, -, -, -}) against TWO target spheres packed per coordinate (Px =
-// {x_0, x_1}, ...); same operation order as cull_ns for each half. The node
-// scalars enter FFMA2/FADD2 as broadcast operands (w = v + s * (-a) equals
-// fma(-s, a, v) exactly: negation is exact).
-__device__ __forceinline__ void cull_t2_ns(float4 n0, float4 n1, float sc, f2 Px, f2 Py, f2 Pz, f2 R, bool& p0,
-                                           bool& p1) {
-  const f2 vx = sub2(Px, pk2(n0.x, n0.x)), vy = sub2(Py, pk2(n0.y, n0.y)), vz = sub2(Pz, pk2(n0.z, n0.z));
-  const f2 s = fma2(vx, pk2(n1.x, n1.x), fma2(vy, pk2(n1.y, n1.y), mul2(vz, pk2(n1.z, n1.z))));
-  const f2 wx = fma2(s, pk2(-n1.x, -n1.x), vx), wy = fma2(s, pk2(-n1.y, -n1.y), vy), wz = fma2(s, pk2(-n1.z, -n1.z), vz);
-  const f2 w2 = fma2(wx, wx, fma2(wy, wy, mul2(wz, wz)));
-  const f2 dr = add2(pk2(n0.w, n0.w), R);
-  float s0, s1;
-  up2(s, s0, s1);
-  const f2 rhs = fma2(pk2(fmaxf(s0, 0.0f), fmaxf(s1, 0.0f)), pk2(n1.w, n1.w), mul2(dr, pk2(sc, sc)));
-  const f2 rr = mul2(rhs, rhs);
-  float w0, w1, r0, r1, d0, d1;
-  up2(w2, w0, w1);
-  up2(rr, r0, r1);
-  up2(dr, d0, d1);
-  p0 = (s0 >= -d0) & (w0 <= r0);
-  p1 = (s1 >= -d1) & (w1 <= r1);
-}
-
 // Moller-Trumbore (mt_ns, same per-half operation order) for two rays given
 // as a paired record {ox0,ox1,oy0,oy1} {oz0,oz1,tmin0,tmin1}
 // {dx0,dx1,dy0,dy1} {dz0,dz1,tmax0,tmax1} against one triangle; the
