@@ -426,3 +426,40 @@ def test_dynamic_scene_parity(cfg, seed):
         assert np.array_equal(hit.cpu().numpy(), ref["hit_tri"])
         assert np.array_equal(t.cpu().numpy().view(np.uint32), ref["t"].view(np.uint32))
         assert_counts_equal(crsh.stats(scene), ref)
+
+
+@pytest.mark.parametrize("levels,leaf,branch,lights", [(2, 64, 32, 3), (8, 2, 2, 1), (5, 4, 4, 16), (1, 2, 2, 16),
+                                                       (6, 8, 2, 2)])
+def test_option_extremes(levels, leaf, branch, lights):
+    """Extremes of the option space: the widest bundles and nodes (B0 64,
+    B 32: span 2048 > 512 rays, K = 1, global-memory groups), the deepest
+    hierarchy (Lv 8 of binary nodes), 16 lights (the hash's 4-bit light
+    field), Lv 1 with 16 lights; hits, counts and every tap bit-exact."""
+    w = make_workload(1, width=40, height=36, levels=levels, leaf_size=leaf, branching=branch, ray_types=1)
+    r = np.random.default_rng(lights)
+    w.lights = np.stack([r.uniform(1, 9, lights), r.uniform(8.5, 9.5, lights), r.uniform(1, 9, lights)], 1).astype(np.float32)
+    tr, hit, t, ref = run_both(w, crsh.F_SORT | crsh.F_MESH_CULL)
+    assert len(ref["stats"]["tests"]) == 3 and ref["stats"]["rays"][0] > 0
+    assert np.array_equal(hit, ref["hit_tri"]) and np.array_equal(t.view(np.uint32), ref["t"].view(np.uint32))
+    assert_counts_equal(crsh.stats(tr.scene), ref)
+    assert_taps_equal(tr, ref, w)
+
+
+def test_api_errors():
+    """Synchronous argument / limit errors (include/crsh.h): nothing is
+    enqueued and the binding raises."""
+    w = make_workload(1, width=16, height=16)
+    tr = tracer_for(w)
+    bad = [dict(levels=9), dict(leaf_size=3), dict(leaf_size=128), dict(branching=64), dict(levels=8, leaf_size=64,
+                                                                                             branching=32)]
+    for kw in bad:
+        opts = crsh.make_opts(**{**dict(levels=2, leaf_size=8, branching=8), **kw})
+        with pytest.raises(Exception):
+            crsh.trace_secondary(tr.scene, tr.hits, w.lights, w.ray_types, opts, tr.hit_tri, tr.t)
+    with pytest.raises(Exception):   # 17 lights exceed the 4-bit light field (S:243)
+        crsh.trace_secondary(tr.scene, tr.hits, np.zeros((17, 3), np.float32), 1, tr.opts, tr.hit_tri, tr.t)
+    with pytest.raises(Exception):   # no ray type
+        crsh.trace_secondary(tr.scene, tr.hits, w.lights, 0, tr.opts, tr.hit_tri, tr.t)
+    tr.run()   # the scene is still usable
+    hit, _ = tr.results()
+    assert np.array_equal(hit, oracle.trace(w)["hit_tri"])
