@@ -54,7 +54,24 @@ def _worker(rank, world, port, q):
     hit, t = cd.decode_packed(packed.numpy())
     cnt = torch.tensor([rank + 1, 10 * (rank + 1)], dtype=torch.int64)
     cd.merge_counters(cnt)
-    q.put((rank, np.array_equal(hit, out["hit_tri"]), np.array_equal(t, out["t"]), cnt.tolist(),
+    # fused peer-store semantics (crsh_trace_secondary_peer): every rank stores
+    # its OWNED slots into every destination and the empty sentinel into
+    # ray-less slots; other slots are untouched. Emulated with an all_gather
+    # of each rank's stores applied to a garbage-initialised window.
+    mine = owner == rank
+    empty = out["hit_tri"] == -2
+    vals = torch.from_numpy(cd.encode_owned(out["hit_tri"], out["t"], mine | empty).copy())
+    mask = torch.from_numpy((mine | empty).astype(np.uint8))
+    gv = [torch.empty_like(vals) for _ in range(world)]
+    gm = [torch.empty_like(mask) for _ in range(world)]
+    dist.all_gather(gv, vals)
+    dist.all_gather(gm, mask)
+    window = torch.full_like(vals, 0x5A5A5A5A5A5A5A5A)
+    for v_, m_ in zip(gv, gm):
+        window[m_.bool()] = v_[m_.bool()]
+    hp, tp = cd.decode_packed(window.numpy())
+    peer_ok = np.array_equal(hp, out["hit_tri"]) and np.array_equal(tp, out["t"])
+    q.put((rank, np.array_equal(hit, out["hit_tri"]) and peer_ok, np.array_equal(t, out["t"]), cnt.tolist(),
            int((owner == rank).sum())))
     dist.destroy_process_group()
 
