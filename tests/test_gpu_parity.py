@@ -156,6 +156,48 @@ def test_cfg3_sampled_vs_brute():
         assert st["final_tests"][seg] <= 8 * st["hits"][seg][1]
 
 
+@pytest.mark.parametrize("cfg,flags,n_pick", [(3, 3, 2048), (4, 7, 512), (4, 3, 256)])
+def test_large_configs_sampled_vs_brute(cfg, flags, n_pick):
+    """cfg3 with the R6 layout and cfg4 (1920x1080, 4 lights, ~1M triangles in
+    100 meshes; both layouts) at full size: sampled rays against N x M brute
+    force, every empty slot -2, monotone per-level culling."""
+    w = make_workload(cfg)
+    tr = tracer_for(w, flags=flags)
+    tr.run()
+    hit, t = tr.results()
+    prep = oracle.ScenePrep(w.tris, w.mesh_ids)
+    rays, keys, empty = oracle.generate(w, prep, flags)
+    ok = np.flatnonzero(empty == 0)
+    pick = np.random.default_rng(cfg + flags).choice(ok, size=n_pick, replace=False)
+    bt, btt = oracle.unpack(oracle.brute(rays[pick], prep))
+    assert np.array_equal(hit[pick], bt) and np.array_equal(t[pick].view(np.uint32), btt.view(np.uint32))
+    assert np.all(hit[empty == 1] == -2)
+    st = crsh.stats(tr.scene)
+    assert sum(st["rays"]) == len(ok)
+    for seg in range(3):
+        assert st["tests"][seg][1] <= 8 * st["hits"][seg][2] and st["final_tests"][seg] <= 8 * st["hits"][seg][1]
+
+
+def test_slot_limit_and_degenerate_triangles():
+    """ELIMIT before any work for >= 2^30 slots; degenerate (zero-area)
+    triangles never hit, on the GPU as in the oracle and brute force."""
+    w = make_workload(1, width=16, height=16)
+    tr = tracer_for(w)
+    big = crsh.make_hits(1 << 15, 1 << 15, tr.pos, tr.nrm, tr.mat, tr.materials, int(w.materials.shape[0]), w.eye)
+    with pytest.raises(Exception):
+        crsh.trace_secondary(tr.scene, big, w.lights, 7, tr.opts, tr.hit_tri, tr.t)
+    r = np.random.default_rng(8)
+    w = make_micro(777, n_tris=120, W=24, H=24, n_meshes=5, n_lights=2, ray_types=7, empty_frac=0.1)
+    tris = w.tris.reshape(-1, 3, 3).copy()
+    deg = r.choice(len(tris), 40, replace=False)
+    tris[deg[:20], 2] = tris[deg[:20], 1]                                   # repeated vertex
+    tris[deg[20:], 2] = 2 * tris[deg[20:], 1] - tris[deg[20:], 0]          # collinear
+    w.tris = tris.reshape(-1, 9).astype(np.float32)
+    tr, hit, t, ref = run_both(w, crsh.F_SORT | crsh.F_MESH_CULL, taps=False)
+    assert np.array_equal(hit, ref["hit_tri"]) and np.array_equal(t.view(np.uint32), ref["t"].view(np.uint32))
+    assert not np.isin(hit, deg[:20]).any()
+
+
 def test_edge_cases():
     # no valid pixel at all
     w = make_micro(1, n_tris=10, W=8, H=8, empty_frac=1.0)
