@@ -70,3 +70,39 @@ def test_product_never_imports_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 src = open(os.path.join(root, f)).read()
                 assert "import oracle" not in src and "from oracle" not in src and "oracle.cpp" not in src, f
+
+
+def test_packed_arithmetic_not_contracted():
+    """NUMSPEC fixes every rounding: ptxas must not fuse a packed
+    multiply into a following add (it does fuse mul.rn.f32x2 + sub.rn.f32x2
+    into FFMA2 when the product has a single use, even under --fmad=false).
+    Per kernel, the SASS of the built library must hold exactly the FFMA2 /
+    FMUL2 / FADD2 the PTX asks for."""
+    import re
+    import shutil
+    import subprocess
+    import tempfile
+    from paper_2312_06538_b200 import build as nb
+    nvcc, cuobjdump = nb.NVCC, shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not (os.path.exists(nvcc) and os.path.exists(cuobjdump)):
+        pytest.skip("CUDA toolchain not available")
+    lib = nb.build()
+    with tempfile.TemporaryDirectory() as d:
+        ptx_path = os.path.join(d, "crsh.ptx")
+        flags = [f for f in nb.FLAGS if f not in ("-shared", "-Xcompiler", "-fPIC", "-cudart", "static", "-lineinfo")]
+        subprocess.check_call([nvcc, *flags, "-ptx", "-o", ptx_path, nb.SRC])
+        ptx = open(ptx_path).read()
+    sass = subprocess.run([cuobjdump, "-sass", lib], capture_output=True, text=True).stdout
+    want = {}
+    for e in re.split(r"\n\.visible \.entry ", ptx)[1:]:
+        name = e.split("(", 1)[0]
+        want[name] = (len(re.findall(r"fma\.rn\.f32x2", e)), len(re.findall(r"mul\.rn\.f32x2", e)),
+                      len(re.findall(r"(?:add|sub)\.rn\.f32x2", e)))
+    checked = 0
+    for f in re.split(r"\n\s*Function : ", sass)[1:]:
+        name = f.split("\n", 1)[0].strip()
+        if name in want and sum(want[name]):
+            got = (len(re.findall(r"\bFFMA2 ", f)), len(re.findall(r"\bFMUL2 ", f)), len(re.findall(r"\bFADD2 ", f)))
+            assert got == want[name], (name, got, want[name])
+            checked += 1
+    assert checked >= 4   # the k_traverse variants at least
