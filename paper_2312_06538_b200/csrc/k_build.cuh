@@ -71,7 +71,8 @@ __global__ void k_tri_prep(const float* __restrict__ tris, int64_t M, float pad,
 }
 
 // ------------------------------------------------------------ nodes
-__device__ __forceinline__ void store_node(float4* nodes, float4* trav, size_t j, const NodeV& n) {
+// so: (leaves) every ray of the bundle starts at the node centre, bit for bit
+__device__ __forceinline__ void store_node(float4* nodes, float4* trav, size_t j, const NodeV& n, bool so = false) {
   nodes[2 * j] = make_float4(n.c.x, n.c.y, n.c.z, n.r);
   nodes[2 * j + 1] = make_float4(n.a.x, n.a.y, n.a.z, n.alpha);
   // traversal layout: {c, d}, {a, tan(alpha)}, {sec(alpha), 0, 0, 0};
@@ -84,7 +85,7 @@ __device__ __forceinline__ void store_node(float4* nodes, float4* trav, size_t j
   }
   trav[3 * j] = make_float4(n.c.x, n.c.y, n.c.z, n.r);
   trav[3 * j + 1] = make_float4(a.x, a.y, a.z, tn);
-  trav[3 * j + 2] = make_float4(sc, 0.f, 0.f, 0.f);
+  trav[3 * j + 2] = make_float4(sc, so ? 1.0f : 0.0f, 0.f, 0.f);
 }
 __device__ __forceinline__ NodeV load_node(const float4* nodes, size_t j) {
   const float4 p = nodes[2 * j], q = nodes[2 * j + 1];
@@ -120,6 +121,8 @@ __global__ void __launch_bounds__(128) k_leaves(const LeafArgs a) {
   float sr[B0];
   f3 x = mk3(0.f, 0.f, 1.f);
   float phi = 0.0f;
+  bool same = true;   // all real rays share the first ray's origin, bit for bit
+  f3 o0 = mk3(0.f, 0.f, 0.f);
 #pragma unroll
   for (int i = 0; i < B0; ++i) {
     float4 r0, r1;
@@ -135,6 +138,10 @@ __global__ void __launch_bounds__(128) k_leaves(const LeafArgs a) {
     a.sorted_rays[2 * (size_t)(p0 + i) + 1] = r1;
     sc[i] = mk3(r0.x, r0.y, r0.z);
     sr[i] = (i < real) ? 0.0f : -1.0f;
+    if (i == 0) o0 = sc[0];
+    if (i > 0 && i < real)
+      same = same && __float_as_uint(r0.x) == __float_as_uint(sc[0].x) && __float_as_uint(r0.y) == __float_as_uint(sc[0].y) &&
+             __float_as_uint(r0.z) == __float_as_uint(sc[0].z);
     if (i < real) {
       const f3 d = mk3(r1.x, r1.y, r1.z);
       if (i == 0) { x = d; phi = 0.0f; }     // leaves start as radius 0 / angle 0
@@ -157,7 +164,10 @@ __global__ void __launch_bounds__(128) k_leaves(const LeafArgs a) {
   } else {
     n.c = sc[0]; n.r = sr[0]; n.a = x; n.alpha = phi;
   }
-  store_node(a.nodes, a.trav, j, n);
+  // shared-origin flag for the final tests: the centre then equals that origin
+  const bool so = real > 0 && same && __float_as_uint(n.c.x) == __float_as_uint(o0.x) &&
+                  __float_as_uint(n.c.y) == __float_as_uint(o0.y) && __float_as_uint(n.c.z) == __float_as_uint(o0.z);
+  store_node(a.nodes, a.trav, j, n, so);
 }
 
 struct UpperArgs {

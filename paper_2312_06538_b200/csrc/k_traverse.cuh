@@ -547,6 +547,36 @@ __global__ void __launch_bounds__(TRAV_THREADS, CRSH_TRAV_MINB) k_traverse(const
         const f3 v0 = mk3(tv0.x, tv0.y, tv0.z), e1 = mk3(te1.x, te1.y, te1.z), e2 = mk3(te2.x, te2.y, te2.z);
         const uint32_t rl0 = e.x << logB0;   // first ray of the bundle (B0 even)
         const uint32_t nr = min((uint32_t)B0, g_real - rl0);   // real rays of the bundle (>= 1: the bundle exists)
+        // the bundle's leaf record: {c, d}, {a, tan}, {sec, shared-origin flag} (k_leaves)
+        const float4* lf = Lv == 1 ? s_top + 3 * e.x
+                                   : (SMALL ? s_nodes + s_noff[1] + 3 * e.x : s_trav[1] + 3 * ((size_t)g * s_pg[1] + e.x));
+        const bool shared_o = SMALL ? lf[2].y != 0.0f : __ldg(&lf[2].y) != 0.0f;
+        if (shared_o && SMALL) {   // all rays start at the leaf centre: per-(bundle, triangle) terms once
+          const float4 c0 = lf[0];
+          const f3 tv = mk3(c0.x, c0.y, c0.z) - v0;
+          const f3 qv = cross3(tv, e1);
+          const float tq = dot3(e2, qv);
+#pragma unroll
+          for (int r = 0; r < (B0T ? B0T : 64); r += 2) {
+            if (!B0T && r >= B0) break;
+            if ((uint32_t)r >= nr) break;
+            const uint32_t rl = rl0 + (uint32_t)r;
+            const float4* rp = s_rays + 2 * rl;
+            const uint32_t sw = ray_swz(rl >> 1);
+            const float4 Bq = rp[1u ^ sw], Cq = rp[2u ^ sw], Dq = rp[3u ^ sw];
+            const bool real1 = (uint32_t)r + 1u < nr;
+            c_mt_t += 1u + (uint32_t)real1;
+            bool h0, h1;
+            float t0, t1;
+            mt2o_ns(Bq, Cq, Dq, e1, e2, tv, qv, tq, h0, t0, h1, t1);
+            h1 &= real1;
+            if (h0 | h1) {
+              c_mt_h += (uint32_t)h0 + (uint32_t)h1;
+              if (h0) atomicMin(s_best + rl, pack_hit(t0, e.y));
+              if (h1) atomicMin(s_best + rl + 1, pack_hit(t1, e.y));
+            }
+          }
+        } else
 #pragma unroll
         for (int r = 0; r < (B0T ? B0T : 64); r += 2) {
           if (!B0T && r >= B0) break;

@@ -331,4 +331,42 @@ __device__ __forceinline__ void mt2_ns(float4 A, float4 Bq, float4 Cq, float4 Dq
   h0 = k0 & (t0 > Bq.z) & (t0 < Dq.z);
   h1 = k1 & (t1 > Bq.w) & (t1 < Dq.w);
 }
+
+// mt2_ns for two rays that share their origin o (bit for bit): tv = o - v0,
+// q = cross(tv, e1) and tq = dot(e2, q) are passed in, computed once for the
+// bundle -- exactly the values mt2_ns computes per ray, so the decisions and
+// t are bit-identical. Ray record halves: Bq = {-, -, tmin0, tmin1},
+// Cq = {dx0, dx1, dy0, dy1}, Dq = {dz0, dz1, tmax0, tmax1}.
+__device__ __forceinline__ void mt2o_ns(float4 Bq, float4 Cq, float4 Dq, f3 e1, f3 e2, f3 tv, f3 q, float tq, bool& h0,
+                                        float& t0, bool& h1, float& t1) {
+  const f2 dx = pk2(Cq.x, Cq.y), dy = pk2(Cq.z, Cq.w), dz = pk2(Dq.x, Dq.y);
+  const f2 px = fma2(dy, pk2(e2.z, e2.z), mul2(dz, pk2(-e2.y, -e2.y)));
+  const f2 py = fma2(dz, pk2(e2.x, e2.x), mul2(dx, pk2(-e2.z, -e2.z)));
+  const f2 pz = fma2(dx, pk2(e2.y, e2.y), mul2(dy, pk2(-e2.x, -e2.x)));
+  const f2 det = fma2(pk2(e1.x, e1.x), px, fma2(pk2(e1.y, e1.y), py, mul2(pk2(e1.z, e1.z), pz)));
+  float d0, d1;
+  up2(det, d0, d1);
+  const f2 sg = pk2(d0 > 0.0f ? 1.0f : -1.0f, d1 > 0.0f ? 1.0f : -1.0f);
+  const f2 adet = mul2(det, sg);
+  const f2 un = mul2(fma2(pk2(tv.x, tv.x), px, fma2(pk2(tv.y, tv.y), py, mul2(pk2(tv.z, tv.z), pz))), sg);
+  float u0, u1, a0v, a1v;
+  up2(un, u0, u1);
+  up2(adet, a0v, a1v);
+  bool k0 = (d0 != 0.0f) & (u0 >= 0.0f) & (u0 <= a0v);
+  bool k1 = (d1 != 0.0f) & (u1 >= 0.0f) & (u1 <= a1v);
+  h0 = h1 = false;
+  if (!(k0 | k1)) return;
+  const f2 vn = mul2(fma2(dx, pk2(q.x, q.x), fma2(dy, pk2(q.y, q.y), mul2(dz, pk2(q.z, q.z)))), sg);
+  const f2 s = add2(un, vn);
+  float v0f, v1f, s0, s1;
+  up2(vn, v0f, v1f);
+  up2(s, s0, s1);
+  k0 &= (v0f >= 0.0f) & (s0 <= a0v);
+  k1 &= (v1f >= 0.0f) & (s1 <= a1v);
+  if (!(k0 | k1)) return;
+  const f2 tt = mul2(pk2(tq, tq), pk2(1.0f / d0, 1.0f / d1));
+  up2(tt, t0, t1);
+  h0 = k0 & (t0 > Bq.z) & (t0 < Dq.z);
+  h1 = k1 & (t1 > Bq.w) & (t1 < Dq.w);
+}
 }  // namespace crsh
