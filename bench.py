@@ -61,6 +61,12 @@ class ClockSampler:
                 text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # the timed region starts once the sampler is live (nvidia-smi takes
+            # ~0.5 s to start); samples from before it are dropped
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 5.0 and self.proc.poll() is None:
+                time.sleep(0.02)
+            self.lines.clear()
         except (OSError, FileNotFoundError):
             self.proc = None
         return self
@@ -70,6 +76,14 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def __exit__(self, *a):
+        if self.proc and not self.lines:   # a region shorter than the 100 ms period: one reading right after it
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index),
+                                      "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=10)
+                self.lines.extend(ln.strip() for ln in out.stdout.splitlines() if ln.strip())
+            except (OSError, subprocess.TimeoutExpired):
+                pass
         if self.proc:
             self.proc.terminate()
             try:
