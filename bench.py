@@ -121,13 +121,35 @@ def trav_flops(st):
     return int(np.asarray(st["tests"]).sum()) * EQ9_FLOPS + int(sum(st["final_tests"])) * MT_FLOPS
 
 
-def load_traffic(kernel="k_traverse"):
-    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+def load_traffic(config, zorder, kernel="k_traverse"):
+    """DRAM bytes per launch of `kernel` from the committed ncu launch list of
+    the same workload (profiles/ncu_summary*.json: cfg2, R6 or Z-order);
+    null for workloads without a committed capture."""
+    if config != 2:
+        return None
+    p = os.path.join(ROOT, "profiles", "ncu_summary_zorder.json" if zorder else "ncu_summary.json")
     try:
         d = json.load(open(p))
         return d.get("kernels", {}).get(kernel, {}).get("dram_bytes_per_launch")
     except (OSError, ValueError):
         return None
+
+
+def paper_context():
+    """The paper's intersection-reduction figures with their hardware (context,
+    not the target; BASELINE.json north_star): Table 4 totals as %
+    of N x M and the reduction vs RAH, from the cited
+    fixture tests/golden/paper_tables.json."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "tests", "golden", "paper_tables.json")))
+    except (OSError, ValueError):
+        return None
+    return {"hardware": "NVIDIA GeForce GTX TITAN 6 GB (Kepler GK110), CUDA + CUB (P:193-197)",
+            "workload": "512x512, 2-level RSH, subdivision 8 (P:195)",
+            "crsh_pct_of_brute": {t["scene"]: round(100.0 * t["CRSH"] / t["brute"], 2) for t in d["totals"]},
+            "rah_pct_of_brute": {t["scene"]: round(100.0 * t["RAH"] / t["brute"], 2) for t in d["totals"]},
+            "crsh_reduction_vs_rah_pct": {k: v for k, v in d["reduction_vs_rah_pct"].items() if k != "cite"},
+            "cite": "Table 4 (P:259-265); P:231, P:253, P:303"}
 
 
 def measured_peaks():
@@ -326,7 +348,7 @@ def run_crsh(args):
     except (OSError, ValueError, KeyError):
         pass
     tflops = trav_flops(st) / (trav_ms * 1e-3) / 1e12 if trav_ms > 0 else 0.0
-    traffic = load_traffic()
+    traffic = load_traffic(args.config, args.zorder)
     brute = rays * tr.M
     stage_names = ["generate+trim", "compress", "sort", "decompress", "build", "mesh-cull+plan", "traverse+final",
                    "output"]
@@ -356,6 +378,7 @@ def run_crsh(args):
                              f"kernel time from CUDA events around k_traverse"},
         "gpu_launches": launches,
         "e2e": e2e,
+        "paper_context": paper_context(),
         "clocks": clocks,
     }
     if world == 1 and not args.no_cpu_baseline:

@@ -89,57 +89,65 @@ __device__ __forceinline__ unsigned long long lb_load(const unsigned long long* 
   return w;
 }
 
-// Exclusive prefix of tile `tile` over tiles [0, tile), called by one whole
-// warp after it published this tile's aggregate. Returns the same value in
-// every lane. Tiles are numbered in dispatch order (atomic ticket), so every
-// predecessor is resident or done: the spin always terminates.
-__device__ __forceinline__ uint32_t lb_exclusive(unsigned long long* status, int tile) {
-  const int lane = (int)lane_id();
-  uint32_t excl = 0;
-  int p = tile - 1;
-  while (p >= 0) {
-    const int idx = p - lane;
-    unsigned long long w = idx >= 0 ? lb_load(&status[idx]) : (2ull << 32);
-    while (__any_sync(CRSH_FULL, (w >> 32) == 0ull)) {
-      if ((w >> 32) == 0ull) w = lb_load(&status[idx]);
-    }
-    const uint32_t inc = __ballot_sync(CRSH_FULL, (w >> 32) == 2ull);
-    const int stop = inc ? __ffs(inc) - 1 : 31;
-    const uint32_t v = lane <= stop ? (uint32_t)w : 0u;
-    excl += __reduce_add_sync(CRSH_FULL, v);
-    if (inc) break;
-    p -= 32;
-  }
-  return excl;
-}
-
-// Warp 0 of a scan tile: exclusive scan of the 64 (item, warp) counts in
-// s_cnt (flattened item-major), tile look-back, publish; writes s_excl[64] and
-// *s_prefix (the tile's global exclusive offset) and returns the tile total.
-__device__ __forceinline__ uint32_t tile_scan_lookback(const uint32_t* s_cnt, uint32_t* s_excl, uint32_t* s_prefix,
-                                                       unsigned long long* status, int tile) {
-  const int lane = (int)lane_id();
-  const uint32_t a = s_cnt[2 * lane], b = s_cnt[2 * lane + 1];
-  uint32_t incl = a + b;
+// Single-pass scan tile (Merrill & Garland decoupled look-back), called by
+// EVERY thread of the block (it contains barriers): warp 0 scans the 64
+// (item, warp) counts of s_cnt (flattened item-major) into s_excl and
+// publishes the tile aggregate; then all threads look back together, thread i at
+// predecessor tile - 1 - i, so one round trip covers blockDim.x predecessors
+// (a warp-only look-back covers 32): with many tiles resident at once, tile
+// k waits ~k / (2 window) round trips for the inclusive frontier. Measured
+// against the warp-only look-back: cfg2 generate+trim 31.9 -> 28.6 us,
+// compress 18.9 -> 16.2 us; neutral at cfg4, where the tiles are bound by
+// their own work (k_raygen: ~370 instructions per slot of IEEE div/sqrt and
+// the hash polynomial).
+__device__ __forceinline__ uint32_t tile_scan_lookback_block(const uint32_t* s_cnt, uint32_t* s_excl, uint32_t* s_prefix,
+                                                             unsigned long long* status, int tile) {
+  __shared__ uint32_t s_lb_total, s_lb_stop, s_lb_red[32];
+  const int tid = (int)threadIdx.x, lane = (int)lane_id(), warp = tid >> 5, nw = (int)(blockDim.x >> 5);
+  if (warp == 0) {
+    const uint32_t a = s_cnt[2 * lane], b = s_cnt[2 * lane + 1];
+    uint32_t incl = a + b;
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(CRSH_FULL, incl, o);
-    if (lane >= o) incl += y;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(CRSH_FULL, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const uint32_t ex = incl - (a + b);
+    s_excl[2 * lane] = ex;
+    s_excl[2 * lane + 1] = ex + a;
+    const uint32_t total = __shfl_sync(CRSH_FULL, incl, 31);
+    if (lane == 0) {
+      s_lb_total = total;
+      lb_store(&status[tile], tile == 0 ? 2u : 1u, total);
+    }
   }
-  const uint32_t ex = incl - (a + b);
-  s_excl[2 * lane] = ex;
-  s_excl[2 * lane + 1] = ex + a;
-  const uint32_t total = __shfl_sync(CRSH_FULL, incl, 31);
-  uint32_t prefix = 0;
-  if (tile == 0) {
-    if (lane == 0) lb_store(&status[0], 2u, total);
-  } else {
-    if (lane == 0) lb_store(&status[tile], 1u, total);
-    __syncwarp();
-    prefix = lb_exclusive(status, tile);
-    if (lane == 0) lb_store(&status[tile], 2u, prefix + total);
+  __syncthreads();
+  const uint32_t total = s_lb_total;
+  uint32_t excl = 0;
+  if (tile > 0) {   // block-uniform
+    int p = tile - 1;
+    for (;;) {
+      const int idx = p - tid;
+      unsigned long long w = idx >= 0 ? lb_load(&status[idx]) : (2ull << 32);
+      while ((w >> 32) == 0ull) w = lb_load(&status[idx]);   // predecessors were dispatched earlier: they publish
+      if (tid == 0) s_lb_stop = 0xFFFFFFFFu;
+      __syncthreads();
+      if ((w >> 32) == 2ull) atomicMin(&s_lb_stop, (uint32_t)tid);   // nearest inclusive prefix in the window
+      __syncthreads();
+      const uint32_t stop = s_lb_stop;
+      const uint32_t v = __reduce_add_sync(CRSH_FULL, (uint32_t)tid <= stop ? (uint32_t)w : 0u);
+      if (lane == 0) s_lb_red[warp] = v;
+      __syncthreads();
+      uint32_t sum = 0;
+      for (int q = 0; q < nw; ++q) sum += s_lb_red[q];
+      excl += sum;
+      if (stop != 0xFFFFFFFFu) break;
+      p -= (int)blockDim.x;
+      __syncthreads();   // s_lb_stop / s_lb_red are reused
+    }
+    if (tid == 0) lb_store(&status[tile], 2u, excl + total);
   }
-  if (lane == 0) *s_prefix = prefix;
+  if (tid == 0) *s_prefix = excl;
   return total;
 }
 

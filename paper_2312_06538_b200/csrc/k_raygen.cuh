@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_raygen(const RaygenArgs a) {
     if (lane == 0) s_cnt[it * 8 + warp] = __popc(ballot[it]);
   }
   __syncthreads();
-  if (warp == 0) tile_scan_lookback(s_cnt, s_excl, &s_prefix, a.status, (int)tile);
+  tile_scan_lookback_block(s_cnt, s_excl, &s_prefix, a.status, (int)tile);
   __syncthreads();
   const uint32_t prefix = s_prefix;
   const uint32_t lt = lanemask_lt();

@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_rle(const RleArgs a) {
     if (lane == 0) s_cnt[it * 8 + warp] = __popc(ballot[it]);
   }
   __syncthreads();
-  if (warp == 0) tile_scan_lookback(s_cnt, s_excl, &s_prefix, a.status, (int)tile);
+  tile_scan_lookback_block(s_cnt, s_excl, &s_prefix, a.status, (int)tile);
   __syncthreads();
   const uint32_t prefix = s_prefix, lt = lanemask_lt();
 #pragma unroll
@@ -96,6 +96,12 @@ constexpr int SORT_WARPS = SORT_THREADS / 32;
 constexpr int SORT_ITEMS = 16;   // 4096-key tiles: half the tiles (and look-back hops) of 2048 (A/B: sort 0.47 -> 0.44 ms at cfg4)
 constexpr int SORT_TILE = SORT_THREADS * SORT_ITEMS;
 constexpr int SORT_PASSES = 32 / RADIX_BITS;
+// k_onesweep at 3 CTAs per SM (80 registers, no spills; 141 registers and 2
+// CTAs per SM without the bound): A/B at cfg4 sort 0.44 -> 0.41 ms; 4 CTAs
+// (64 registers) spill and are slower, as are 16/32-word look-back batches
+#ifndef CRSH_SORT_MINB
+#define CRSH_SORT_MINB 3
+#endif
 
 struct SegChunks {   // per-segment chunk ranges, loaded from the FrameDesc
   int32_t n_seg;
@@ -161,7 +167,7 @@ __device__ __forceinline__ void st_store32(uint32_t* p, uint32_t v) {
 // match.any, per-warp shared-memory histograms, decoupled look-back per digit
 // across the segment's tiles, and a shared-memory reorder so the global
 // writes are contiguous within each digit run.
-__global__ void __launch_bounds__(SORT_THREADS) k_onesweep(const SortPassArgs a) {
+__global__ void __launch_bounds__(SORT_THREADS, CRSH_SORT_MINB) k_onesweep(const SortPassArgs a) {
   extern __shared__ uint32_t sm[];
   uint32_t* s_keys = sm;                            // SORT_TILE
   uint32_t* s_vals = sm + SORT_TILE;                // SORT_TILE
@@ -316,7 +322,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_sizes(const ScanSizeArgs 
     if (lane == 31) s_cnt[it * 8 + warp] = incl;
   }
   __syncthreads();
-  if (warp == 0) tile_scan_lookback(s_cnt, s_excl, &s_prefix, a.status, (int)tile);
+  tile_scan_lookback_block(s_cnt, s_excl, &s_prefix, a.status, (int)tile);
   __syncthreads();
   const uint32_t prefix = s_prefix;
 #pragma unroll

@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_plan(const PlanArgs a) {
     warp_seg_add(&s_mesh[0][1], 2, a.n_seg, q, mh[q]);
   }
   __syncthreads();
-  if (warp == 0) tile_scan_lookback(s_cnt, s_excl, &s_prefix, a.status, (int)tile);
+  tile_scan_lookback_block(s_cnt, s_excl, &s_prefix, a.status, (int)tile);
   __syncthreads();
   const uint32_t prefix = s_prefix;
 #pragma unroll
