@@ -293,7 +293,18 @@ constexpr int TRAV_THREADS = CRSH_TRAV_THREADS;
 constexpr int TRAV_WARPS = TRAV_THREADS / 32;
 constexpr uint32_t SMALL_GROUP_RAYS = 512;   // groups up to this size live in shared memory
 constexpr int LOWQ = 64;                     // capacity of a warp queue below level Lv-1
-__device__ __forceinline__ uint32_t ray_swz(uint32_t pp) { return (pp >> 1) & 3u; }
+// The group's rays as paired records (rays 2i, 2i+1; mt2_ns) in four planes
+// of float4 (plane k = float4 #k of every record): record pp sits at index
+// ray_rix(pp) = pp + pp / 8 of each plane. The skew of one slot per 8 records
+// (two bundles of B0 = 8) puts the k-th load of 32 lanes at 8 different
+// bundles on 8 different 16-byte bank groups, and the bundle's records are
+// contiguous, so one base index per (bundle, triangle) entry addresses all
+// its loads with compile-time offsets (RAY_PLANE is fixed for the largest
+// shared-memory group). Replaces an XOR swizzle of 64-byte records (A/B:
+// cfg2 R6 83.5 -> 89.1 Mrays/s, Z-order 497 -> 520: the swizzle's per-load
+// address arithmetic and its remaining bank conflicts).
+__host__ __device__ __forceinline__ constexpr uint32_t ray_rix(uint32_t pp) { return pp + (pp >> 3); }
+constexpr uint32_t RAY_PLANE = ray_rix(SMALL_GROUP_RAYS / 2u) + 1u;   // float4 per ray plane (289)
 
 struct TravArgs {
   int32_t Lv, B0, B, K, logB0, logB;
@@ -349,7 +360,7 @@ struct TravSmem {
       uint32_t n4 = 0;   // float4 slots of the group's nodes below the top level
       for (int k = 1; k < Lv; ++k) { s.node_off[k] = n4; n4 += 3u * per_group[k]; }
       s.off_nodes = take(16u * (n4 ? n4 : 1u));
-      s.off_rays = take(32u * group_rays);
+      s.off_rays = take(64u * RAY_PLANE);
       s.off_best = take(8u * group_rays);
       // level Lv-1 nodes as paired records for the packed child tests (cull2_ns)
       s.off_pairs = take(Lv >= 2 ? 80u * (per_group[Lv - 1] / 2u) : 16u);
@@ -439,21 +450,18 @@ __global__ void __launch_bounds__(TRAV_THREADS, CRSH_TRAV_MINB) k_traverse(const
           const float4* src = s_trav[k] + (size_t)g * n4;
           for (uint32_t j = tid; j < n4; j += TRAV_THREADS) sn[s_noff[k] + j] = __ldg(src + j);
         }
-        // the group's rays as paired records (rays 2i, 2i+1) for mt2_ns; the
-        // four float4 of record pp sit in slots k ^ ray_swz(pp), so that the
-        // k-th load of 32 lanes at random records spreads over all eight
-        // 16-byte bank groups of a 128-byte line (unswizzled, 64-byte records
-        // put every lane on 2 of the 8 and each LDS.128 replays 16 times)
+        // the group's rays as paired records (rays 2i, 2i+1) for mt2_ns, in
+        // ray planes (ray_rix above)
         float4* sr = reinterpret_cast<float4*>(smraw + L.off_rays);
         const float4* rs = a.sorted_rays + 2 * (size_t)g * a.group_rays;
         for (uint32_t pp = tid; pp < a.group_rays / 2u; pp += TRAV_THREADS) {
           const float4 a0 = __ldg(rs + 4 * pp), a1 = __ldg(rs + 4 * pp + 1), b0 = __ldg(rs + 4 * pp + 2),
                        b1 = __ldg(rs + 4 * pp + 3);
-          const uint32_t sw = ray_swz(pp);
-          sr[4 * pp + (0u ^ sw)] = make_float4(a0.x, b0.x, a0.y, b0.y);
-          sr[4 * pp + (1u ^ sw)] = make_float4(a0.z, b0.z, a0.w, b0.w);
-          sr[4 * pp + (2u ^ sw)] = make_float4(a1.x, b1.x, a1.y, b1.y);
-          sr[4 * pp + (3u ^ sw)] = make_float4(a1.z, b1.z, a1.w, b1.w);
+          float4* rp = sr + ray_rix(pp);
+          rp[0] = make_float4(a0.x, b0.x, a0.y, b0.y);
+          rp[RAY_PLANE] = make_float4(a0.z, b0.z, a0.w, b0.w);
+          rp[2 * RAY_PLANE] = make_float4(a1.x, b1.x, a1.y, b1.y);
+          rp[3 * RAY_PLANE] = make_float4(a1.z, b1.z, a1.w, b1.w);
         }
       }
       if (tid == 0) { s_carry = 0u; s_carry_c = 0u; }
@@ -546,6 +554,14 @@ __global__ void __launch_bounds__(TRAV_THREADS, CRSH_TRAV_MINB) k_traverse(const
         const float4 tv0 = __ldg(te), te1 = __ldg(te + 1), te2 = __ldg(te + 2);
         const f3 v0 = mk3(tv0.x, tv0.y, tv0.z), e1 = mk3(te1.x, te1.y, te1.z), e2 = mk3(te2.x, te2.y, te2.z);
         const uint32_t rl0 = e.x << logB0;   // first ray of the bundle (B0 even)
+        // ray-plane base of the bundle: its records are ray_rix(rl0/2) + i
+        // while they stay inside one block of 8 (compile-time B0 <= 16)
+        constexpr bool RB_CONST = B0T >= 2 && B0T <= 16;
+        const float4* rb = s_rays + ray_rix(rl0 >> 1);
+        auto ray_rec = [&](uint32_t rl, int r, int k) -> float4 {
+          if (RB_CONST) return rb[(uint32_t)k * RAY_PLANE + (uint32_t)(r >> 1)];
+          return s_rays[(uint32_t)k * RAY_PLANE + ray_rix(rl >> 1)];
+        };
         const uint32_t nr = min((uint32_t)B0, g_real - rl0);   // real rays of the bundle (>= 1: the bundle exists)
         // the bundle's leaf record: {c, d}, {a, tan}, {sec, shared-origin flag} (k_leaves)
         const float4* lf = Lv == 1 ? s_top + 3 * e.x
@@ -561,9 +577,7 @@ __global__ void __launch_bounds__(TRAV_THREADS, CRSH_TRAV_MINB) k_traverse(const
             if (!B0T && r >= B0) break;
             if ((uint32_t)r >= nr) break;
             const uint32_t rl = rl0 + (uint32_t)r;
-            const float4* rp = s_rays + 2 * rl;
-            const uint32_t sw = ray_swz(rl >> 1);
-            const float4 Bq = rp[1u ^ sw], Cq = rp[2u ^ sw], Dq = rp[3u ^ sw];
+            const float4 Bq = ray_rec(rl, r, 1), Cq = ray_rec(rl, r, 2), Dq = ray_rec(rl, r, 3);
             const bool real1 = (uint32_t)r + 1u < nr;
             c_mt_t += 1u + (uint32_t)real1;
             bool h0, h1;
@@ -584,9 +598,7 @@ __global__ void __launch_bounds__(TRAV_THREADS, CRSH_TRAV_MINB) k_traverse(const
           const uint32_t rl = rl0 + (uint32_t)r;
           float4 A, Bq, Cq, Dq;
           if (SMALL) {
-            const float4* rp = s_rays + 2 * rl;   // paired record of rays rl, rl+1 (swizzled slots)
-            const uint32_t sw = ray_swz(rl >> 1);
-            A = rp[0u ^ sw]; Bq = rp[1u ^ sw]; Cq = rp[2u ^ sw]; Dq = rp[3u ^ sw];
+            A = ray_rec(rl, r, 0); Bq = ray_rec(rl, r, 1); Cq = ray_rec(rl, r, 2); Dq = ray_rec(rl, r, 3);
           } else {
             const float4* rs = a.sorted_rays + 2 * (rbase + rl);
             const float4 a0 = __ldg(rs), a1 = __ldg(rs + 1), b0 = __ldg(rs + 2), b1 = __ldg(rs + 3);
