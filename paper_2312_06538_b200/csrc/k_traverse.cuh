@@ -370,8 +370,10 @@ struct TravSmem {
   }
 };
 
-// BT / B0T: compile-time branching factor / bundle size (0 = runtime a.B / a.B0)
-template <bool SMALL, int BT, int B0T>
+// BT / B0T / LVT: compile-time branching factor / bundle size / levels (0 =
+// runtime a.B / a.B0 / a.Lv); with LVT the length of the bundle-level queue
+// Q[1] lives in a (warp-uniform) register instead of shared memory
+template <bool SMALL, int BT, int B0T, int LVT>
 #ifndef CRSH_TRAV_MINB
 #define CRSH_TRAV_MINB 3
 #endif
@@ -402,7 +404,7 @@ __global__ void __launch_bounds__(TRAV_THREADS, CRSH_TRAV_MINB) k_traverse(const
     s_trav[threadIdx.x] = a.trav[threadIdx.x];
   }
 
-  const int Lv = a.Lv, K = a.K, logB0 = a.logB0;
+  const int Lv = LVT ? LVT : a.Lv, K = a.K, logB0 = a.logB0;
   const int B = BT ? BT : a.B;
   const int logB = BT ? __builtin_ctz(BT) : a.logB;
   const uint32_t Bm = (uint32_t)B - 1u;
@@ -410,6 +412,13 @@ __global__ void __launch_bounds__(TRAV_THREADS, CRSH_TRAV_MINB) k_traverse(const
   const uint32_t lt = lanemask_lt();
   uint2* q = reinterpret_cast<uint2*>(smraw + L.off_q) + warp * L.q_warp;
   uint32_t* qlen = s_qlen[warp];
+  constexpr bool QREG = LVT != 0;
+  uint32_t q1n = 0;   // QREG: length of Q[1]
+  auto qget = [&](int k) -> uint32_t { return (QREG && k == 1) ? q1n : qlen[k]; };
+  auto qset = [&](int k, uint32_t v) {   // all 32 lanes, between __syncwarp()s
+    if (QREG && k == 1) q1n = v;
+    else if (lane == 0) qlen[k] = v;
+  };
   const uint32_t step_exp = (32u >> logB) ? (32u >> logB) : 1u;   // entries per expansion step
   const uint32_t step_mt = 32u;                                   // entries per final-test step (one per lane)
   for (uint32_t i = tid; i < MAX_SEG * CTR_STRIDE; i += TRAV_THREADS) s_ctr[i] = 0ull;
@@ -546,7 +555,7 @@ __global__ void __launch_bounds__(TRAV_THREADS, CRSH_TRAV_MINB) k_traverse(const
     const uint2* q1base = q + s_qoff[1];
     const int B0 = B0T ? B0T : a.B0;
     auto step_mt_fn = [&]() {
-      const uint32_t qk = qlen[1];
+      const uint32_t qk = qget(1);
       const uint32_t n = min(qk, step_mt);
       if (lane < n) {
         const uint2 e = q1base[qk - n + lane];
@@ -563,6 +572,7 @@ __global__ void __launch_bounds__(TRAV_THREADS, CRSH_TRAV_MINB) k_traverse(const
           return s_rays[(uint32_t)k * RAY_PLANE + ray_rix(rl >> 1)];
         };
         const uint32_t nr = min((uint32_t)B0, g_real - rl0);   // real rays of the bundle (>= 1: the bundle exists)
+        c_mt_t += nr;   // every real ray of the bundle is tested against the triangle
         // the bundle's leaf record: {c, d}, {a, tan}, {sec, shared-origin flag} (k_leaves)
         const float4* lf = Lv == 1 ? s_top + 3 * e.x
                                    : (SMALL ? s_nodes + s_noff[1] + 3 * e.x : s_trav[1] + 3 * ((size_t)g * s_pg[1] + e.x));
@@ -579,7 +589,6 @@ __global__ void __launch_bounds__(TRAV_THREADS, CRSH_TRAV_MINB) k_traverse(const
             const uint32_t rl = rl0 + (uint32_t)r;
             const float4 Bq = ray_rec(rl, r, 1), Cq = ray_rec(rl, r, 2), Dq = ray_rec(rl, r, 3);
             const bool real1 = (uint32_t)r + 1u < nr;
-            c_mt_t += 1u + (uint32_t)real1;
             bool h0, h1;
             float t0, t1;
             mt2o_ns(Bq, Cq, Dq, e1, e2, tv, qv, tq, h0, t0, h1, t1);
@@ -606,7 +615,6 @@ __global__ void __launch_bounds__(TRAV_THREADS, CRSH_TRAV_MINB) k_traverse(const
             Cq = make_float4(a1.x, b1.x, a1.y, b1.y); Dq = make_float4(a1.z, b1.z, a1.w, b1.w);
           }
           const bool real1 = (uint32_t)r + 1u < nr;   // padding rays come last
-          c_mt_t += 1u + (uint32_t)real1;
           bool h0, h1;
           float t0, t1;
           mt2_ns(A, Bq, Cq, Dq, v0, e1, e2, h0, t0, h1, t1);
@@ -625,12 +633,12 @@ __global__ void __launch_bounds__(TRAV_THREADS, CRSH_TRAV_MINB) k_traverse(const
         }
       }
       __syncwarp();
-      if (lane == 0) qlen[1] = qk - n;
+      qset(1, qk - n);
       __syncwarp();
     };
     // expansion step at level k >= 2 (only when Lv >= 3 reaches below Lv-1)
     auto step_exp_fn = [&](int k) {
-      const uint32_t qk = qlen[k];
+      const uint32_t qk = qget(k);
       const uint32_t n = min(qk, step_exp);
       const uint2* qin = q + s_qoff[k] + (qk - n);
       const uint32_t e_i = lane >> logB;
@@ -652,12 +660,12 @@ __global__ void __launch_bounds__(TRAV_THREADS, CRSH_TRAV_MINB) k_traverse(const
       }
       const uint32_t bt = __ballot_sync(CRSH_FULL, test);
       const uint32_t b = __ballot_sync(CRSH_FULL, pass);
-      const uint32_t q1 = qlen[k - 1];
+      const uint32_t q1 = qget(k - 1);
       if (pass) q[s_qoff[k - 1] + q1 + __popc(b & lt)] = out;
       __syncwarp();
+      qset(k - 1, q1 + __popc(b));
+      qset(k, qk - n);
       if (lane == 0) {
-        qlen[k - 1] = q1 + __popc(b);
-        qlen[k] = qk - n;
         atomicAdd(&ctr[CTR_TESTS + (k - 1)], (unsigned long long)__popc(bt));
         atomicAdd(&ctr[CTR_HITS + (k - 1)], (unsigned long long)__popc(b));
       }
@@ -667,14 +675,14 @@ __global__ void __launch_bounds__(TRAV_THREADS, CRSH_TRAV_MINB) k_traverse(const
     // with partial steps
     auto drain = [&](bool all) {
       for (;;) {
-        if (qlen[1] >= step_mt) { step_mt_fn(); continue; }
+        if (qget(1) >= step_mt) { step_mt_fn(); continue; }
         int pick = 0;
         for (int k = 2; k < Lv - (Lv >= 2 ? 0 : 0); ++k)   // levels 2 .. Lv-1 (Lv >= 3 only)
-          if (qlen[k] >= step_exp) { pick = k; break; }
+          if (qget(k) >= step_exp) { pick = k; break; }
         if (!pick && all) {
-          if (qlen[1]) { step_mt_fn(); continue; }
+          if (qget(1)) { step_mt_fn(); continue; }
           for (int k = 2; k < Lv; ++k)
-            if (qlen[k]) { pick = k; break; }
+            if (qget(k)) { pick = k; break; }
         }
         if (!pick) return;
         step_exp_fn(pick);
@@ -707,20 +715,20 @@ __global__ void __launch_bounds__(TRAV_THREADS, CRSH_TRAV_MINB) k_traverse(const
         cull2_ns(s_tpairs + 5 * (j >> 1), Px, Py, Pz, Pr, p0, p1);
         p0 &= n0;
         p1 &= n1;
-        c_top_t += (uint32_t)n0 + (uint32_t)n1;
-        c_top_h += (uint32_t)p0 + (uint32_t)p1;
         pm |= ((uint32_t)p0 << j) | ((uint32_t)p1 << (j + 1));
       }
+      c_top_t += __popc(nm);   // every (node, triangle) with a surviving mesh was tested (skipped pairs have none)
+      c_top_h += __popc(pm);
       // then each top node that passed for some lane
       for (uint32_t jm = __reduce_or_sync(CRSH_FULL, pm); jm; jm &= jm - 1) {
         const int j = __ffs(jm) - 1;
         const bool pass = (pm >> j) & 1u;
         const uint32_t b = __ballot_sync(CRSH_FULL, pass);
         if (Lv == 1) {   // the top level is the bundle level: queue for the final tests
-          const uint32_t ql = qlen[1];
+          const uint32_t ql = qget(1);
           if (pass) q[s_qoff[1] + ql + __popc(b & lt)] = make_uint2((uint32_t)j, tri);
           __syncwarp();
-          if (lane == 0) qlen[1] = ql + __popc(b);
+          qset(1, ql + __popc(b));
           __syncwarp();
           drain(false);   // keeps the queue below one top node's passes plus a partial step
           continue;
@@ -760,7 +768,7 @@ __global__ void __launch_bounds__(TRAV_THREADS, CRSH_TRAV_MINB) k_traverse(const
           if ((int)lane >= o) incl += y;
         }
         const uint32_t tot = __shfl_sync(CRSH_FULL, incl, 31);
-        const uint32_t ql0 = qlen[k1];
+        const uint32_t ql0 = qget(k1);
         uint2* qd = q + s_qoff[k1] + ql0 + (incl - cnt);
         while (m) {
           const uint32_t c = __ffs(m) - 1;
@@ -768,7 +776,7 @@ __global__ void __launch_bounds__(TRAV_THREADS, CRSH_TRAV_MINB) k_traverse(const
           *qd++ = make_uint2(cbase | c, tri);
         }
         __syncwarp();
-        if (lane == 0) qlen[k1] = ql0 + tot;
+        qset(k1, ql0 + tot);
         __syncwarp();
         drain(false);
       }
