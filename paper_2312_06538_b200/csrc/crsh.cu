@@ -540,7 +540,7 @@ crsh_status enqueue_frame(crsh_scene* sc, const FrameInfo& fi, const crsh_primar
         kern<<<per_sm * sc->sm_count, TRAV_THREADS, L.total, st>>>(t, L);
         return cudaGetLastError();
       };
-      if (B == 8 && B0 == 8 && Lv == 2) CK(small ? launch(k_traverse<true, 8, 8, 2>) : launch(k_traverse<false, 8, 8, 2>));
+      if (B == 8 && B0 == 8 && Lv == 2 && fi.K == 8) CK(small ? launch(k_traverse<true, 8, 8, 2>) : launch(k_traverse<false, 8, 8, 2>));
       else if (B == 8 && B0 == 8) CK(small ? launch(k_traverse<true, 8, 8, 0>) : launch(k_traverse<false, 8, 8, 0>));
       else CK(small ? launch(k_traverse<true, 0, 0, 0>) : launch(k_traverse<false, 0, 0, 0>));
       ++nl;

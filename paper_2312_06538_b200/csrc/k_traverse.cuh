@@ -404,7 +404,10 @@ __global__ void __launch_bounds__(TRAV_THREADS, CRSH_TRAV_MINB) k_traverse(const
     s_trav[threadIdx.x] = a.trav[threadIdx.x];
   }
 
-  const int Lv = LVT ? LVT : a.Lv, K = a.K, logB0 = a.logB0;
+  // K (top nodes per group, host: min(32, 512 / span)) is compile-time when the shape is
+  constexpr int SPAN_T = (LVT && BT && B0T) ? B0T * (LVT >= 2 ? BT : 1) * (LVT >= 3 ? BT : 1) : 0;
+  constexpr int KT = (LVT && LVT <= 3 && SPAN_T) ? (SPAN_T >= 512 ? 1 : (512 / SPAN_T < 32 ? 512 / SPAN_T : 32)) : 0;
+  const int Lv = LVT ? LVT : a.Lv, K = KT ? KT : a.K, logB0 = a.logB0;
   const int B = BT ? BT : a.B;
   const int logB = BT ? __builtin_ctz(BT) : a.logB;
   const uint32_t Bm = (uint32_t)B - 1u;
@@ -573,6 +576,9 @@ __global__ void __launch_bounds__(TRAV_THREADS, CRSH_TRAV_MINB) k_traverse(const
         };
         const uint32_t nr = min((uint32_t)B0, g_real - rl0);   // real rays of the bundle (>= 1: the bundle exists)
         c_mt_t += nr;   // every real ray of the bundle is tested against the triangle
+        // a padding ray (odd nr: the partner of the last real ray) has
+        // tmin = tmax = -1 (k_leaves), so no t passes tmin < t < tmax: it
+        // never hits and needs no mask
         // the bundle's leaf record: {c, d}, {a, tan}, {sec, shared-origin flag} (k_leaves)
         const float4* lf = Lv == 1 ? s_top + 3 * e.x
                                    : (SMALL ? s_nodes + s_noff[1] + 3 * e.x : s_trav[1] + 3 * ((size_t)g * s_pg[1] + e.x));
@@ -588,11 +594,9 @@ __global__ void __launch_bounds__(TRAV_THREADS, CRSH_TRAV_MINB) k_traverse(const
             if ((uint32_t)r >= nr) break;
             const uint32_t rl = rl0 + (uint32_t)r;
             const float4 Bq = ray_rec(rl, r, 1), Cq = ray_rec(rl, r, 2), Dq = ray_rec(rl, r, 3);
-            const bool real1 = (uint32_t)r + 1u < nr;
             bool h0, h1;
             float t0, t1;
             mt2o_ns(Bq, Cq, Dq, e1, e2, tv, qv, tq, h0, t0, h1, t1);
-            h1 &= real1;
             if (h0 | h1) {
               c_mt_h += (uint32_t)h0 + (uint32_t)h1;
               if (h0) atomicMin(s_best + rl, pack_hit(t0, e.y));
@@ -614,11 +618,9 @@ __global__ void __launch_bounds__(TRAV_THREADS, CRSH_TRAV_MINB) k_traverse(const
             A = make_float4(a0.x, b0.x, a0.y, b0.y); Bq = make_float4(a0.z, b0.z, a0.w, b0.w);
             Cq = make_float4(a1.x, b1.x, a1.y, b1.y); Dq = make_float4(a1.z, b1.z, a1.w, b1.w);
           }
-          const bool real1 = (uint32_t)r + 1u < nr;   // padding rays come last
           bool h0, h1;
           float t0, t1;
           mt2_ns(A, Bq, Cq, Dq, v0, e1, e2, h0, t0, h1, t1);
-          h1 &= real1;
           if (h0 | h1) {
             c_mt_h += (uint32_t)h0 + (uint32_t)h1;
             if (h0) {
@@ -634,7 +636,7 @@ __global__ void __launch_bounds__(TRAV_THREADS, CRSH_TRAV_MINB) k_traverse(const
       }
       __syncwarp();
       qset(1, qk - n);
-      __syncwarp();
+      if (!QREG) __syncwarp();
     };
     // expansion step at level k >= 2 (only when Lv >= 3 reaches below Lv-1)
     auto step_exp_fn = [&](int k) {
@@ -708,6 +710,7 @@ __global__ void __launch_bounds__(TRAV_THREADS, CRSH_TRAV_MINB) k_traverse(const
       // records); a lane tests node j only if its triangle's mesh survived
       // j's mesh cull. pm = the lane's passing top nodes.
       uint32_t pm = 0;
+#pragma unroll
       for (int j = 0; j < K; j += 2) {
         const bool n0 = (nm >> j) & 1u, n1 = (nm >> (j + 1)) & 1u;
         if (__ballot_sync(CRSH_FULL, n0 | n1) == 0u) continue;   // no lane's mesh kept node j or j+1
@@ -729,7 +732,7 @@ __global__ void __launch_bounds__(TRAV_THREADS, CRSH_TRAV_MINB) k_traverse(const
           if (pass) q[s_qoff[1] + ql + __popc(b & lt)] = make_uint2((uint32_t)j, tri);
           __syncwarp();
           qset(1, ql + __popc(b));
-          __syncwarp();
+          if (!QREG) __syncwarp();
           drain(false);   // keeps the queue below one top node's passes plus a partial step
           continue;
         }
@@ -777,7 +780,7 @@ __global__ void __launch_bounds__(TRAV_THREADS, CRSH_TRAV_MINB) k_traverse(const
         }
         __syncwarp();
         qset(k1, ql0 + tot);
-        __syncwarp();
+        if (!QREG || k1 != 1) __syncwarp();
         drain(false);
       }
     }
