@@ -594,13 +594,12 @@ __global__ void __launch_bounds__(TRAV_THREADS, CRSH_TRAV_MINB) k_traverse(const
             if ((uint32_t)r >= nr) break;
             const uint32_t rl = rl0 + (uint32_t)r;
             const float4 Bq = ray_rec(rl, r, 1), Cq = ray_rec(rl, r, 2), Dq = ray_rec(rl, r, 3);
-            bool h0, h1;
             float t0, t1;
-            mt2o_ns(Bq, Cq, Dq, e1, e2, tv, qv, tq, h0, t0, h1, t1);
-            if (h0 | h1) {
-              c_mt_h += (uint32_t)h0 + (uint32_t)h1;
-              if (h0) atomicMin(s_best + rl, pack_hit(t0, e.y));
-              if (h1) atomicMin(s_best + rl + 1, pack_hit(t1, e.y));
+            const uint32_t hm = mt2o_ns(Bq, Cq, Dq, e1, e2, tv, qv, tq, t0, t1);   // bit i: ray rl+i hit
+            if (hm) {
+              c_mt_h += __popc(hm);
+              if (hm & 1u) atomicMin(s_best + rl, pack_hit(t0, e.y));
+              if (hm & 2u) atomicMin(s_best + rl + 1, pack_hit(t1, e.y));
             }
           }
         } else
@@ -618,16 +617,15 @@ __global__ void __launch_bounds__(TRAV_THREADS, CRSH_TRAV_MINB) k_traverse(const
             A = make_float4(a0.x, b0.x, a0.y, b0.y); Bq = make_float4(a0.z, b0.z, a0.w, b0.w);
             Cq = make_float4(a1.x, b1.x, a1.y, b1.y); Dq = make_float4(a1.z, b1.z, a1.w, b1.w);
           }
-          bool h0, h1;
           float t0, t1;
-          mt2_ns(A, Bq, Cq, Dq, v0, e1, e2, h0, t0, h1, t1);
-          if (h0 | h1) {
-            c_mt_h += (uint32_t)h0 + (uint32_t)h1;
-            if (h0) {
+          const uint32_t hm = mt2_ns(A, Bq, Cq, Dq, v0, e1, e2, t0, t1);   // bit i: ray rl+i hit
+          if (hm) {
+            c_mt_h += __popc(hm);
+            if (hm & 1u) {
               const unsigned long long pk = pack_hit(t0, e.y);
               if (SMALL) atomicMin(s_best + rl, pk); else atomicMin(a.best + rbase + rl, pk);
             }
-            if (h1) {
+            if (hm & 2u) {
               const unsigned long long pk = pack_hit(t1, e.y);
               if (SMALL) atomicMin(s_best + rl + 1, pk); else atomicMin(a.best + rbase + rl + 1, pk);
             }

@@ -289,12 +289,15 @@ namespace crsh {
 // as a paired record {ox0,ox1,oy0,oy1} {oz0,oz1,tmin0,tmin1}
 // {dx0,dx1,dy0,dy1} {dz0,dz1,tmax0,tmax1} against one triangle; the
 // triangle's scalars enter the packed instructions as broadcast operands.
+// Returns a hit mask (bit i: ray i hits in (tmin, tmax)) with t0 / t1; a
+// mask rather than two bools keeps the hit test in predicates and one
+// register (bools set on several return paths were materialised as bytes).
 // EARLY: leave as soon as both rays failed a barycentric test (a warp of 32
 // lanes almost never takes that exit together, so the branch-free form, which
 // lets independent ray pairs interleave, is the default in the traversal).
 template <bool EARLY = true>
-__device__ __forceinline__ void mt2_ns(float4 A, float4 Bq, float4 Cq, float4 Dq, f3 v0, f3 e1, f3 e2, bool& h0,
-                                       float& t0, bool& h1, float& t1) {
+__device__ __forceinline__ uint32_t mt2_ns(float4 A, float4 Bq, float4 Cq, float4 Dq, f3 v0, f3 e1, f3 e2, float& t0,
+                                           float& t1) {
   const f2 ox = pk2(A.x, A.y), oy = pk2(A.z, A.w), oz = pk2(Bq.x, Bq.y);
   const f2 dx = pk2(Cq.x, Cq.y), dy = pk2(Cq.z, Cq.w), dz = pk2(Dq.x, Dq.y);
   const f2 px = fma2(dy, pk2(e2.z, e2.z), mul2(dz, pk2(-e2.y, -e2.y)));
@@ -312,8 +315,7 @@ __device__ __forceinline__ void mt2_ns(float4 A, float4 Bq, float4 Cq, float4 Dq
   up2(adet, a0v, a1v);
   bool k0 = (d0 != 0.0f) & (u0 >= 0.0f) & (u0 <= a0v);
   bool k1 = (d1 != 0.0f) & (u1 >= 0.0f) & (u1 <= a1v);
-  h0 = h1 = false;
-  if (EARLY && !(k0 | k1)) return;
+  if (EARLY && !(k0 | k1)) return 0u;
   const f2 qx = fma2(ty, pk2(e1.z, e1.z), mul2(tz, pk2(-e1.y, -e1.y)));
   const f2 qy = fma2(tz, pk2(e1.x, e1.x), mul2(tx, pk2(-e1.z, -e1.z)));
   const f2 qz = fma2(tx, pk2(e1.y, e1.y), mul2(ty, pk2(-e1.x, -e1.x)));
@@ -324,12 +326,11 @@ __device__ __forceinline__ void mt2_ns(float4 A, float4 Bq, float4 Cq, float4 Dq
   up2(s, s0, s1);
   k0 &= (v0f >= 0.0f) & (s0 <= a0v);
   k1 &= (v1f >= 0.0f) & (s1 <= a1v);
-  if (EARLY && !(k0 | k1)) return;
+  if (EARLY && !(k0 | k1)) return 0u;
   const f2 tt = mul2(fma2(pk2(e2.x, e2.x), qx, fma2(pk2(e2.y, e2.y), qy, mul2(pk2(e2.z, e2.z), qz))),
                      pk2(1.0f / d0, 1.0f / d1));
   up2(tt, t0, t1);
-  h0 = k0 & (t0 > Bq.z) & (t0 < Dq.z);
-  h1 = k1 & (t1 > Bq.w) & (t1 < Dq.w);
+  return ((k0 & (t0 > Bq.z) & (t0 < Dq.z)) ? 1u : 0u) | ((k1 & (t1 > Bq.w) & (t1 < Dq.w)) ? 2u : 0u);
 }
 
 // mt2_ns for two rays that share their origin o (bit for bit): tv = o - v0,
@@ -337,8 +338,8 @@ __device__ __forceinline__ void mt2_ns(float4 A, float4 Bq, float4 Cq, float4 Dq
 // bundle -- exactly the values mt2_ns computes per ray, so the decisions and
 // t are bit-identical. Ray record halves: Bq = {-, -, tmin0, tmin1},
 // Cq = {dx0, dx1, dy0, dy1}, Dq = {dz0, dz1, tmax0, tmax1}.
-__device__ __forceinline__ void mt2o_ns(float4 Bq, float4 Cq, float4 Dq, f3 e1, f3 e2, f3 tv, f3 q, float tq, bool& h0,
-                                        float& t0, bool& h1, float& t1) {
+__device__ __forceinline__ uint32_t mt2o_ns(float4 Bq, float4 Cq, float4 Dq, f3 e1, f3 e2, f3 tv, f3 q, float tq, float& t0,
+                                            float& t1) {
   const f2 dx = pk2(Cq.x, Cq.y), dy = pk2(Cq.z, Cq.w), dz = pk2(Dq.x, Dq.y);
   const f2 px = fma2(dy, pk2(e2.z, e2.z), mul2(dz, pk2(-e2.y, -e2.y)));
   const f2 py = fma2(dz, pk2(e2.x, e2.x), mul2(dx, pk2(-e2.z, -e2.z)));
@@ -354,8 +355,7 @@ __device__ __forceinline__ void mt2o_ns(float4 Bq, float4 Cq, float4 Dq, f3 e1, 
   up2(adet, a0v, a1v);
   bool k0 = (d0 != 0.0f) & (u0 >= 0.0f) & (u0 <= a0v);
   bool k1 = (d1 != 0.0f) & (u1 >= 0.0f) & (u1 <= a1v);
-  h0 = h1 = false;
-  if (!(k0 | k1)) return;
+  if (!(k0 | k1)) return 0u;
   const f2 vn = mul2(fma2(dx, pk2(q.x, q.x), fma2(dy, pk2(q.y, q.y), mul2(dz, pk2(q.z, q.z)))), sg);
   const f2 s = add2(un, vn);
   float v0f, v1f, s0, s1;
@@ -363,10 +363,9 @@ __device__ __forceinline__ void mt2o_ns(float4 Bq, float4 Cq, float4 Dq, f3 e1, 
   up2(s, s0, s1);
   k0 &= (v0f >= 0.0f) & (s0 <= a0v);
   k1 &= (v1f >= 0.0f) & (s1 <= a1v);
-  if (!(k0 | k1)) return;
+  if (!(k0 | k1)) return 0u;
   const f2 tt = mul2(pk2(tq, tq), pk2(1.0f / d0, 1.0f / d1));
   up2(tt, t0, t1);
-  h0 = k0 & (t0 > Bq.z) & (t0 < Dq.z);
-  h1 = k1 & (t1 > Bq.w) & (t1 < Dq.w);
+  return ((k0 & (t0 > Bq.z) & (t0 < Dq.z)) ? 1u : 0u) | ((k1 & (t1 > Bq.w) & (t1 < Dq.w)) ? 2u : 0u);
 }
 }  // namespace crsh
