@@ -293,6 +293,19 @@ constexpr int TRAV_THREADS = CRSH_TRAV_THREADS;
 constexpr int TRAV_WARPS = TRAV_THREADS / 32;
 constexpr uint32_t SMALL_GROUP_RAYS = 512;   // groups up to this size live in shared memory
 constexpr int LOWQ = 64;                     // capacity of a warp queue below level Lv-1
+// Consecutive work items per ticket: the items of a group are consecutive, so
+// a chunk shares the group setup (rays, nodes, mesh list into shared memory)
+// across its items; chunks cost load balance at the end of the kernel, so
+// the chunk grows with the items per CTA: min(ITEM_CHUNK_MAX, n_items /
+// (CTAs x ITEM_CHUNK_DIV)), at least 1 (A/B, fixed chunks of 1 / 2 / 4: cfg2
+// R6 103.4 / 100.7 / 93.6 Mrays/s, 46 items per CTA; cfg3 R6 53.2 / - / 55.6;
+// adaptive: cfg2 unchanged, cfg3 R6 53.2 -> 55.0, cfg3 Z-order 510 -> 550)
+#ifndef CRSH_ITEM_CHUNK_MAX
+#define CRSH_ITEM_CHUNK_MAX 4
+#endif
+#ifndef CRSH_ITEM_CHUNK_DIV
+#define CRSH_ITEM_CHUNK_DIV 64
+#endif
 // The group's rays as paired records (rays 2i, 2i+1; mt2_ns) in four planes
 // of float4 (plane k = float4 #k of every record): record pp sits at index
 // ray_rix(pp) = pp + pp / 8 of each plane. The skew of one slot per 8 records
@@ -432,11 +445,18 @@ __global__ void __launch_bounds__(TRAV_THREADS, CRSH_TRAV_MINB) k_traverse(const
   for (int q = 0; q <= a.n_seg; ++q) seg_group_start[q] = a.fd->seg_pad_base[q] / a.group_rays;
   for (int q = 0; q < a.n_seg; ++q) seg_real_end[q] = a.fd->seg_pad_base[q] + a.fd->seg_n[q];
 
+  const uint32_t chunk =
+      max(1u, min((uint32_t)CRSH_ITEM_CHUNK_MAX, n_items / (gridDim.x * (uint32_t)CRSH_ITEM_CHUNK_DIV)));
+  uint32_t ch_next = 0, ch_end = 0;   // CTA-uniform: the rest of the current ticket's chunk of items
   for (;;) {
     __syncthreads();
-    if (tid == 0) s_item = atomicAdd(a.ticket, 1u);
+    if (ch_next >= ch_end && tid == 0) s_item = atomicAdd(a.ticket, 1u) * chunk;
     __syncthreads();
-    const uint32_t it = s_item;
+    if (ch_next >= ch_end) {
+      ch_next = s_item;
+      ch_end = min(ch_next + chunk, n_items);
+    }
+    const uint32_t it = ch_next++;
     if (it >= n_items) break;
     const uint4 item = __ldg(a.items + it);
     const uint32_t g = item.x;
