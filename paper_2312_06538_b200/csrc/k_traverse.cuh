@@ -386,11 +386,18 @@ struct TravSmem {
 // BT / B0T / LVT: compile-time branching factor / bundle size / levels (0 =
 // runtime a.B / a.B0 / a.Lv); with LVT the length of the bundle-level queue
 // Q[1] lives in a (warp-uniform) register instead of shared memory
-template <bool SMALL, int BT, int B0T, int LVT>
+// Occupancy: the compile-time Lv = 2 shape runs 4 CTAs (32 warps) per SM at
+// 64 registers (A/B: +3.4 % at cfg2, +3.8 % at cfg3 over 3 CTAs at 80
+// registers, despite ~100 bytes of spills); the runtime shapes keep 3.
 #ifndef CRSH_TRAV_MINB
 #define CRSH_TRAV_MINB 3
 #endif
-__global__ void __launch_bounds__(TRAV_THREADS, CRSH_TRAV_MINB) k_traverse(const TravArgs a, const TravSmem L) {
+#ifndef CRSH_TRAV_MINB_LV2
+#define CRSH_TRAV_MINB_LV2 4
+#endif
+template <bool SMALL, int BT, int B0T, int LVT>
+__global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : CRSH_TRAV_MINB)
+    k_traverse(const TravArgs a, const TravSmem L) {
   extern __shared__ __align__(16) unsigned char smraw[];
   float4* s_top = reinterpret_cast<float4*>(smraw + L.off_top);
   uint32_t* s_act_nmask = reinterpret_cast<uint32_t*>(smraw + L.off_act_nmask);
@@ -585,7 +592,7 @@ __global__ void __launch_bounds__(TRAV_THREADS, CRSH_TRAV_MINB) k_traverse(const
         const float4* te = a.tri_e + 3 * (size_t)e.y;
         const float4 tv0 = __ldg(te), te1 = __ldg(te + 1), te2 = __ldg(te + 2);
         const f3 v0 = mk3(tv0.x, tv0.y, tv0.z), e1 = mk3(te1.x, te1.y, te1.z), e2 = mk3(te2.x, te2.y, te2.z);
-        const uint32_t rl0 = e.x << logB0;   // first ray of the bundle (B0 even)
+        const uint32_t rl0 = B0T ? e.x * (uint32_t)B0T : e.x << logB0;   // first ray of the bundle (B0 even)
         // ray-plane base of the bundle: its records are ray_rix(rl0/2) + i
         // while they stay inside one block of 8 (compile-time B0 <= 16)
         constexpr bool RB_CONST = B0T >= 2 && B0T <= 16;
@@ -709,16 +716,24 @@ __global__ void __launch_bounds__(TRAV_THREADS, CRSH_TRAV_MINB) k_traverse(const
       }
     };
 
+    uint32_t mlo = 0xFFFFFFFFu;   // the lane's active-mesh index in its previous slice (v only grows)
     for (uint32_t s = item.y + warp * 32u; s < item.z; s += TRAV_THREADS) {
       const uint32_t v = s + lane;
       uint32_t nm = 0, tri = 0;
       float4 sph = make_float4(0.f, 0.f, 0.f, 0.f);
       if (v < item.z) {
-        uint32_t lo = 0, hi = n_act;   // largest p with prefix[p] <= v
-        while (hi - lo > 1) {
-          const uint32_t mid = (lo + hi) >> 1;
-          if (s_act_prefix[mid] <= v) lo = mid; else hi = mid;
+        uint32_t lo = 0;   // largest p with prefix[p] <= v
+        if (mlo == 0xFFFFFFFFu) {   // first slice of the item: binary search
+          uint32_t hi = n_act;
+          while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (s_act_prefix[mid] <= v) lo = mid; else hi = mid;
+          }
+        } else {                    // then forward from the previous slice's mesh
+          lo = mlo;
+          while (lo + 1 < n_act && s_act_prefix[lo + 1] <= v) ++lo;
         }
+        mlo = lo;
         tri = s_act_first[lo] + (v - s_act_prefix[lo]);
         sph = __ldg(a.tri_sph + tri);
         nm = s_act_nmask[lo];
