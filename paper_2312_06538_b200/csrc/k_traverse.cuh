@@ -408,7 +408,6 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
   const float4* s_rays = reinterpret_cast<const float4*>(smraw + L.off_rays);
   uint32_t* s_exm = reinterpret_cast<uint32_t*>(smraw + L.off_exm);
   float4* s_pairs = reinterpret_cast<float4*>(smraw + L.off_pairs);
-  const uint32_t pairs_sa = smem_addr_opaque(s_pairs);   // LVT: the child records' shared address, kept in a register
   float4* s_tpairs = reinterpret_cast<float4*>(smraw + L.off_tpairs);
   __shared__ uint32_t s_item, s_cur_g, s_n_act, s_carry, s_carry_c;
   __shared__ uint32_t s_warp[TRAV_WARPS];
@@ -781,8 +780,7 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
           if (!BT && c >= B) break;
           bool p0, p1;
           if (SMALL) {
-            if (LVT) cull2_sa(pairs_sa + 80u * ((cbase >> 1) + (uint32_t)(c >> 1)), Px, Py, Pz, Pr, p0, p1);
-            else cull2_ns(s_pairs + 5 * ((cbase >> 1) + (uint32_t)(c >> 1)), Px, Py, Pz, Pr, p0, p1);
+            cull2_ns(s_pairs + 5 * ((cbase >> 1) + (uint32_t)(c >> 1)), Px, Py, Pz, Pr, p0, p1);
           } else {
             const float4* nd = s_trav[k1] + 3 * ((size_t)g * s_pg[k1] + cbase + (uint32_t)c);
             const float4 a0 = __ldg(nd), a1 = __ldg(nd + 1), a2 = __ldg(nd + 2), b0 = __ldg(nd + 3),

@@ -261,35 +261,8 @@ __device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) { return __ffma2_rn(a, b, c
 // {Cx0,Cx1,Cy0,Cy1}, {Cz0,Cz1,d0,d1}, {ax0,ax1,ay0,ay1}, {az0,az1,tan0,tan1}, {sec0,sec1,-,-}
 // Eq 9 for both children against one target sphere (px,py,pz,r); same
 // operation order as cull_ns.
-__device__ __forceinline__ void cull2_nsv(float4 A, float4 Bv, float4 Cc, float4 D, float2 E, f2 Px, f2 Py, f2 Pz, f2 R,
-                                          bool& p0, bool& p1);
 __device__ __forceinline__ void cull2_ns(const float4* rec, f2 Px, f2 Py, f2 Pz, f2 R, bool& p0, bool& p1) {
-  const float4 E4 = rec[4];
-  cull2_nsv(rec[0], rec[1], rec[2], rec[3], make_float2(E4.x, E4.y), Px, Py, Pz, R, p0, p1);
-}
-// the same record at a 32-bit shared-memory address held in a register
-// (ld.shared through inline PTX: the compiler cannot rematerialise the
-// address from the shared-window base inside the loop)
-__device__ __forceinline__ uint32_t smem_addr_opaque(const void* p) {
-  uint32_t a;
-  asm volatile("{ .reg .u64 t; cvta.to.shared.u64 t, %1; cvt.u32.u64 %0, t; }" : "=r"(a) : "l"(p));
-  return a;
-}
-__device__ __forceinline__ float4 lds128(uint32_t sa) {
-  float4 v;
-  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(sa));
-  return v;
-}
-__device__ __forceinline__ float2 lds64(uint32_t sa) {
-  float2 v;
-  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(sa));
-  return v;
-}
-__device__ __forceinline__ void cull2_sa(uint32_t sa, f2 Px, f2 Py, f2 Pz, f2 R, bool& p0, bool& p1) {
-  cull2_nsv(lds128(sa), lds128(sa + 16u), lds128(sa + 32u), lds128(sa + 48u), lds64(sa + 64u), Px, Py, Pz, R, p0, p1);
-}
-__device__ __forceinline__ void cull2_nsv(float4 A, float4 Bv, float4 Cc, float4 D, float2 E, f2 Px, f2 Py, f2 Pz, f2 R,
-                                          bool& p0, bool& p1) {
+  const float4 A = rec[0], Bv = rec[1], Cc = rec[2], D = rec[3], E = rec[4];
   const f2 cx = pk2(A.x, A.y), cy = pk2(A.z, A.w), cz = pk2(Bv.x, Bv.y), dd = pk2(Bv.z, Bv.w);
   const f2 ax = pk2(Cc.x, Cc.y), ay = pk2(Cc.z, Cc.w), az = pk2(D.x, D.y), tn = pk2(D.z, D.w), sc = pk2(E.x, E.y);
   const f2 vx = sub2(Px, cx), vy = sub2(Py, cy), vz = sub2(Pz, cz);
