@@ -178,6 +178,36 @@ def test_large_configs_sampled_vs_brute(cfg, flags, n_pick):
         assert st["tests"][seg][1] <= 8 * st["hits"][seg][2] and st["final_tests"][seg] <= 8 * st["hits"][seg][1]
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("flags", [3, 7])
+def test_cfg3_top_level_work_exact(flags):
+    """cfg3 at full size in the bench's launch configuration (hundreds of
+    thousands of work items, handed out in chunks of consecutive items):
+    every (top node, triangle of a mesh the node kept) pair is tested exactly
+    once -- the top-level test count equals the sum over the GPU's top nodes
+    of the triangles of the meshes whose sphere passes Eq 9 (the oracle's
+    cull), and the mesh tests / passes equal that count too (a
+    skipped or twice-processed work item would break the first identity)."""
+    w = make_workload(3)
+    tr = tracer_for(w, flags=flags)
+    tr.run()
+    st = crsh.stats(tr.scene)
+    prep = oracle.ScenePrep(w.tris, w.mesh_ids)
+    counts = (prep.mesh_range[:, 1] - prep.mesh_range[:, 0])[:prep.n_meshes]
+    live = np.flatnonzero(counts > 0)
+    for seg, _, _ in oracle.segments(w.P, w.lights.shape[0], w.ray_types):
+        top = crsh.debug_tap(tr.scene, crsh.TAP_NODES, seg, w.levels)
+        work = mh = 0
+        for node in top:
+            for m in live:
+                if oracle.cull(node, prep.mesh_sph[m]):
+                    mh += 1
+                    work += int(counts[m])
+        assert st["mesh_tests"][seg] == len(top) * len(live), seg
+        assert st["mesh_hits"][seg] == mh, (seg, st["mesh_hits"][seg], mh)
+        assert st["tests"][seg][w.levels] == work, (seg, st["tests"][seg][w.levels], work)
+
+
 def test_slot_limit_and_degenerate_triangles():
     """ELIMIT before any work for >= 2^30 slots; degenerate (zero-area)
     triangles never hit, on the GPU as in the oracle and brute force."""
