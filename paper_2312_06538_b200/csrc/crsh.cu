@@ -398,6 +398,7 @@ crsh_status enqueue_frame(crsh_scene* sc, const FrameInfo& fi, const crsh_primar
       CK(cudaGetLastError());
       ++nl;
       const size_t sm_bytes = (2 * SORT_TILE + SORT_WARPS * RADIX_BINS) * 4;
+      if (sm_bytes > 48 * 1024) CK(cudaFuncSetAttribute(k_onesweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_bytes));
       const uint32_t* kin = sc->ckey.as<uint32_t>();
       const uint32_t* vin = nullptr;
       for (int p = 0; p < SORT_PASSES; ++p) {

@@ -93,7 +93,10 @@ constexpr int RADIX_BITS = 8;
 constexpr int RADIX_BINS = 256;
 constexpr int SORT_THREADS = 256;
 constexpr int SORT_WARPS = SORT_THREADS / 32;
-constexpr int SORT_ITEMS = 16;   // 4096-key tiles: half the tiles (and look-back hops) of 2048 (A/B: sort 0.47 -> 0.44 ms at cfg4)
+#ifndef CRSH_SORT_ITEMS
+#define CRSH_SORT_ITEMS 16
+#endif
+constexpr int SORT_ITEMS = CRSH_SORT_ITEMS;   // 4096-key tiles: half the tiles (and look-back hops) of 2048 (A/B: sort 0.47 -> 0.44 ms at cfg4)
 constexpr int SORT_TILE = SORT_THREADS * SORT_ITEMS;
 constexpr int SORT_PASSES = 32 / RADIX_BITS;
 // k_onesweep at 3 CTAs per SM (80 registers, no spills; 141 registers and 2
