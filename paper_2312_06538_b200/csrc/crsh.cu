@@ -290,9 +290,19 @@ cudaError_t dispatch_b(int B, F&& f) {
 }
 
 #ifndef CRSH_ITEM_TRIS
-#define CRSH_ITEM_TRIS 2048
+#define CRSH_ITEM_TRIS 0   // 0: chosen per frame by item_tris_for(); else fixed (A/B builds)
 #endif
-constexpr uint32_t ITEM_TRIS = CRSH_ITEM_TRIS;   // triangles per traversal work item (load balance)
+// Triangles per traversal work item (load balance). Small frames (about one
+// group per traversal CTA, cfg2) need 2048-triangle items to spread the work;
+// frames with many groups per CTA (cfg3, cfg4) lose less to per-item setup
+// with 4096 (measured on B200, cfg2 R6 2048 / 4096: 109.6 / 107.1 Mrays/s,
+// cfg3 R6 60.0 / 62.1). ITEM_TRIS_MIN sizes the item buffer.
+constexpr uint32_t ITEM_TRIS_MIN = CRSH_ITEM_TRIS ? CRSH_ITEM_TRIS : 2048;
+constexpr uint64_t ITEM_BIG_GROUPS_PER_SM = 16;   // G_max at or above 16 groups per SM -> 4096
+inline uint32_t item_tris_for(uint64_t G_max, int sm_count) {
+  if (CRSH_ITEM_TRIS) return CRSH_ITEM_TRIS;
+  return G_max >= ITEM_BIG_GROUPS_PER_SM * (uint64_t)std::max(sm_count, 1) ? 4096u : 2048u;
+}
 
 // Everything a frame's launch sequence depends on: if the key of a call equals
 // the cached one, the cached CUDA graph is replayed.
@@ -508,7 +518,7 @@ crsh_status enqueue_frame(crsh_scene* sc, const FrameInfo& fi, const crsh_primar
       ++nl;
       PlanArgs p{};
       p.fd = fd; p.group_rays = fi.GR; p.n_seg = fi.n_seg; p.gstat = sc->gstat.as<uint4>(); p.counters = counters;
-      p.item_tris = ITEM_TRIS;
+      p.item_tris = item_tris_for(fi.G_max, sc->sm_count);
       p.items = sc->items.as<uint4>();
       p.status = reinterpret_cast<unsigned long long*>(zb + Z.st_plan); p.ticket = tickets + T_PLAN;
       k_plan<<<cdiv(std::max<uint64_t>(fi.G_max, 1), SCAN_TILE), SCAN_THREADS, 0, st>>>(p);
@@ -646,7 +656,7 @@ crsh_status trace_impl(crsh_scene* sc, const crsh_primary_hits* h, const float* 
   size_t total_nodes = 0;
   for (int k = 1; k <= Lv; ++k) total_nodes += fi.level_max[k];
   const int W = (sc->n_meshes + 31) / 32;
-  const uint64_t items_cap = std::max<uint64_t>(fi.G_max, 1) * cdiv(std::max<int64_t>(sc->M, 1), ITEM_TRIS);
+  const uint64_t items_cap = std::max<uint64_t>(fi.G_max, 1) * cdiv(std::max<int64_t>(sc->M, 1), ITEM_TRIS_MIN);
   CK(grow(sc, sc->zero, Z.total));
   CK(grow(sc, sc->rays, 32 * S));
   CK(grow(sc, sc->keys_c, 4 * S));
