@@ -295,14 +295,18 @@ cudaError_t dispatch_b(int B, F&& f) {
 // Triangles per traversal work item (load balance). Small frames (about one
 // group per traversal CTA, cfg2) need 2048-triangle items to spread the work;
 // frames with many groups per CTA (cfg3, cfg4) lose less to per-item setup
-// with larger items (measured on B200, R6 Mrays/s at 2048 / 4096 / 8192:
-// cfg2 109.6 / 107.1 / -, cfg3 60.0 / 62.1 / 62.8, cfg4 17.2 / 18.0 / 18.4;
-// Z-order cfg3 587 / 636 / 666, cfg4 234 / 261 / 275). ITEM_TRIS_MIN sizes
+// with larger items (measured on B200, Mrays/s at 2048 / 4096 / 8192 /
+// 16384 / 32768 / 65536 / one item per group:
+//   cfg3 R6      60.0 / 62.1 / 62.8 / 63.3 / 62.8 / 63.2 / 55.0
+//   cfg3 Z-order  587 /  636 /  666 /  697 /  698 /  661 /  424
+//   cfg4 R6      17.2 / 18.0 / 18.4 / 18.6 / 18.7 / 18.7 / 18.3
+//   cfg4 Z-order  234 /  261 /  275 /  284 /  289 /  292 /  219;
+// cfg2 R6 at 2048 / 3072 / 4096: 109.6 / 109.1 / 107.1). ITEM_TRIS_MIN sizes
 // the item buffer.
 constexpr uint32_t ITEM_TRIS_MIN = CRSH_ITEM_TRIS ? CRSH_ITEM_TRIS : 2048;
 constexpr uint64_t ITEM_BIG_GROUPS_PER_SM = 16;   // G_max at or above 16 groups per SM -> ITEM_TRIS_BIG
 #ifndef CRSH_ITEM_TRIS_BIG
-#define CRSH_ITEM_TRIS_BIG 8192
+#define CRSH_ITEM_TRIS_BIG 16384
 #endif
 inline uint32_t item_tris_for(uint64_t G_max, int sm_count) {
   if (CRSH_ITEM_TRIS) return CRSH_ITEM_TRIS;
