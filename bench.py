@@ -4,16 +4,18 @@
 One step = one frame of the whole hot path through the C
 ABI call crsh_trace_secondary: generate + hash + trim, compress, radix sort,
 decompress, build, mesh cull, traversal, final tests, per-slot output (plus,
-at N > 1, the NCCL min-merge of the per-rank packed results).
+at N > 1, the library's own NCCL merge of the per-rank results, crsh_dist_init).
 
-Default workload: BASELINE.json configs[1] ("512x512 shadow+reflection rays,
-~70k-triangle multi-mesh procedural scene, 1 B200"), seeded synthetic scene +
-rasterised G-buffer (workloads/).  Timing: W untimed warm-up frames, then K
-frames, each bracketed by CUDA events on the launching stream after an L2
-flush (a 512 MiB write outside the bracket); barrier + synchronize on both
-sides; max over ranks.
+Default workload: BASELINE.json configs[3], the metric's configuration
+("1920x1080 all secondary ray types, 1M triangles in 100 meshes"), seeded
+synthetic scene + rasterised G-buffer (workloads/), with the R6 hash of
+SURVEY §8(c) as `value` and the Z-order hash (NEXT-4) as `value_zorder`.
+--config 2 selects configs[1] (the paper's 512x512 workload).  Timing: W
+untimed warm-up frames, then K frames, each bracketed by CUDA events on the
+launching stream after an L2 flush (a 512 MiB write outside the bracket);
+barrier + synchronize on both sides; max over ranks.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl crsh|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl crsh|reference]
   torchrun --nproc-per-node N bench.py --gpus N ...    (hash-range sharding)
 """
 from __future__ import annotations
@@ -183,7 +185,7 @@ def oracle_sample(w, flags, target_s=12.0):
     seconds, rows, cores)."""
     import oracle
     prep = oracle.ScenePrep(w.tris, w.mesh_ids)
-    rows = max(1, w.height // 64)
+    rows = 1
     while True:
         rays, dt = oracle_band(w, flags, rows, prep)
         if dt >= target_s / 4 or rows >= w.height:
@@ -192,6 +194,98 @@ def oracle_sample(w, flags, target_s=12.0):
 
 
 # ----------------------------------------------------------------------------- GPU arm
+def hbm_bytes(P, st, leaf_size):
+    """Algorithmic HBM bytes of the hash/sort/build stages a1-a8 for one frame,
+    SURVEY §8(d)'s per-ray model with c = chunks / rays:
+    28 B per pixel of G-buffer read (28/rho per ray), then per ray 40 (ray
+    record + key + value) + 4 + 8c (RLE) + 68c (4 onesweep passes of 8-bit
+    digits) + 12c + 8 (decompression) + 4 + 32 + 32 (permutation, gather,
+    sorted-ray write) + 64/B0 (nodes) = 120 + 88c + 64/B0."""
+    n = int(sum(st["rays"]))
+    c = int(sum(st["chunks"]))
+    return 28 * P + n * (120 + 64.0 / leaf_size) + 88 * c
+
+
+def _max_over_ranks(vals, world):
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(vals, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.tolist()
+
+
+def _barrier(world):
+    import torch
+    import torch.distributed as dist
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+def measure(w, flags, args, local, world, flush, clocks=None):
+    """W warm-up frames, then K frames each bracketed by CUDA events on the
+    launching stream after an L2 flush (outside the bracket); barrier +
+    synchronize on both sides; max over ranks. At N > 1 the scene is joined to
+    the NCCL world (crsh_dist_init) and every frame includes the library's
+    merge. Then 3 diagnostic frames with per-stage events (not timed)."""
+    import torch
+
+    import paper_2312_06538_b200 as crsh
+    from paper_2312_06538_b200.api import tracer_for
+    tr = tracer_for(w, device=local, flags=flags | crsh.F_KERNEL_TIMING)
+    if world > 1:
+        tr.dist_init()
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        tr.run(stream)
+    _barrier(world)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    trav = 0.0
+    launches = 0
+    import contextlib
+    with (clocks if clocks is not None else contextlib.nullcontext()):
+        for i in range(args.steps):
+            flush.zero_()
+            ev[i][0].record(stream)
+            tr.run(stream)
+            ev[i][1].record(stream)
+            st = tr.stats()          # synchronises; outside the event bracket
+            trav += st["stage_ms"][6]
+            launches += tr.launches()
+        torch.cuda.synchronize()
+    _barrier(world)
+    total_ms = sum(a.elapsed_time(b) for a, b in ev)
+    st = tr.stats()
+    merge = st["merge"]
+    del tr
+    # per-stage breakdown (diagnostic, outside the timed region): all stage events
+    trs = tracer_for(w, device=local, flags=flags | crsh.F_STAGE_TIMING)
+    if world > 1:
+        trs.dist_init()
+    stage = np.zeros(8)
+    for k in range(4):
+        flush.zero_()
+        trs.run(stream)
+        s_ = trs.stats()
+        if k > 0:
+            stage += np.asarray(s_["stage_ms"]) / 3
+    del trs
+    total_ms, trav_ms, *stage = _max_over_ranks([total_ms, trav / args.steps, *stage.tolist()], world)
+    return dict(total_ms=total_ms, ms=total_ms / args.steps, trav_ms=trav_ms, stage=stage, st=st,
+                launches=launches, merge=merge)
+
+
+def config_dict(w, zorder, world, merge):
+    return {"workload": w.name, "pixels": w.width * w.height, "triangles": int(w.tris.shape[0]),
+            "meshes": int(w.n_meshes), "ray_types": w.ray_types, "lights": int(w.lights.shape[0]),
+            "levels": w.levels, "leaf_size": w.leaf_size, "branching": w.branching,
+            "hash": "zorder" if zorder else "R6 (SPEC layout)",
+            "parallelism": f"hash-range shard x{world}" if world > 1 else "single GPU", "merge": merge,
+            "l2": "flushed before every timed step (512 MiB write outside the event bracket)"}
+
+
 def run_crsh(args):
     import torch
     import torch.distributed as dist
@@ -203,140 +297,51 @@ def run_crsh(args):
     rank, world, local = env_rank()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    flags = crsh.F_SORT | crsh.F_MESH_CULL | (crsh.F_ZORDER if args.zorder else 0)
+        # host plumbing only (NCCL id broadcast, barriers, max over ranks): the
+        # data path is libcrsh's own NCCL communicator (crsh_dist_init)
+        dist.init_process_group("gloo")
+    base = crsh.F_SORT | crsh.F_MESH_CULL
     w = make_workload(args.config)
-    tr = tracer_for(w, device=local, flags=flags | crsh.F_KERNEL_TIMING, shard_rank=rank, shard_world=world)
-    stream = torch.cuda.current_stream()
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device="cuda")
-    packed = torch.empty(max(tr.slots, 1), dtype=torch.int64, device="cuda") if world > 1 else None
-    # N > 1 merge: the fused epilogue stores each rank's owned
-    # results straight into every rank's symmetric window over NVLink
-    # (crsh_trace_secondary_peer), bracketed by device-side barriers; checked
-    # once against the NCCL MIN all-reduce merge, which it replaces (and which
-    # stays the path if the symmetric window is unavailable or disagrees).
-    merge, hdl, ptrs, sbuf = ("none" if world == 1 else "nccl"), None, None, None
-    if world > 1 and not args.nccl_merge:
-        # every rank allocates first and the ranks agree before the collective
-        # rendezvous, so one rank's failure cannot leave the others waiting in it
-        try:
-            import torch.distributed._symmetric_memory as symm_mem
-            sbuf = symm_mem.empty(max(tr.slots, 1), dtype=torch.int64, device=torch.device("cuda", local))
-            ok_alloc = 1
-        except Exception as e:
-            print(f"[bench] symmetric allocation failed ({type(e).__name__}: {e})", file=sys.stderr)
-            ok_alloc = 0
-        flag = torch.tensor([ok_alloc], dtype=torch.int32, device="cuda")
-        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
-    if world > 1 and not args.nccl_merge and int(flag) == 1:
-        try:
-            hdl = symm_mem.rendezvous(sbuf, dist.group.WORLD)
-            ptrs = [int(hdl.buffer_ptrs[r]) for r in range(world)]
-            hdl.barrier()
-            tr.run_peer(ptrs, stream)
-            hdl.barrier()
-            tr.run_packed(packed, stream)
-            dist.all_reduce(packed, op=dist.ReduceOp.MIN)
-            ok = torch.tensor([1 if torch.equal(sbuf, packed) else 0], dtype=torch.int32, device="cuda")
-            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
-            merge = "peer" if int(ok) == 1 else "nccl"
-        except Exception as e:   # no P2P / symmetric memory on this box: keep the NCCL merge
-            print(f"[bench] fused peer merge unavailable ({type(e).__name__}: {e}); NCCL all-reduce merge", file=sys.stderr)
-            merge = "nccl"
-
-    def step():
-        if world == 1:
-            tr.run(stream)
-        elif merge == "peer":
-            hdl.barrier()                      # every rank done reading the previous frame
-            tr.run_peer(ptrs, stream)          # owned results -> every rank's window
-            hdl.barrier()                      # all stores landed
-            tr.unpack(sbuf, stream)
-        else:
-            tr.run_packed(packed, stream)
-            dist.all_reduce(packed, op=dist.ReduceOp.MIN)   # per-slot min-merge over NVLink
-            tr.unpack(packed, stream)
-
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    st0 = tr.stats()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    stage = np.zeros(8)
-    launches = 0
-    with ClockSampler(local) as clk:
-        for i in range(args.steps):
-            flush.zero_()
-            ev[i][0].record(stream)
-            step()
-            ev[i][1].record(stream)
-            st = tr.stats()          # synchronises; outside the event bracket
-            stage += np.asarray(st["stage_ms"])
-            launches += tr.launches() + (1 if world > 1 else 0)   # + the unpack kernel
-        torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    ms = np.array([a.elapsed_time(b) for a, b in ev])
-    total_ms = float(ms.sum())
-    trav_ms = stage[6] / args.steps
-    # per-stage breakdown (diagnostic, outside the timed region): same frames with all stage events
-    trs = tracer_for(w, device=local, flags=flags | crsh.F_STAGE_TIMING, shard_rank=rank, shard_world=world)
-    stage = np.zeros(8)
-    n_diag = 3
-    for _ in range(n_diag + 1):
-        if world == 1:
-            trs.run(stream)
-        else:
-            trs.run_packed(packed, stream)
-            dist.all_reduce(packed, op=dist.ReduceOp.MIN)
-            trs.unpack(packed, stream)
-        s_ = trs.stats()
-        if _ > 0:
-            stage += np.asarray(s_["stage_ms"])
-    stage *= args.steps / n_diag
-    del trs
-    st = tr.stats()
-    # counters: traversal counters are per rank (sum); ray counts are global
-    vec = torch.tensor([total_ms, trav_ms], dtype=torch.float64, device="cuda")
-    cnt = torch.tensor([int(np.asarray(st["tests"]).sum()), int(sum(st["final_tests"])), int(sum(st["mesh_tests"]))],
-                       dtype=torch.int64, device="cuda")
-    if world > 1:
-        dist.all_reduce(vec, op=dist.ReduceOp.MAX)
-        dist.all_reduce(cnt, op=dist.ReduceOp.SUM)
-    total_ms, trav_ms_max = float(vec[0]), float(vec[1])
-    tests_all, final_all, mesh_all = (int(x) for x in cnt.tolist())
+    clk = ClockSampler(local)
+    main_z = bool(args.zorder)
+    m = measure(w, base | (crsh.F_ZORDER if main_z else 0), args, local, world, flush, clk)
+    other = None if args.single_hash else measure(w, base | (0 if main_z else crsh.F_ZORDER), args, local, world, flush)
+    st = m["st"]
     rays = int(sum(st["rays"]))
-    mrays = rays * args.steps / (total_ms * 1e-3) / 1e6
-    # end to end through the public API with HOST buffers (crsh_trace_secondary_host), N = 1 path
-    e2e = None
-    if world == 1:
-        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
-        hpos, hnrm, hmat, hmats = pin(w.pos), pin(w.nrm), pin(w.mat), pin(w.materials)
-        hh = torch.empty(tr.slots, dtype=torch.int32).pin_memory()
-        ht = torch.empty(tr.slots, dtype=torch.float32).pin_memory()
-        for _ in range(2):
-            tr.run_host(hpos.numpy(), hnrm.numpy(), hmat.numpy(), hmats.numpy(), hh.numpy(), ht.numpy(), stream)
-        e_ms = []
-        for _ in range(args.steps):
-            flush.zero_()
-            torch.cuda.synchronize()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            tr.run_host(hpos.numpy(), hnrm.numpy(), hmat.numpy(), hmats.numpy(), hh.numpy(), ht.numpy(), stream)
-            b.record(stream)
-            torch.cuda.synchronize()
-            e_ms.append(a.elapsed_time(b))
-        P = w.width * w.height
-        e2e = {"value": round(rays * len(e_ms) / (sum(e_ms) * 1e-3) / 1e6, 3), "unit": "Mrays/s",
-               "h2d_bytes_per_step": 28 * P + 12 * int(w.materials.shape[0]), "d2h_bytes_per_step": 8 * tr.slots,
-               "api": "crsh_trace_secondary_host"}
+    mrays = rays * args.steps / (m["total_ms"] * 1e-3) / 1e6
+    # end to end through the public API with HOST buffers (crsh_trace_secondary_host):
+    # G-buffer H2D from pinned memory and hit_tri / t D2H inside the timed region
+    tr = tracer_for(w, device=local, flags=base | (crsh.F_ZORDER if main_z else 0))
+    if world > 1:
+        tr.dist_init()
+    stream = torch.cuda.current_stream()
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+    hpos, hnrm, hmat, hmats = pin(w.pos), pin(w.nrm), pin(w.mat), pin(w.materials)
+    hh = torch.empty(tr.slots, dtype=torch.int32).pin_memory()
+    ht = torch.empty(tr.slots, dtype=torch.float32).pin_memory()
+    for _ in range(args.warmup):
+        tr.run_host(hpos.numpy(), hnrm.numpy(), hmat.numpy(), hmats.numpy(), hh.numpy(), ht.numpy(), stream)
+    _barrier(world)
+    e_ms = 0.0
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        tr.run_host(hpos.numpy(), hnrm.numpy(), hmat.numpy(), hmats.numpy(), hh.numpy(), ht.numpy(), stream)
+        b.record(stream)
+        torch.cuda.synchronize()
+        e_ms += a.elapsed_time(b)
+    _barrier(world)
+    e_ms = _max_over_ranks([e_ms], world)[0]
+    P = w.width * w.height
+    e2e = {"value": round(rays * args.steps / (e_ms * 1e-3) / 1e6, 3), "unit": "Mrays/s",
+           "h2d_bytes_per_step": 28 * P + 12 * int(w.materials.shape[0]), "d2h_bytes_per_step": 8 * tr.slots,
+           "api": "crsh_trace_secondary_host"}
+    del tr
     if rank != 0:
-        if world > 1:
-            dist.destroy_process_group()
+        dist.destroy_process_group()
         return
     peaks = measured_peaks()
     clocks = clk.summary()
@@ -347,42 +352,80 @@ def run_crsh(args):
         peak_src = "measured FFMA microbenchmark (profiles/fp32_peak.json)"
     except (OSError, ValueError, KeyError):
         pass
-    tflops = trav_flops(st) / (trav_ms * 1e-3) / 1e12 if trav_ms > 0 else 0.0
-    traffic = load_traffic(args.config, args.zorder)
-    brute = rays * tr.M
-    stage_names = ["generate+trim", "compress", "sort", "decompress", "build", "mesh-cull+plan", "traverse+final",
-                   "output"]
+    hbm_peak = float(peaks.get("hbm_gbs", 6548.2))
+
+    def kernel_roof(mm):
+        s_ = mm["st"]
+        fl = trav_flops(s_) / world          # per GPU: each rank traverses its share
+        a_ = fl / (mm["trav_ms"] * 1e-3) / 1e12 if mm["trav_ms"] > 0 else 0.0
+        fl_s = (int(np.asarray(s_["tests"]).sum()) * 28 + int(sum(s_["final_tests"])) * 55) / world
+        a_s = fl_s / (mm["trav_ms"] * 1e-3) / 1e12 if mm["trav_ms"] > 0 else 0.0
+        return a_, a_s
+
+    def hbm_roof(mm):
+        b_ = hbm_bytes(P, mm["st"], w.leaf_size)
+        t_ = sum(mm["stage"][0:5])
+        return b_, t_
+
+    tfl, tfl_s = kernel_roof(m)
+    hb, hms = hbm_roof(m)
+    t_roof = hb / (hbm_peak * 1e9) * 1e3 + trav_flops(st) / world / (peak_tflops * 1e12) * 1e3
+    tests_all, final_all = int(np.asarray(st["tests"]).sum()), int(sum(st["final_tests"]))
+    brute = rays * w.tris.shape[0]
     out = {
         "metric": METRIC, "value": round(mrays, 3), "unit": "Mrays/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
+        "warmup": args.warmup, "ms_per_step": round(m["ms"], 4), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded procedural scene + rasterised G-buffer, workloads/)",
-        "config": {"workload": w.name, "pixels": w.width * w.height, "triangles": tr.M, "meshes": int(w.n_meshes),
-                   "ray_types": w.ray_types, "lights": int(w.lights.shape[0]), "levels": w.levels,
-                   "leaf_size": w.leaf_size, "branching": w.branching, "hash": "zorder" if args.zorder else "R6 (SPEC layout)",
-                   "parallelism": f"hash-range shard x{world}" if world > 1 else "single GPU",
-                   "merge": {"none": "none (1 GPU)", "peer": "fused peer stores into symmetric windows (NVLink)",
-                             "nccl": "NCCL MIN all-reduce"}[merge],
-                   "l2": "flushed before every timed step (512 MiB write outside the event bracket)"},
+        "config": config_dict(w, main_z, world, crsh.MERGE.get(m["merge"], str(m["merge"]))),
         "rays_per_step": rays,
         "tests_per_ray": round((tests_all + final_all) / max(rays, 1), 2),
         "tests_by_level": {f"L{k}": int(np.asarray(st["tests"])[:, k].sum()) for k in range(w.levels, 0, -1)},
         "hits_by_level": {f"L{k}": int(np.asarray(st["hits"])[:, k].sum()) for k in range(w.levels, 0, -1)},
-        "final_tests": final_all, "mesh_tests": mesh_all,
-        "naive_tests_per_ray": tr.M,
+        "final_tests": final_all, "mesh_tests": int(sum(st["mesh_tests"])),
+        "naive_tests_per_ray": int(w.tris.shape[0]),
         "relative_pct_of_brute": round(100.0 * (tests_all + final_all) / max(brute, 1), 4),
-        "stage_ms": {n: round(v / args.steps, 4) for n, v in zip(stage_names, stage)},
-        "roofline": {"bound": "alu", "kernel": "k_traverse", "achieved": round(tflops, 3), "peak": round(peak_tflops, 2),
-                     "unit": "TFLOP/s", "frac": round(tflops / peak_tflops, 4), "traffic": traffic,
-                     "note": f"FP32: {EQ9_FLOPS} flops per Eq 9 test, {MT_FLOPS} per MT test; peak: {peak_src}; "
-                             f"kernel time from CUDA events around k_traverse"},
-        "gpu_launches": launches,
+        "stage_ms": {n: round(v, 4) for n, v in zip(crsh.STAGES, m["stage"])},
+        "roofline": {
+            "bound": "alu", "kernel": "k_traverse (a9-a12, the dominant kernel)", "achieved": round(tfl, 3),
+            "peak": round(peak_tflops, 2), "unit": "TFLOP/s", "frac": round(tfl / peak_tflops, 4), "traffic": None,
+            "flops_convention": f"{EQ9_FLOPS} flops per Eq 9 test and {MT_FLOPS} per Moller-Trumbore test, the "
+                                f"operations of the evaluated formulas (DESIGN.md §5); with SURVEY §8(d)'s estimates "
+                                f"(28 / 55) frac = {tfl_s / peak_tflops:.4f}",
+            "frac_survey_convention": round(tfl_s / peak_tflops, 4),
+            "note": f"peak: {peak_src}; kernel time from CUDA events around k_traverse on the frame's stream, "
+                    f"per GPU; traffic: see profiles/ (ncu --set full capture), not measured in this run",
+            "hbm_stages": {"bound": "hbm", "stages": "a1-a8 (generate+trim, compress, sort, decompress, build)",
+                           "bytes": int(hb), "ms": round(hms, 4), "achieved": round(hb / (hms * 1e-3) / 1e9, 1),
+                           "peak": hbm_peak, "unit": "GB/s", "frac": round(hb / (hms * 1e-3) / 1e9 / hbm_peak, 4),
+                           "bytes_model": "SURVEY §8(d): 28 B/pixel + (120 + 88 c + 64/B0) B/ray, c = chunks/rays"},
+            "end_to_end": {"t_roof_ms": round(t_roof, 4), "t_measured_ms": round(m["ms"], 4),
+                           "frac": round(t_roof / m["ms"], 4),
+                           "model": "t_roof = a1-a8 bytes / HBM peak + traversal flops per GPU / FP32 peak"},
+        },
+        "gpu_launches": m["launches"],
         "e2e": e2e,
         "paper_context": paper_context(),
         "clocks": clocks,
     }
+    if other is not None:
+        so = other["st"]
+        ro = int(sum(so["rays"]))
+        to = int(np.asarray(so["tests"]).sum()) + int(sum(so["final_tests"]))
+        oa, _ = kernel_roof(other)
+        ob, oms = hbm_roof(other)
+        key = "r6" if main_z else "zorder"
+        out[f"value_{key}"] = round(ro * args.steps / (other["total_ms"] * 1e-3) / 1e6, 3)
+        out[f"ms_per_step_{key}"] = round(other["ms"], 4)
+        out[f"tests_per_ray_{key}"] = round(to / max(ro, 1), 2)
+        out[f"relative_pct_of_brute_{key}"] = round(100.0 * to / max(ro * w.tris.shape[0], 1), 4)
+        out[f"roofline_{key}"] = {"k_traverse_frac": round(oa / peak_tflops, 4),
+                                  "hbm_stages_frac": round(ob / (oms * 1e-3) / 1e9 / hbm_peak, 4),
+                                  "hbm_stages_ms": round(oms, 4),
+                                  "stage_ms": {n: round(v, 4) for n, v in zip(crsh.STAGES, other["stage"])}}
+        out["gpu_launches"] += other["launches"]
     if world == 1 and not args.no_cpu_baseline:
-        cr, cs, rows, cores = oracle_sample(w, flags & 7)
+        cr, cs, rows, cores = oracle_sample(w, base | (crsh.F_ZORDER if main_z else 0))
         out["cpu_baseline"] = {"value": round(cr / cs / 1e6, 5), "unit": "Mrays/s", "cores": cores, "kind": "oracle",
                                "sample": f"{rows} of {w.height} image rows (centre band), {cr} rays, {cs:.1f} s"}
     print(json.dumps(out), flush=True)
@@ -413,7 +456,7 @@ def run_reference(args):
     out = {"metric": METRIC, "value": round(v, 5), "unit": "Mrays/s", "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": round(1e3 * sum(times) / len(times), 2), "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
-           "config": {"workload": w.name},
+           "config": config_dict(w, bool(args.zorder), 1, "none"),
            "cpu_baseline": {"value": round(v, 5), "unit": "Mrays/s", "cores": oracle.default_threads(),
                             "kind": "oracle", "sample": f"{rows_probe} of {w.height} image rows per step"},
            "e2e": {"value": round(v, 5), "unit": "Mrays/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -621,11 +664,13 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=4, help="BASELINE.json configs[N-1]; 4 = the metric's 1920x1080 "
+                                                                 "headline workload")
     ap.add_argument("--impl", default="crsh", choices=["crsh", "reference"])
     ap.add_argument("--zorder", action="store_true", help="Z-order hash layout (SURVEY §8(f) NEXT-4)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--nccl-merge", action="store_true", help="N > 1: NCCL MIN all-reduce merge instead of the fused peer stores")
+    ap.add_argument("--single-hash", action="store_true", help="skip the second hash layout's extra keys")
     ap.add_argument("--table4", action="store_true", help="CRSH vs RAH vs N x M report (not the contract line)")
     ap.add_argument("--sweep", action="store_true", help="cfg5 depth/bundle sweep (not the contract line)")
     ap.add_argument("--whitted", type=int, default=None, metavar="D",
@@ -643,6 +688,8 @@ def main():
         return run_sweep(args)
     if args.warmup < 3:
         args.warmup = 3
+    if args.nccl_merge:
+        os.environ["CRSH_DIST_MERGE"] = "nccl"
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -36,7 +36,7 @@ typedef enum {
   CRSH_ELIMIT = 4, /* exceeds an encoding limit (lights > 16, slots >= 2^30, ...) */
   CRSH_ENOMEM = 5, /* device allocation failed */
   CRSH_ECUDA = 6,  /* CUDA runtime error (incl. no device) */
-  CRSH_ENCCL = 7   /* reserved for collective failures */
+  CRSH_ENCCL = 7   /* NCCL failure (crsh_dist_*, the multi-GPU merge, asynchronous errors) */
 } crsh_status;
 
 /* Ray types (bitmask), "Batches can consist of any combination of
@@ -130,7 +130,9 @@ typedef struct {
   uint64_t mesh_tests[3], mesh_hits[3];
   uint64_t tests[3][9], hits[3][9];
   uint64_t final_tests[3], final_hits[3], rays_hit[3], brute[3];
-  int32_t levels, reserved;
+  int32_t levels;
+  int32_t merge;     /* multi-GPU merge of the last trace: 0 none (one rank), 1 NCCL all-reduce MIN,
+                        2 fused peer stores into the symmetric window (crsh_dist_init) */
   float stage_ms[8]; /* generate+trim, compress, sort, decompress, build,
                         mesh-cull+plan, traverse+final, output */
 } crsh_stats_t;
@@ -278,6 +280,42 @@ crsh_status crsh_trace_secondary_host(crsh_scene_t scene, const crsh_primary_hit
 
 /* Counters of the last trace (synchronises its stream). out: host. */
 crsh_status crsh_stats(crsh_scene_t scene, crsh_stats_t* out);
+
+/* ---------------------------------------------------------------------------
+ * Multi-GPU data plane (SURVEY §8(b) crsh_dist_init, §8(e); BASELINE.json
+ * north_star: "Sorted rays are sharded by contiguous hash range across the GPUs
+ * of one 8xB200 box. Each GPU builds and traverses its own sub-hierarchy, and
+ * the per-pixel hits are gathered with NCCL over NVLink"; the paper itself is
+ * single-GPU). One process per GPU; every rank holds the same scene
+ * and G-buffer and makes the same calls.
+ *
+ * crsh_dist_unique_id: a fresh NCCL unique id (128 bytes, host) that rank 0
+ * creates and every rank receives out of band (e.g. a torch.distributed
+ * broadcast). Errors: EINVAL (null), ENCCL.
+ *
+ * crsh_dist_init: joins `scene` (on its device) to an NCCL communicator of
+ * `world` ranks built from `nccl_uid` (host, 128 bytes); collective over the
+ * ranks. From then on crsh_trace_secondary / crsh_trace_secondary_host on
+ * this scene trace rank `rank`'s work-balanced share of the top-node groups
+ * (opts.shard_rank / shard_world must be 0 / 1 or equal to rank / world) and
+ * MERGE inside the call: every rank's hit_tri / t receive the whole frame and
+ * crsh_stats reports the counters summed over the ranks (stats.merge says
+ * which merge ran). The merge is the fused one of §8(e) -- each rank's
+ * epilogue stores its owned packed results into every rank's symmetric NCCL
+ * window over NVLink (LSA pointers), bracketed by device-side LSA barriers --
+ * when all ranks share one load/store domain of <= 8 GPUs, else (or with the
+ * environment variable CRSH_DIST_MERGE=nccl at init) ncclAllReduce(ncclMin,
+ * ncclUint64) of the packed frames; counters use ncclAllReduce(ncclSum).
+ * Both run inside the frame's CUDA graph on the scene's stream. The window
+ * (8 bytes per slot, ncclMemAlloc) grows collectively on the first trace
+ * that needs more. crsh_trace_secondary_packed / _peer / crsh_trace_rays /
+ * crsh_render_whitted / crsh_primary_gbuffer are unaffected (no merge).
+ * crsh_scene_destroy releases the communicator. Called once per scene.
+ * Errors: EINVAL (bad rank/world, second call), ENCCL (communicator or window
+ * setup), ECUDA. Asynchronous NCCL errors surface as ENCCL from crsh_stats
+ * (ncclCommGetAsyncError). */
+crsh_status crsh_dist_unique_id(void* uid);
+crsh_status crsh_dist_init(crsh_scene_t scene, const void* nccl_uid, int32_t rank, int32_t world);
 
 /* Number of CUDA kernels the library launched during the last trace. */
 int64_t crsh_launch_count(crsh_scene_t scene);

@@ -93,6 +93,8 @@ def lib():
         L.or_traverse.argtypes = [C.c_int32, C.c_int32, C.c_int32, vp, vp, C.c_int64, vp, vp, vp, C.c_int32, vp,
                                   vp, C.c_uint32, C.c_int32, vp, vp]
         L.or_brute.argtypes = [C.c_int64, vp, C.c_int64, vp, C.c_int32, vp]
+        L.or_mesh_cull.restype = None
+        L.or_mesh_cull.argtypes = [C.c_int64, vp, C.c_int32, vp, vp, vp]
         _lib = L
     return _lib
 
@@ -351,6 +353,41 @@ def primary_gbuffer(tris, mesh_ids, tri_mat, cam13, W: int, H: int, levels=2, le
                      _p(np.ascontiguousarray(out["t"], np.float32)), _p(prep.tri_e),
                      _p(np.ascontiguousarray(tri_mat, np.int32)), _p(pos), _p(nrm), _p(mat))
     return pos, nrm, mat, out["hit_tri"], out["t"], out["stats"]
+
+
+def mesh_cull(top_nodes, prep: ScenePrep):
+    """The whole-mesh cull alone (a9) over the given top nodes of the
+    ORACLE's hierarchy: (mesh tests, mesh passes, triangles of the passing
+    meshes = the top-level test count of the traversal)."""
+    top = _f32(top_nodes).reshape(-1, 8)
+    out = np.zeros(3, np.uint64)
+    lib().or_mesh_cull(top.shape[0], _p(top), prep.n_meshes, _p(prep.mesh_sph), _p(prep.mesh_range), _p(out))
+    return int(out[0]), int(out[1]), int(out[2])
+
+
+def top_level_counts(w, prep: ScenePrep | None = None, flags: int = F_SORT | F_MESH_CULL):
+    """Per segment (0 = SH, 1 = RE, 2 = RR): the oracle's own generate -> trim
+    -> sort -> build up to the top level, then the whole-mesh cull of its top
+    nodes; returns {seg: (rays, n_top, mesh_tests, mesh_hits, top_level_tests)}.
+    Checks the counts that do not need the (expensive) descent, at sizes where
+    the full oracle traversal takes too long."""
+    prep = prep or ScenePrep(w.tris, w.mesh_ids)
+    rays, keys, empty = generate(w, prep, flags)
+    S = rays.shape[0]
+    keys_c, vals_c = trim(empty, keys, np.arange(S, dtype=np.uint32))
+    out = {}
+    for seg, s0, ns in segments(w.P, w.lights.shape[0], w.ray_types):
+        sel = (vals_c >= s0) & (vals_c < s0 + ns)
+        k, v = keys_c[sel], vals_c[sel]
+        if len(k) == 0:
+            out[seg] = (0, 0, 0, 0, 0)
+            continue
+        if flags & F_SORT:
+            ck, cb, cs = compress(k)
+            _, v, _ = sort_decompress(ck, cb, cs, v)
+        levels = build_levels(rays[v.astype(np.int64)], w.levels, w.leaf_size, w.branching)
+        out[seg] = (len(k), levels[-1].shape[0], *mesh_cull(levels[-1], prep))
+    return out
 
 
 def _trace_core(rays, keys, empty, segs, prep: ScenePrep, Lv, B0, B, flags, n_threads, taps):

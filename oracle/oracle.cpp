@@ -740,6 +740,30 @@ EXPORT void or_traverse(int32_t Lv, int32_t B0, int32_t B, const float* const* l
   counters_out[18] = tot.final_tests; counters_out[19] = tot.final_hits;
 }
 
+/* Whole-mesh culling alone, the first step of
+ * or_traverse's top-node loop without the descent: for every top node and every
+ * non-empty mesh one Eq 9 test against the mesh sphere; out3 = {mesh tests,
+ * mesh passes, triangles of the passing meshes}. The third number is what
+ * or_traverse counts as the top-level tests (tests[Lv], one per triangle of a
+ * kept mesh), so it checks that count at sizes where the full traversal is too
+ * slow for the oracle. */
+EXPORT void or_mesh_cull(int64_t n_top, const float* top_nodes, int32_t n_meshes, const float* mesh_sph,
+                         const int64_t* mesh_range, uint64_t* out3) {
+  uint64_t tests = 0, hits = 0, kept = 0;
+  for (int64_t n = 0; n < n_top; ++n) {
+    Node top = load_node(top_nodes + 8 * n);
+    for (int32_t m = 0; m < n_meshes; ++m) {
+      if (mesh_range[2 * m + 1] <= mesh_range[2 * m]) continue;
+      tests++;
+      const float* ms = mesh_sph + 4 * m;
+      if (!cull_test(top, v3(ms[0], ms[1], ms[2]), ms[3])) continue;
+      hits++;
+      kept += (uint64_t)(mesh_range[2 * m + 1] - mesh_range[2 * m]);
+    }
+  }
+  out3[0] = tests; out3[1] = hits; out3[2] = kept;
+}
+
 /* Naive N x M ray tracing: closest hit of every ray over all triangles,
  * the plain definition the conservative CRSH path must reproduce (A1). */
 EXPORT void or_brute(int64_t n_rays, const float* rays, int64_t M, const float* tri_e, int32_t n_threads,

@@ -25,6 +25,7 @@ TAP_KEYS, TAP_VALS, TAP_CHUNK_KEYS, TAP_CHUNK_BASE, TAP_SORTED_KEYS, TAP_SORTED_
 TAP_NODES, TAP_SORTED_RAYS, TAP_TRI_SPHERES, TAP_MESH_SPHERES, TAP_SCENE_CONSTS = 7, 8, 9, 10, 11
 TAP_GROUP_RANGE, TAP_GROUP_WORK = 12, 13
 STATUS = {0: "OK", 2: "EINVAL", 3: "EIO", 4: "ELIMIT", 5: "ENOMEM", 6: "ECUDA", 7: "ENCCL"}
+MERGE = {0: "none", 1: "nccl-allreduce-min", 2: "fused-peer-stores"}
 STAGES = ["generate+trim", "compress", "sort", "decompress", "build", "mesh-cull+plan", "traverse+final", "output"]
 
 
@@ -69,7 +70,7 @@ class Stats(C.Structure):
                 ("mesh_tests", C.c_uint64 * 3), ("mesh_hits", C.c_uint64 * 3),
                 ("tests", (C.c_uint64 * 9) * 3), ("hits", (C.c_uint64 * 9) * 3),
                 ("final_tests", C.c_uint64 * 3), ("final_hits", C.c_uint64 * 3), ("rays_hit", C.c_uint64 * 3),
-                ("brute", C.c_uint64 * 3), ("levels", C.c_int32), ("reserved", C.c_int32),
+                ("brute", C.c_uint64 * 3), ("levels", C.c_int32), ("merge", C.c_int32),
                 ("stage_ms", C.c_float * 8)]
 
 
@@ -118,6 +119,10 @@ def load():
     L.crsh_stats.argtypes = [vp, C.POINTER(Stats)]
     L.crsh_launch_count.restype = C.c_int64
     L.crsh_launch_count.argtypes = [vp]
+    L.crsh_dist_unique_id.restype = st
+    L.crsh_dist_unique_id.argtypes = [vp]
+    L.crsh_dist_init.restype = st
+    L.crsh_dist_init.argtypes = [vp, vp, C.c_int32, C.c_int32]
     L.crsh_debug_tap.restype = st
     L.crsh_debug_tap.argtypes = [vp, C.c_int32, C.c_int32, C.c_int32, vp, C.c_size_t, C.POINTER(C.c_size_t)]
     _lib = L
@@ -266,7 +271,7 @@ def stats(scene: Scene) -> dict:
                 mesh_hits=list(s.mesh_hits), tests=np.array([list(r) for r in s.tests], np.uint64),
                 hits=np.array([list(r) for r in s.hits], np.uint64), final_tests=list(s.final_tests),
                 final_hits=list(s.final_hits), rays_hit=list(s.rays_hit), brute=list(s.brute), levels=s.levels,
-                stage_ms=list(s.stage_ms))
+                merge=s.merge, stage_ms=list(s.stage_ms))
 
 
 def launch_count(scene: Scene) -> int:

@@ -44,6 +44,14 @@ class Tracer:
         self.hit_tri = torch.empty(max(self.slots, 1), dtype=torch.int32, device=self.device)
         self.t = torch.empty(max(self.slots, 1), dtype=torch.float32, device=self.device)
 
+    def dist_init(self, group=None):
+        """Join the scene to the torch.distributed world (crsh_dist_init): later
+        run() calls trace this rank's share and return the merged frame."""
+        from . import dist
+        rank, world = dist.init_from_torch(self.scene, group)
+        self.opts.shard_rank, self.opts.shard_world = rank, world
+        return rank, world
+
     def run(self, stream=None):
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         trace_secondary(self.scene, self.hits, self.lights, self.ray_types, self.opts, self.hit_tri, self.t,

@@ -17,6 +17,20 @@ FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-li
          "-prec-div=true", "-prec-sqrt=true", "-ftz=false", "-Xcompiler", "-fPIC", "-shared", "-cudart", "static"]
 
 
+def nccl_dir() -> str:
+    """The NCCL 2.28 that torch ships (headers incl. the device API, and
+    libnccl.so.2); libcrsh links it with an rpath, so a process that already
+    loaded torch's NCCL shares that one copy (same soname)."""
+    import nvidia.nccl
+    return list(nvidia.nccl.__path__)[0]
+
+
+def nccl_flags():
+    d = nccl_dir()
+    return ["-I" + os.path.join(d, "include"), "-L" + os.path.join(d, "lib"), "-l:libnccl.so.2", "-Xlinker",
+            "-rpath=" + os.path.join(d, "lib")]
+
+
 def sources():
     return sorted(glob.glob(os.path.join(HERE, "csrc", "*.cu*"))) + [os.path.join(os.path.dirname(HERE), "include",
                                                                                  "crsh.h")]
@@ -31,7 +45,7 @@ def needs_build() -> bool:
 
 def build(force: bool = False, verbose: bool = False) -> str:
     if force or needs_build():
-        cmd = [NVCC, *FLAGS, *(["-Xptxas", "-v"] if verbose else []), "-o", OUT + ".tmp", SRC]
+        cmd = [NVCC, *FLAGS, *nccl_flags(), *(["-Xptxas", "-v"] if verbose else []), "-o", OUT + ".tmp", SRC]
         subprocess.check_call(cmd)
         os.replace(OUT + ".tmp", OUT)
     return OUT

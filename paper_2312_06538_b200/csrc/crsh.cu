@@ -21,6 +21,7 @@
 #include "k_traverse.cuh"
 #include "k_whitted.cuh"
 #include "k_primary.cuh"
+#include "dist.cuh"
 
 using namespace crsh;
 
@@ -37,6 +38,13 @@ crsh_status fail(crsh_status s, const char* fmt, ...) {
   g_err = buf;
   return s;
 }
+
+#define NCK(call)                                                                                    \
+  do {                                                                                               \
+    ncclResult_t n_ = (call);                                                                        \
+    if (n_ != ncclSuccess) return fail(CRSH_ENCCL, "%s: %s (%s:%d)", #call, ncclGetErrorString(n_),   \
+                                       __FILE__, __LINE__);                                          \
+  } while (0)
 
 #define CK(call)                                                                                     \
   do {                                                                                               \
@@ -190,6 +198,7 @@ struct FrameInfo {
   size_t level_off[MAX_LEVELS + 1] = {0};   // node offset of level k in the node arrays (from the bounds)
   uint64_t level_max[MAX_LEVELS + 1] = {0};
   uint32_t flags = 0;
+  uint32_t item_tris = 2048;                // triangles per traversal work item (item_tris_for)
   int rank = 0, world = 1;
   bool sorted = false, timed = false, ktimed = false, brute = false;
   const float4* in_rays = nullptr;          // ray-batch mode (crsh_trace_rays)
@@ -227,6 +236,7 @@ struct crsh_scene {
   // dynamic scenes (crsh_scene_transform): creation-time geometry and spheres
   Buf tris0, mesh_ids, tris_cur, xf, boxk;
   std::vector<float> h_mesh_sph0;
+  Dist* dist = nullptr;                 // crsh_dist_init: NCCL communicator, window, merge mode
 };
 
 namespace {
@@ -301,16 +311,24 @@ cudaError_t dispatch_b(int B, F&& f) {
 //   cfg3 Z-order  587 /  636 /  666 /  697 /  698 /  661 /  424
 //   cfg4 R6      17.2 / 18.0 / 18.4 / 18.6 / 18.7 / 18.7 / 18.3
 //   cfg4 Z-order  234 /  261 /  275 /  284 /  289 /  292 /  219;
-// cfg2 R6 at 2048 / 3072 / 4096: 109.6 / 109.1 / 107.1). ITEM_TRIS_MIN sizes
-// the item buffer.
-constexpr uint32_t ITEM_TRIS_MIN = CRSH_ITEM_TRIS ? CRSH_ITEM_TRIS : 2048;
+// cfg2 R6 at 2048 / 3072 / 4096: 109.6 / 109.1 / 107.1).
 constexpr uint64_t ITEM_BIG_GROUPS_PER_SM = 16;   // G_max at or above 16 groups per SM -> ITEM_TRIS_BIG
 #ifndef CRSH_ITEM_TRIS_BIG
 #define CRSH_ITEM_TRIS_BIG 16384
 #endif
-inline uint32_t item_tris_for(uint64_t G_max, int sm_count) {
+// The decision uses this rank's share of the groups (G_max / world): with
+// hash-range sharding a rank traverses about G_max / world groups, and a small
+// share needs the small items to balance. CRSH_ITEM_TRIS=<n> (environment,
+// read per call) forces n triangles per item -- a test hook that runs the
+// large-item path on small frames.
+inline uint32_t item_tris_for(uint64_t G_max, int world, int sm_count) {
   if (CRSH_ITEM_TRIS) return CRSH_ITEM_TRIS;
-  return G_max >= ITEM_BIG_GROUPS_PER_SM * (uint64_t)std::max(sm_count, 1) ? (uint32_t)CRSH_ITEM_TRIS_BIG : 2048u;
+  if (const char* e = std::getenv("CRSH_ITEM_TRIS")) {
+    const long v = std::strtol(e, nullptr, 10);
+    if (v >= 32 && v <= (1l << 24) && (v % 32) == 0) return (uint32_t)v;
+  }
+  const uint64_t share = G_max / (uint64_t)std::max(world, 1);
+  return share >= ITEM_BIG_GROUPS_PER_SM * (uint64_t)std::max(sm_count, 1) ? (uint32_t)CRSH_ITEM_TRIS_BIG : 2048u;
 }
 
 // Everything a frame's launch sequence depends on: if the key of a call equals
@@ -323,6 +341,7 @@ struct CallKey {
   uint32_t types;
   crsh_opts o;
   uint64_t gen;
+  uint32_t item_tris;
 };
 
 // The ray-definition part of K1's arguments (G-buffer, lights, slot layout);
@@ -348,7 +367,7 @@ RaygenArgs raygen_def(const crsh_scene* sc, const FrameInfo& fi, const crsh_prim
 // number of kernels launched.
 crsh_status enqueue_frame(crsh_scene* sc, const FrameInfo& fi, const crsh_primary_hits* h, const float* lights,
                           int32_t n_lights, int32_t* out_hit, float* out_t, unsigned long long* out_packed,
-                          const PeerOut& peer, cudaStream_t st, int64_t* n_launch) {
+                          const PeerOut& peer, cudaStream_t st, int64_t* n_launch, const Dist* dist = nullptr) {
   const uint64_t S = fi.S;
   const int Lv = fi.Lv, B0 = fi.B0, B = fi.B;
   const ZeroLayout Z = ZeroLayout::make(S, fi.G_max);
@@ -367,6 +386,13 @@ crsh_status enqueue_frame(crsh_scene* sc, const FrameInfo& fi, const crsh_primar
                                                 : cudaEventRecord(sc->ev[i], st);
   };
   CK(cudaMemsetAsync(sc->zero.p, 0, Z.total, st));
+  if (dist && dist->mode == MERGE_PEER) {
+    // every rank has finished reading its window (previous frame's unpack)
+    // before any rank stores this frame's results into it
+    k_lsa_barrier<<<1, 128, 0, st>>>(dist->dev);
+    CK(cudaGetLastError());
+    ++nl;
+  }
   CK(mark(0));
 
   // ---------------------------------------------------------------- K1: generate + hash + trim
@@ -527,7 +553,7 @@ crsh_status enqueue_frame(crsh_scene* sc, const FrameInfo& fi, const crsh_primar
       ++nl;
       PlanArgs p{};
       p.fd = fd; p.group_rays = fi.GR; p.n_seg = fi.n_seg; p.gstat = sc->gstat.as<uint4>(); p.counters = counters;
-      p.item_tris = item_tris_for(fi.G_max, sc->sm_count);
+      p.item_tris = fi.item_tris;
       p.items = sc->items.as<uint4>();
       p.status = reinterpret_cast<unsigned long long*>(zb + Z.st_plan); p.ticket = tickets + T_PLAN;
       k_plan<<<cdiv(std::max<uint64_t>(fi.G_max, 1), SCAN_TILE), SCAN_THREADS, 0, st>>>(p);
@@ -576,6 +602,20 @@ crsh_status enqueue_frame(crsh_scene* sc, const FrameInfo& fi, const crsh_primar
       ++nl;
     }
   }
+  if (dist) {   // a14: merge the per-rank results into hit_tri / t on every rank, sum the counters
+    unsigned long long* wb = static_cast<unsigned long long*>(dist->wbuf);
+    if (dist->mode == MERGE_PEER) {
+      k_lsa_barrier<<<1, 128, 0, st>>>(dist->dev);   // every rank's stores have landed in every window
+      CK(cudaGetLastError());
+      ++nl;
+    } else {
+      NCK(ncclAllReduce(wb, wb, S, ncclUint64, ncclMin, dist->comm, st));
+    }
+    k_unpack_packed<<<std::min<uint32_t>(cdiv(S, 256), 8 * sc->sm_count), 256, 0, st>>>(wb, S, out_hit, out_t);
+    CK(cudaGetLastError());
+    ++nl;
+    NCK(ncclAllReduce(counters, counters, (size_t)MAX_SEG * CTR_STRIDE, ncclUint64, ncclSum, dist->comm, st));
+  }
   CK(mark(8));
   CK(cudaMemcpyAsync(sc->h_counters, counters, 8 * MAX_SEG * CTR_STRIDE, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(sc->h_fd, fd, sizeof(FrameDesc), cudaMemcpyDeviceToHost, st));
@@ -583,10 +623,12 @@ crsh_status enqueue_frame(crsh_scene* sc, const FrameInfo& fi, const crsh_primar
   return CRSH_OK;
 }
 
+crsh_status dist_window(crsh_scene* sc, size_t bytes);
+
 crsh_status trace_impl(crsh_scene* sc, const crsh_primary_hits* h, const float* lights, int32_t n_lights,
                        uint32_t types, const crsh_opts* o, int32_t* out_hit, float* out_t,
-                       unsigned long long* out_packed, const PeerOut& peer, cudaStream_t st, bool graph_ok = true,
-                       const float4* in_rays = nullptr) {
+                       unsigned long long* out_packed, const PeerOut& peer_in, cudaStream_t st, bool graph_ok = true,
+                       const float4* in_rays = nullptr, bool use_dist = false) {
   if (!sc || !h || !o) return fail(CRSH_EINVAL, "null scene / hits / opts");
   if (h->width <= 0 || h->height <= 0) return fail(CRSH_EINVAL, "width/height must be positive");
   const uint64_t P64 = (uint64_t)h->width * (uint64_t)h->height;
@@ -604,10 +646,20 @@ crsh_status trace_impl(crsh_scene* sc, const crsh_primary_hits* h, const float* 
   uint64_t span = B0;
   for (int k = 1; k < Lv; ++k) span *= B;
   if (span > (1ull << 22)) return fail(CRSH_ELIMIT, "leaf_size * branching^(levels-1) > 2^22");
-  const int world = std::max(1, o->shard_world), rank = o->shard_rank;
+  int world = std::max(1, o->shard_world), rank = o->shard_rank;
   if (rank < 0 || rank >= world) return fail(CRSH_EINVAL, "bad shard rank/world");
+  const Dist* dist = (use_dist && sc && sc->dist) ? sc->dist : nullptr;
+  if (dist) {   // the scene's NCCL world decides the shard (crsh_dist_init)
+    if (world > 1 && (world != dist->world || rank != dist->rank))
+      return fail(CRSH_EINVAL, "opts shard (%d of %d) differs from crsh_dist_init (%d of %d)", rank, world,
+                  dist->rank, dist->world);
+    rank = dist->rank;
+    world = dist->world;
+  }
+  PeerOut peer = peer_in;
   if ((o->flags & ~63u) != 0) return fail(CRSH_EINVAL, "unknown flags");
   if (!peer.n && !out_packed && (!out_hit || !out_t)) return fail(CRSH_EINVAL, "null output");
+  if (dist && (peer.n || out_packed || in_rays)) return fail(CRSH_EINVAL, "internal: dist merge with explicit outputs");
 
   // ---------------------------------------------------------------- static plan
   FrameInfo fi;
@@ -649,6 +701,12 @@ crsh_status trace_impl(crsh_scene* sc, const crsh_primary_hits* h, const float* 
     }
   }
   CK(cudaSetDevice(sc->device));
+  if (dist && S > 0) {   // the packed frame lives in the symmetric window (collective growth)
+    crsh_status rc = dist_window(sc, 8 * S);
+    if (rc != CRSH_OK) return rc;
+    if (dist->mode == MERGE_PEER) peer = dist->peers;
+    else out_packed = static_cast<unsigned long long*>(dist->wbuf);
+  }
   sc->last_stream = st;
   sc->fi = fi;
   sc->fi.valid = false;
@@ -665,7 +723,9 @@ crsh_status trace_impl(crsh_scene* sc, const crsh_primary_hits* h, const float* 
   size_t total_nodes = 0;
   for (int k = 1; k <= Lv; ++k) total_nodes += fi.level_max[k];
   const int W = (sc->n_meshes + 31) / 32;
-  const uint64_t items_cap = std::max<uint64_t>(fi.G_max, 1) * cdiv(std::max<int64_t>(sc->M, 1), ITEM_TRIS_MIN);
+  fi.item_tris = item_tris_for(fi.G_max, world, sc->sm_count);
+  sc->fi.item_tris = fi.item_tris;
+  const uint64_t items_cap = std::max<uint64_t>(fi.G_max, 1) * cdiv(std::max<int64_t>(sc->M, 1), fi.item_tris);
   CK(grow(sc, sc->zero, Z.total));
   CK(grow(sc, sc->rays, 32 * S));
   CK(grow(sc, sc->keys_c, 4 * S));
@@ -696,13 +756,13 @@ crsh_status trace_impl(crsh_scene* sc, const crsh_primary_hits* h, const float* 
   key.W = h->width; key.H = h->height; key.n_mat = h->n_mat; key.n_lights = n_lights;
   for (int i = 0; i < 3; ++i) key.eye[i] = h->eye[i];
   for (int i = 0; i < 3 * n_lights; ++i) key.lights[i] = lights[i];
-  key.types = types; key.o = *o; key.gen = sc->gen;
+  key.types = types; key.o = *o; key.gen = sc->gen; key.item_tris = fi.item_tris;
   std::vector<unsigned char> kb(sizeof(CallKey));
   std::memcpy(kb.data(), &key, sizeof(CallKey));
   static const bool use_graph = !std::getenv("CRSH_NO_GRAPH");
   if (!use_graph || !graph_ok) {
     int64_t nl = 0;
-    crsh_status rc = enqueue_frame(sc, fi, h, lights, n_lights, out_hit, out_t, out_packed, peer, st, &nl);
+    crsh_status rc = enqueue_frame(sc, fi, h, lights, n_lights, out_hit, out_t, out_packed, peer, st, &nl, dist);
     if (rc != CRSH_OK) return rc;
     sc->launches = nl;
   } else {
@@ -710,7 +770,8 @@ crsh_status trace_impl(crsh_scene* sc, const crsh_primary_hits* h, const float* 
       if (sc->gexec) { cudaGraphExecDestroy(sc->gexec); sc->gexec = nullptr; }
       CK(cudaStreamBeginCapture(sc->gstream, cudaStreamCaptureModeThreadLocal));
       int64_t nl = 0;
-      crsh_status rc = enqueue_frame(sc, fi, h, lights, n_lights, out_hit, out_t, out_packed, peer, sc->gstream, &nl);
+      crsh_status rc = enqueue_frame(sc, fi, h, lights, n_lights, out_hit, out_t, out_packed, peer, sc->gstream, &nl,
+                                     dist);
       cudaGraph_t g = nullptr;
       cudaError_t e = cudaStreamEndCapture(sc->gstream, &g);
       if (rc != CRSH_OK) { if (g) cudaGraphDestroy(g); return rc; }
@@ -738,6 +799,11 @@ crsh_status sync_frame(crsh_scene* sc) {
   CK(cudaSetDevice(sc->device));
   CK(cudaStreamSynchronize(sc->last_stream));
   if (sc->gstream) CK(cudaStreamSynchronize(sc->gstream));
+  if (sc->dist) {
+    ncclResult_t ae = ncclSuccess;
+    NCK(ncclCommGetAsyncError(sc->dist->comm, &ae));
+    if (ae != ncclSuccess) return fail(CRSH_ENCCL, "NCCL asynchronous error: %s", ncclGetErrorString(ae));
+  }
   if (sc->fi.valid && !sc->fi.fd_fresh) {
     sc->fi.fd = *sc->h_fd;
     sc->fi.fd_fresh = true;
@@ -745,10 +811,87 @@ crsh_status sync_frame(crsh_scene* sc) {
   return CRSH_OK;
 }
 
+// Grow the symmetric window that holds the packed frame (collective: every
+// rank calls it in the same trace, with the same slot count). No frame may
+// still use the old window.
+crsh_status dist_window(crsh_scene* sc, size_t bytes) {
+  Dist* d = sc->dist;
+  if (d->wbuf && d->wcap >= bytes) return CRSH_OK;
+  CK(cudaStreamSynchronize(sc->last_stream));
+  if (sc->gstream) CK(cudaStreamSynchronize(sc->gstream));
+  if (d->win) { NCK(ncclCommWindowDeregister(d->comm, d->win)); d->win = nullptr; }
+  if (d->wbuf) { NCK(ncclMemFree(d->wbuf)); d->wbuf = nullptr; d->wcap = 0; }
+  const size_t want = roundup(std::max<size_t>(bytes + bytes / 8, 4096), NCCL_WIN_REQUIRED_ALIGNMENT);
+  NCK(ncclMemAlloc(&d->wbuf, want));
+  d->wcap = want;
+  if (d->mode == MERGE_PEER) {
+    NCK(ncclCommWindowRegister(d->comm, d->wbuf, want, &d->win, NCCL_WIN_COLL_SYMMETRIC));
+    k_window_peers<<<1, 32>>>(d->win, d->world, d->d_ptrs);
+    CK(cudaGetLastError());
+    unsigned long long h[MAX_PEERS] = {0};
+    CK(cudaMemcpy(h, d->d_ptrs, 8 * d->world, cudaMemcpyDeviceToHost));
+    d->peers = PeerOut{};
+    for (int r = 0; r < d->world; ++r) {
+      if (!h[r]) return fail(CRSH_ENCCL, "no load/store pointer to the window of rank %d", r);
+      d->peers.p[r] = reinterpret_cast<unsigned long long*>(h[r]);
+    }
+    d->peers.n = d->world;
+  }
+  ++sc->gen;   // the frame graph holds the window addresses: recapture
+  return CRSH_OK;
+}
+
 }  // namespace
 
 // ============================================================== C ABI
 extern "C" {
+
+crsh_status crsh_dist_unique_id(void* uid) {
+  if (!uid) return fail(CRSH_EINVAL, "uid is null");
+  ncclUniqueId id;
+  NCK(ncclGetUniqueId(&id));
+  std::memcpy(uid, &id, sizeof id);
+  return CRSH_OK;
+}
+
+crsh_status crsh_dist_init(crsh_scene_t sc, const void* nccl_uid, int32_t rank, int32_t world) {
+  if (!sc || !nccl_uid) return fail(CRSH_EINVAL, "null argument");
+  if (world < 1 || rank < 0 || rank >= world) return fail(CRSH_EINVAL, "bad rank %d / world %d", rank, world);
+  if (sc->dist) return fail(CRSH_EINVAL, "crsh_dist_init already called on this scene");
+  CK(cudaSetDevice(sc->device));
+  auto* d = new Dist();
+  d->rank = rank;
+  d->world = world;
+  ncclUniqueId id;
+  std::memcpy(&id, nccl_uid, sizeof id);
+  ncclResult_t r = ncclCommInitRank(&d->comm, world, id, rank);
+  if (r != ncclSuccess) {
+    delete d;
+    return fail(CRSH_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+  }
+  sc->dist = d;   // from here on crsh_scene_destroy releases it
+  // the fused merge needs every rank reachable by load/store (one NVLink
+  // domain), at most MAX_PEERS ranks and the device API; the NCCL all-reduce
+  // merge is the fallback (or CRSH_DIST_MERGE=nccl). All ranks agree.
+  const char* want = std::getenv("CRSH_DIST_MERGE");
+  int peer_ok = (!want || std::strcmp(want, "nccl") != 0) && world <= MAX_PEERS &&
+                ncclTeamLsa(d->comm).nRanks == world;
+  if (peer_ok) {
+    ncclDevCommRequirements req{};
+    req.lsaBarrierCount = 1;
+    peer_ok = ncclDevCommCreate(d->comm, &req, &d->dev) == ncclSuccess;
+    d->dev_ok = peer_ok != 0;
+  }
+  CK(cudaMalloc(&d->d_ptrs, 8 * MAX_PEERS + 8));
+  int* flag = reinterpret_cast<int*>(d->d_ptrs + MAX_PEERS);
+  CK(cudaMemcpy(flag, &peer_ok, sizeof(int), cudaMemcpyHostToDevice));
+  NCK(ncclAllReduce(flag, flag, 1, ncclInt32, ncclMin, d->comm, sc->gstream));
+  CK(cudaStreamSynchronize(sc->gstream));
+  CK(cudaMemcpy(&peer_ok, flag, sizeof(int), cudaMemcpyDeviceToHost));
+  d->mode = peer_ok ? MERGE_PEER : MERGE_NCCL;
+  ++sc->gen;
+  return CRSH_OK;
+}
 
 const char* crsh_last_error(void) { return g_err.c_str(); }
 
@@ -858,6 +1001,16 @@ void crsh_scene_destroy(crsh_scene_t sc) {
   for (auto& w : sc->wb) for (auto& b : w) b.release();
   sc->w_hit.release(); sc->w_t.release(); sc->w_zero.release(); sc->prim_rays.release();
   sc->tris0.release(); sc->mesh_ids.release(); sc->tris_cur.release(); sc->xf.release(); sc->boxk.release();
+  if (sc->dist) {
+    Dist* d = sc->dist;
+    if (d->win) ncclCommWindowDeregister(d->comm, d->win);
+    if (d->wbuf) ncclMemFree(d->wbuf);
+    if (d->dev_ok) ncclDevCommDestroy(d->comm, &d->dev);
+    if (d->d_ptrs) cudaFree(d->d_ptrs);
+    if (d->comm) ncclCommDestroy(d->comm);
+    delete d;
+    sc->dist = nullptr;
+  }
   if (sc->h_counters) cudaFreeHost(sc->h_counters);
   if (sc->h_fd) cudaFreeHost(sc->h_fd);
   if (sc->gexec) cudaGraphExecDestroy(sc->gexec);
@@ -870,7 +1023,8 @@ void crsh_scene_destroy(crsh_scene_t sc) {
 
 crsh_status crsh_trace_secondary(crsh_scene_t sc, const crsh_primary_hits* h, const float* lights, int32_t n_lights,
                                  uint32_t types, const crsh_opts* o, int32_t* hit_tri, float* t, void* stream) {
-  return trace_impl(sc, h, lights, n_lights, types, o, hit_tri, t, nullptr, PeerOut{}, (cudaStream_t)stream);
+  return trace_impl(sc, h, lights, n_lights, types, o, hit_tri, t, nullptr, PeerOut{}, (cudaStream_t)stream, true,
+                    nullptr, true);
 }
 
 crsh_status crsh_trace_secondary_packed(crsh_scene_t sc, const crsh_primary_hits* h, const float* lights,
@@ -934,6 +1088,10 @@ extern "C" {
 crsh_status crsh_scene_transform(crsh_scene_t sc, const float* xforms) {
   if (!sc || !xforms) return fail(CRSH_EINVAL, "null argument");
   CK(cudaSetDevice(sc->device));
+  // an in-flight frame (on the caller's stream or the scene's graph stream,
+  // both possibly non-blocking) still reads the geometry rewritten below
+  CK(cudaStreamSynchronize(sc->last_stream));
+  if (sc->gstream) CK(cudaStreamSynchronize(sc->gstream));
   const int n = sc->n_meshes;
   for (int i = 0; i < 12 * n; ++i)
     if (!std::isfinite(xforms[i])) return fail(CRSH_EINVAL, "non-finite transform");
@@ -1159,7 +1317,7 @@ crsh_status crsh_trace_secondary_host(crsh_scene_t sc, const crsh_primary_hits* 
   dh.pos = dpos; dh.nrm = dnrm; dh.mat = dmat; dh.materials = dmats;
   int32_t* dhit = sc->stage_out.as<int32_t>();
   float* dt = reinterpret_cast<float*>(dhit + S);
-  crsh_status rc = trace_impl(sc, &dh, lights, n_lights, types, o, dhit, dt, nullptr, PeerOut{}, st);
+  crsh_status rc = trace_impl(sc, &dh, lights, n_lights, types, o, dhit, dt, nullptr, PeerOut{}, st, true, nullptr, true);
   if (rc != CRSH_OK) return rc;
   CK(cudaMemcpyAsync(hit_tri, dhit, 4 * (size_t)S, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(t, dt, 4 * (size_t)S, cudaMemcpyDeviceToHost, st));
@@ -1175,6 +1333,7 @@ crsh_status crsh_stats(crsh_scene_t sc, crsh_stats_t* out) {
   const FrameInfo& fi = sc->fi;
   if (!fi.valid) return CRSH_OK;
   out->levels = fi.Lv;
+  out->merge = sc->dist ? sc->dist->mode : MERGE_NONE;
   for (int s = 0; s < fi.n_seg; ++s) {
     const int ty = fi.seg_type[s];
     const unsigned long long* c = sc->h_counters + s * CTR_STRIDE;

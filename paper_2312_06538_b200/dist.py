@@ -1,86 +1,50 @@
-"""Hash-range sharding across GPUs: host-side plumbing.
-
-Each rank traces the whole frame's a1-a8 (generate .. build, < 2% of a frame)
-and traverses its contiguous range of top-node groups, writing one packed
-uint64 per slot (crsh_trace_secondary_packed, encoding in include/crsh.h).
-The per-slot results are merged by an element-wise MIN all-reduce (NCCL over
-NVLink on GPUs, gloo in the CPU tests) -- each slot has exactly one owner,
-whose value is below every non-owner sentinel -- and the traversal counters
-are summed.
-"""
+"""Multi-GPU binding (include/crsh.h: crsh_dist_unique_id, crsh_dist_init):
+the NCCL communicator, the symmetric window and the merge all live in
+libcrsh.so (csrc/dist.cuh); this module only marshals arguments and moves the
+128-byte NCCL unique id from rank 0 to the other ranks through
+torch.distributed (any backend; gloo is enough -- the data path never touches
+torch's process group)."""
 from __future__ import annotations
 
-import numpy as np
+import ctypes as C
 
-PACK_EMPTY = 0x7FFFFFFFFFFFFFFF
-PACK_MISS = 0x7F800000FFFFFFFF
-
-
-def group_range(G: int, rank: int, world: int):
-    """Contiguous group range of `rank` by group COUNT (the library's rule
-    when no group has any work)."""
-    return G * rank // world, G * (rank + 1) // world
+from . import MERGE, Scene, _check, load
 
 
-def balanced_cut(work, rank: int, world: int):
-    """Host mirror of k_cut (include/crsh.h, shard_rank/shard_world): the
-    contiguous group range of `rank` cut at equal work. With P(g) the work of
-    groups [0, g) and T = P(G): cut(q) = min{g : P(g) >= ceil(T q / world)},
-    cut(0) = 0, cut(world) = G; rank r owns [cut(r), cut(r+1))."""
-    work = np.asarray(work, dtype=np.uint64)
-    G = len(work)
-    total = int(work.sum())
-    if world <= 1:
-        return 0, G
-    if total == 0:
-        return group_range(G, rank, world)
-    pre = np.concatenate([[0], np.cumsum(work, dtype=np.uint64)]).astype(object)
-
-    def cut(q):
-        if q <= 0:
-            return 0
-        if q >= world:
-            return G
-        target = (total * q + world - 1) // world
-        return next(g for g in range(G + 1) if pre[g] >= target)
-    lo, hi = cut(rank), cut(rank + 1)
-    return lo, max(lo, hi)
+def unique_id() -> bytes:
+    """crsh_dist_unique_id: a fresh NCCL unique id (call on rank 0)."""
+    buf = C.create_string_buffer(128)
+    _check(load().crsh_dist_unique_id(buf))
+    return buf.raw
 
 
-def merge_packed(packed, group=None):
-    """In-place element-wise MIN over ranks of an int64 tensor of packed hits."""
+def init(scene: Scene, uid: bytes, rank: int, world: int) -> None:
+    """crsh_dist_init: join `scene` to the world-`world` NCCL communicator of
+    `uid` as `rank` (collective). Later crsh_trace_secondary calls on this
+    scene trace this rank's share and merge the frame on every rank."""
+    if len(uid) != 128:
+        raise ValueError("an NCCL unique id is 128 bytes")
+    buf = C.create_string_buffer(bytes(uid), 128)
+    _check(load().crsh_dist_init(scene.handle, buf, int(rank), int(world)))
+
+
+def init_from_torch(scene: Scene, group=None) -> tuple[int, int]:
+    """crsh_dist_init with rank / world of the initialised torch.distributed
+    default (or given) group; rank 0's unique id is broadcast over it.
+    Returns (rank, world)."""
     import torch.distributed as dist
-    dist.all_reduce(packed, op=dist.ReduceOp.MIN, group=group)
-    return packed
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    init(scene, broadcast_uid(group), rank, world)
+    return rank, world
 
 
-def merge_counters(counters, group=None):
-    """Sum per-rank traversal counters (int64 tensor)."""
+def broadcast_uid(group=None) -> bytes:
+    """Rank 0's fresh NCCL unique id, received by every rank of the group."""
     import torch.distributed as dist
-    dist.all_reduce(counters, op=dist.ReduceOp.SUM, group=group)
-    return counters
+    obj = [unique_id() if dist.get_rank(group) == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    return obj[0]
 
 
-def decode_packed(packed: np.ndarray):
-    """packed int64 -> (hit_tri int32, t float32), the host mirror of
-    crsh_unpack_hits: EMPTY -> (-2, inf), MISS -> (-1, inf)."""
-    p = np.asarray(packed).astype(np.int64).view(np.uint64)
-    hit = (p & np.uint64(0xFFFFFFFF)).astype(np.int64).astype(np.int32)
-    t = (p >> np.uint64(32)).astype(np.uint32).view(np.float32).copy()
-    empty = p == np.uint64(PACK_EMPTY)
-    miss = (p >> np.uint64(32)) == np.uint64(0x7F800000)
-    hit[miss] = -1
-    hit[empty] = -2
-    t[empty | miss] = np.inf
-    return hit, t
-
-
-def encode_owned(hit_tri: np.ndarray, t: np.ndarray, owned: np.ndarray) -> np.ndarray:
-    """Host mirror of the packed encoding (for tests): owned hits/misses,
-    everything else EMPTY."""
-    out = np.full(hit_tri.shape, PACK_EMPTY, np.uint64)
-    hit = owned & (hit_tri >= 0)
-    miss = owned & (hit_tri == -1)
-    out[hit] = (t[hit].view(np.uint32).astype(np.uint64) << np.uint64(32)) | hit_tri[hit].astype(np.uint64)
-    out[miss] = np.uint64(PACK_MISS)
-    return out.view(np.int64)
+def merge_name(code: int) -> str:
+    return MERGE.get(code, str(code))

@@ -91,6 +91,7 @@ def test_packed_arithmetic_not_contracted():
     with tempfile.TemporaryDirectory() as d:
         ptx_path = os.path.join(d, "crsh.ptx")
         flags = [f for f in nb.FLAGS if f not in ("-shared", "-Xcompiler", "-fPIC", "-cudart", "static", "-lineinfo")]
+        flags += [f for f in nb.nccl_flags() if f.startswith("-I")]
         subprocess.check_call([nvcc, *flags, "-ptx", "-o", ptx_path, nb.SRC])
         ptx = open(ptx_path).read()
     sass = subprocess.run([cuobjdump, "-sass", lib], capture_output=True, text=True).stdout

@@ -11,7 +11,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2312_06538_b200 import dist as cd
+import host_mirror as cd
 
 
 def _frame():
@@ -123,3 +123,34 @@ def test_balanced_cut_partitions_and_balances(seed):
             assert int(work[lo:hi].sum()) <= tot / world + int(work.max(initial=0))
     assert [cd.balanced_cut(np.zeros(10), q, 3) for q in range(3)] == [(0, 3), (3, 6), (6, 10)]
     assert [cd.balanced_cut([5, 0, 0, 5], q, 2) for q in range(2)] == [(0, 1), (1, 4)]
+
+
+def _uid_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2312_06538_b200 import dist as crsh_dist
+    uid = crsh_dist.broadcast_uid()
+    q.put((rank, uid))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_nccl_unique_id_broadcast():
+    """crsh_dist_unique_id (libcrsh, no GPU needed) on rank 0, broadcast over a
+    world-2 gloo group: both ranks hold the same 128-byte NCCL id, the input of
+    crsh_dist_init on every rank."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_uid_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert len(got[0]) == 128 and got[0] == got[1] and any(got[0])

@@ -16,7 +16,7 @@ if not torch.cuda.is_available():
 import oracle  # noqa: E402
 import paper_2312_06538_b200 as crsh  # noqa: E402
 from paper_2312_06538_b200.api import tracer_for  # noqa: E402
-from paper_2312_06538_b200 import dist as cd  # noqa: E402
+import host_mirror as cd  # noqa: E402
 from workloads import make_micro, make_workload  # noqa: E402
 
 SEG = {0: oracle.SH, 1: oracle.RE, 2: oracle.RR}
@@ -109,13 +109,18 @@ def test_micro_scenes(seed):
     assert np.array_equal(hit[ok], bt)
 
 
+@pytest.mark.parametrize("item_tris", [None, "16384"])
 @pytest.mark.parametrize("levels,leaf,branch", [(1, 8, 8), (1, 64, 4), (3, 4, 4), (3, 16, 8), (4, 8, 8), (2, 32, 2),
                                                 (2, 2, 16)])
-def test_option_space_many_triangles(levels, leaf, branch):
+def test_option_space_many_triangles(levels, leaf, branch, item_tris, monkeypatch):
     """cfg2's 70k-triangle scene at 96x96 over the option space: work items
     of thousands of triangles (several slices per warp, queues refilled and
     drained many times), both the shared-memory (group <= 512 rays) and the
-    global-memory group paths (span > 512), Lv 1 (top = bundle level) to 4."""
+    global-memory group paths (span > 512), Lv 1 (top = bundle level) to 4;
+    with the per-frame item size (2048 triangles at this size) and with the
+    16384-triangle items of large frames forced (CRSH_ITEM_TRIS)."""
+    if item_tris:
+        monkeypatch.setenv("CRSH_ITEM_TRIS", item_tris)
     w = make_workload(2, width=96, height=96, levels=levels, leaf_size=leaf, branching=branch)
     tr, hit, t, ref = run_both(w, crsh.F_SORT | crsh.F_MESH_CULL, taps=False)
     assert np.array_equal(hit, ref["hit_tri"]) and np.array_equal(t.view(np.uint32), ref["t"].view(np.uint32))
@@ -133,79 +138,7 @@ def test_cfg2_full_parity(flags):
     assert_taps_equal(tr, ref, w)
 
 
-def test_cfg3_sampled_vs_brute():
-    """cfg3 (1024x1024 SH+RE+RR, ~250k tris / 30 meshes) in the bench's launch
-    configuration: 4096 sampled rays against N x M brute force (oracle)."""
-    w = make_workload(3)
-    tr = tracer_for(w, flags=7)
-    tr.run()
-    hit, t = tr.results()
-    prep = oracle.ScenePrep(w.tris, w.mesh_ids)
-    rays, keys, empty = oracle.generate(w, prep, 7)
-    ok = np.flatnonzero(empty == 0)
-    rng = np.random.default_rng(3)
-    pick = rng.choice(ok, size=4096, replace=False)
-    bt, btt = oracle.unpack(oracle.brute(rays[pick], prep))
-    assert np.array_equal(hit[pick], bt) and np.array_equal(t[pick].view(np.uint32), btt.view(np.uint32))
-    assert np.all(hit[empty == 1] == -2)
-    st = crsh.stats(tr.scene)
-    for seg in range(3):
-        for k in range(1, 3):
-            assert st["tests"][seg][k] >= st["hits"][seg][k]
-        assert st["tests"][seg][1] <= 8 * st["hits"][seg][2]          # monotone culling (S:470)
-        assert st["final_tests"][seg] <= 8 * st["hits"][seg][1]
-
-
-@pytest.mark.parametrize("cfg,flags,n_pick", [(3, 3, 2048), (4, 7, 512), (4, 3, 256)])
-def test_large_configs_sampled_vs_brute(cfg, flags, n_pick):
-    """cfg3 with the R6 layout and cfg4 (1920x1080, 4 lights, ~1M triangles in
-    100 meshes; both layouts) at full size: sampled rays against N x M brute
-    force, every empty slot -2, monotone per-level culling."""
-    w = make_workload(cfg)
-    tr = tracer_for(w, flags=flags)
-    tr.run()
-    hit, t = tr.results()
-    prep = oracle.ScenePrep(w.tris, w.mesh_ids)
-    rays, keys, empty = oracle.generate(w, prep, flags)
-    ok = np.flatnonzero(empty == 0)
-    pick = np.random.default_rng(cfg + flags).choice(ok, size=n_pick, replace=False)
-    bt, btt = oracle.unpack(oracle.brute(rays[pick], prep))
-    assert np.array_equal(hit[pick], bt) and np.array_equal(t[pick].view(np.uint32), btt.view(np.uint32))
-    assert np.all(hit[empty == 1] == -2)
-    st = crsh.stats(tr.scene)
-    assert sum(st["rays"]) == len(ok)
-    for seg in range(3):
-        assert st["tests"][seg][1] <= 8 * st["hits"][seg][2] and st["final_tests"][seg] <= 8 * st["hits"][seg][1]
-
-
-@pytest.mark.gpu
-@pytest.mark.parametrize("flags", [3, 7])
-def test_cfg3_top_level_work_exact(flags):
-    """cfg3 at full size in the bench's launch configuration (hundreds of
-    thousands of work items, handed out in chunks of consecutive items):
-    every (top node, triangle of a mesh the node kept) pair is tested exactly
-    once -- the top-level test count equals the sum over the GPU's top nodes
-    of the triangles of the meshes whose sphere passes Eq 9 (the oracle's
-    cull), and the mesh tests / passes equal that count too (a
-    skipped or twice-processed work item would break the first identity)."""
-    w = make_workload(3)
-    tr = tracer_for(w, flags=flags)
-    tr.run()
-    st = crsh.stats(tr.scene)
-    prep = oracle.ScenePrep(w.tris, w.mesh_ids)
-    counts = (prep.mesh_range[:, 1] - prep.mesh_range[:, 0])[:prep.n_meshes]
-    live = np.flatnonzero(counts > 0)
-    for seg, _, _ in oracle.segments(w.P, w.lights.shape[0], w.ray_types):
-        top = crsh.debug_tap(tr.scene, crsh.TAP_NODES, seg, w.levels)
-        work = mh = 0
-        for node in top:
-            for m in live:
-                if oracle.cull(node, prep.mesh_sph[m]):
-                    mh += 1
-                    work += int(counts[m])
-        assert st["mesh_tests"][seg] == len(top) * len(live), seg
-        assert st["mesh_hits"][seg] == mh, (seg, st["mesh_hits"][seg], mh)
-        assert st["tests"][seg][w.levels] == work, (seg, st["tests"][seg][w.levels], work)
+# cfg3 / cfg4 at full size: tests/test_gpu_headline.py (full-frame oracle parity)
 
 
 def test_slot_limit_and_degenerate_triangles():
@@ -249,19 +182,32 @@ def test_edge_cases():
     assert np.array_equal(hit, ref["hit_tri"])
 
 
-def test_sharded_equals_single():
+def _oracle_packed(ref):
+    """The oracle frame in the packed encoding of include/crsh.h (world 1:
+    every slot owned): hit (float_bits(t) << 32) | tri, miss
+    0x7F800000FFFFFFFF, no ray 0x7FFFFFFFFFFFFFFF."""
+    h, t = ref["hit_tri"], ref["t"]
+    out = np.full(h.shape, 0x7FFFFFFFFFFFFFFF, np.uint64)
+    hit = h >= 0
+    out[hit] = (t[hit].view(np.uint32).astype(np.uint64) << np.uint64(32)) | h[hit].astype(np.uint64)
+    out[h == -1] = np.uint64(0x7F800000FFFFFFFF)
+    return out.view(np.int64)
+
+
+def test_sharded_equals_oracle():
     """Hash-range sharding: the min-merge of the per-rank packed
-    results equals the single-GPU result, and the per-rank counters sum to the
-    single-GPU counters (here the ranks run one after another on one GPU)."""
+    results equals the ORACLE's frame, and the per-rank counters sum to the
+    oracle's counters (the ranks run one after another on one GPU; no rank
+    waits on another)."""
     w = make_workload(2, width=256, height=256)
-    tr = tracer_for(w)
-    tr.run()
-    hit1, t1 = tr.results()
-    st1 = tr.stats()
+    ref = oracle.trace(w)
+    rs = ref["stats"]
     Lv = w.levels
     for world in (2, 3, 8):
         merged = None
         tsum = np.zeros((3, 9), np.uint64)
+        hsum = np.zeros((3, 9), np.uint64)
+        fsum = np.zeros(3, np.uint64)
         msum = np.zeros(3, np.uint64)
         top = []
         for rank in range(world):
@@ -271,6 +217,8 @@ def test_sharded_equals_single():
             merged = packed.clone() if merged is None else torch.minimum(merged, packed)
             st = trr.stats()
             tsum += st["tests"]
+            hsum += st["hits"]
+            fsum += np.asarray(st["final_tests"], np.uint64)
             msum += np.asarray(st["mesh_tests"], np.uint64)
             top.append(int(st["tests"][:, Lv].sum()))
             # the device cut equals the host mirror on the device's group work,
@@ -281,9 +229,11 @@ def test_sharded_equals_single():
             assert top[-1] == int(work[lo:hi].sum())
         trr.unpack(merged)
         hit, t = trr.results()
-        assert np.array_equal(hit, hit1) and np.array_equal(t, t1)
-        assert np.array_equal(tsum, st1["tests"])
-        assert np.array_equal(msum, np.asarray(st1["mesh_tests"], np.uint64))
+        assert np.array_equal(merged.cpu().numpy(), _oracle_packed(ref)), world
+        assert np.array_equal(hit, ref["hit_tri"]) and np.array_equal(t.view(np.uint32), ref["t"].view(np.uint32))
+        assert np.array_equal(tsum, rs["tests"]) and np.array_equal(hsum, rs["hits"]), world
+        assert np.array_equal(fsum, np.asarray(rs["final_tests"], np.uint64)), world
+        assert np.array_equal(msum, np.asarray(rs["mesh_tests"], np.uint64)), world
         # work-balanced cut: every rank's top-level tests within one group's
         # worth (K top nodes x the scene) of an equal share
         share = sum(top) / world
@@ -291,34 +241,33 @@ def test_sharded_equals_single():
         assert min(top) > 0, (world, top)
 
 
-def test_peer_store_equals_single():
+def test_peer_store_equals_oracle():
     """Fused multi-GPU epilogue (crsh_trace_secondary_peer): each rank stores
     its owned results into every destination (here two buffers on this GPU
     standing for the own and a peer's window; the ranks run one after another,
-    none waits on another). Both destinations must equal the single-rank
-    packed frame, though they start as garbage: every slot is written exactly
-    once with its final value, so no reduction is needed."""
+    none waits on another). Both destinations must equal the oracle's frame in
+    the packed encoding, though they start as garbage: every slot is written
+    exactly once with its final value, so no reduction is needed."""
     w = make_workload(2, width=256, height=256)
-    tr = tracer_for(w)
-    ref = torch.empty(tr.slots, dtype=torch.int64, device="cuda")
-    tr.run_packed(ref)   # world 1: every slot owned
-    st1 = tr.stats()
+    ref = oracle.trace(w)
+    want = torch.as_tensor(_oracle_packed(ref)).cuda()
+    slots = len(ref["hit_tri"])
     for world in (1, 2, 5):
-        dst = [torch.full((tr.slots,), 0x5A5A5A5A5A5A5A5A, dtype=torch.int64, device="cuda") for _ in range(2)]
+        dst = [torch.full((slots,), 0x5A5A5A5A5A5A5A5A, dtype=torch.int64, device="cuda") for _ in range(2)]
         tsum = np.zeros((3, 9), np.uint64)
         for rank in range(world):
             trr = tracer_for(w, shard_rank=rank, shard_world=world)
             trr.run_peer([d.data_ptr() for d in dst])
             tsum += trr.stats()["tests"]
         torch.cuda.synchronize()
-        assert torch.equal(dst[0], ref) and torch.equal(dst[1], ref), world
-        assert np.array_equal(tsum, st1["tests"]), world
+        assert torch.equal(dst[0], want) and torch.equal(dst[1], want), world
+        assert np.array_equal(tsum, ref["stats"]["tests"]), world
     # brute-force engine through the same epilogue
     trb = tracer_for(w, flags=crsh.F_BRUTE)
     d = torch.full((trb.slots,), -1, dtype=torch.int64, device="cuda")
     trb.run_peer([d.data_ptr()])
     torch.cuda.synchronize()
-    assert torch.equal(d, ref)
+    assert torch.equal(d, want)
 
 
 def test_host_variant_and_determinism():
@@ -500,13 +449,17 @@ def test_dynamic_scene_parity(cfg, seed):
         assert_counts_equal(crsh.stats(scene), ref)
 
 
+@pytest.mark.parametrize("item_tris", [None, "16384"])
 @pytest.mark.parametrize("levels,leaf,branch,lights", [(2, 64, 32, 3), (8, 2, 2, 1), (5, 4, 4, 16), (1, 2, 2, 16),
                                                        (6, 8, 2, 2)])
-def test_option_extremes(levels, leaf, branch, lights):
+def test_option_extremes(levels, leaf, branch, lights, item_tris, monkeypatch):
     """Extremes of the option space: the widest bundles and nodes (B0 64,
     B 32: span 2048 > 512 rays, K = 1, global-memory groups), the deepest
     hierarchy (Lv 8 of binary nodes), 16 lights (the hash's 4-bit light
-    field), Lv 1 with 16 lights; hits, counts and every tap bit-exact."""
+    field), Lv 1 with 16 lights; hits, counts and every tap bit-exact; also
+    with the large frames' 16384-triangle work items forced."""
+    if item_tris:
+        monkeypatch.setenv("CRSH_ITEM_TRIS", item_tris)
     w = make_workload(1, width=40, height=36, levels=levels, leaf_size=leaf, branching=branch, ray_types=1)
     r = np.random.default_rng(lights)
     w.lights = np.stack([r.uniform(1, 9, lights), r.uniform(8.5, 9.5, lights), r.uniform(1, 9, lights)], 1).astype(np.float32)
@@ -535,3 +488,25 @@ def test_api_errors():
     tr.run()   # the scene is still usable
     hit, _ = tr.results()
     assert np.array_equal(hit, oracle.trace(w)["hit_tri"])
+
+
+def test_transform_waits_for_inflight_frame():
+    """crsh_scene_transform is synchronous with respect to frames still in
+    flight: a frame traced on a non-blocking stream and a transform issued
+    right after it, with no host synchronisation in between, gives the frame
+    of the UNMOVED scene (the oracle's), and the next frame the moved one."""
+    w = make_workload(2, width=192, height=192)
+    ref0 = oracle.trace(w)
+    tr = tracer_for(w)
+    side = torch.cuda.Stream()
+    n_m = int(w.mesh_ids.max()) + 1
+    X = np.tile(np.array([1, 0, 0, 0.5, 0, 1, 0, 0, 0, 0, 1, 0], np.float32), (n_m, 1))
+    with torch.cuda.stream(side):
+        for _ in range(3):   # several frames queued so the transform lands while they run
+            tr.run(side)
+        crsh.scene_transform(tr.scene, X)
+    hit, t = tr.results()
+    assert np.array_equal(hit, ref0["hit_tri"]) and np.array_equal(t.view(np.uint32), ref0["t"].view(np.uint32))
+    tr.run()
+    hit1, _ = tr.results()
+    assert not np.array_equal(hit1, ref0["hit_tri"])

@@ -78,6 +78,70 @@ def test_mt_vs_plane_then_barycentric(orc):
     assert checked > 4000
 
 
+def test_mt_vs_divide_first_moller_trumbore(orc):
+    """R15 pin: the oracle's sign-folded, division-deferred decision order
+    against an independent float32 transcription of the textbook two-sided
+    Moller-Trumbore (MT97's non-culling branch: inv_det = 1/det first, then
+    u = (T.P) inv_det in [0, 1], v = (D.Q) inv_det >= 0, u + v <= 1,
+    t = (E2.Q) inv_det), written here with numpy's plain float32 dot products
+    (no fma), and both against the same quantities in fp64.  On 2*10^4 random
+    pairs away from the barycentric edges (u, v, 1-u-v all > 1e-4 in fp64) and
+    from tmin: (1) both orders accept exactly the pairs fp64 accepts; (2) t of
+    the two float32 orders agree within 1e-5 relative (the north-star bar) on
+    >= 99.5 % of hits -- the rest are ill-conditioned pairs (cancellation in
+    E2.Q) where both are off; (3) the oracle's order is no less accurate than
+    divide-first: its 99th/99.9th-percentile relative error against fp64 is at
+    most divide-first's."""
+    r = np.random.default_rng(97)
+    n = 20000
+    V = r.normal(size=(n, 3, 3)).astype(np.float32)
+    o = (r.normal(size=(n, 3)) * 2).astype(np.float32)
+    w = r.dirichlet([1, 1, 1], size=n)
+    target = np.where(r.uniform(size=(n, 1)) < 0.6, np.einsum("nk,nkj->nj", w, V.astype(np.float64)),
+                      r.normal(size=(n, 3)))
+    d = target - o
+    d = (d / np.linalg.norm(d, axis=1, keepdims=True)).astype(np.float32)
+    f = np.float32
+    e1, e2 = V[:, 1] - V[:, 0], V[:, 2] - V[:, 0]
+    tv = o - V[:, 0]
+
+    def dot(a, b):
+        return (a[:, 0] * b[:, 0] + a[:, 1] * b[:, 1] + a[:, 2] * b[:, 2]).astype(np.float32)
+
+    with np.errstate(divide="ignore", invalid="ignore", over="ignore"):
+        p = np.cross(d, e2).astype(np.float32)
+        det = dot(e1, p)
+        inv = (f(1) / det).astype(np.float32)
+        u = dot(tv, p) * inv
+        q = np.cross(tv, e1).astype(np.float32)
+        v = dot(d, q) * inv
+        t = dot(e2, q) * inv
+        # the same quantities in fp64 on the float32 inputs
+        D, E1, E2, TV = (a.astype(np.float64) for a in (d, e1, e2, tv))
+        P64 = np.cross(D, E2)
+        DET = (E1 * P64).sum(1)
+        Q64 = np.cross(TV, E1)
+        U, V64, T = (TV * P64).sum(1) / DET, (D * Q64).sum(1) / DET, (E2 * Q64).sum(1) / DET
+    tmin = f(1e-4)
+    hit = (det != 0) & (u >= 0) & (u <= 1) & (v >= 0) & (u + v <= 1) & (t > tmin)
+    hit64 = (U >= 0) & (V64 >= 0) & (U + V64 <= 1) & (T > 1e-4)
+    clear = (DET != 0) & (np.minimum(np.minimum(np.abs(U), np.abs(V64)), np.abs(1 - U - V64)) > 1e-4) & \
+        (np.abs(T - 1e-4) > 1e-4) & np.isfinite(T)
+    checked, e_or, e_df, agree = 0, [], [], []
+    for k in np.flatnonzero(clear):
+        got = orc.mt([*o[k], tmin, *d[k], np.inf], np.concatenate([V[k, 0], e1[k], e2[k]]))
+        assert (got is not None) == bool(hit64[k]) == bool(hit[k]), (k, U[k], V64[k], T[k])
+        if got is not None:
+            e_or.append(abs(got - T[k]) / T[k])
+            e_df.append(abs(float(t[k]) - T[k]) / T[k])
+            agree.append(abs(got - float(t[k])) <= 1e-5 * abs(float(t[k])))
+        checked += 1
+    assert checked > 15000 and len(e_or) > 5000
+    assert np.mean(agree) >= 0.995
+    for qq in (0.99, 0.999):
+        assert np.quantile(e_or, qq) <= np.quantile(e_df, qq), qq
+
+
 # ----------------------------------------------------------------- spheres
 def brute_min_sphere(P):
     """Combinatorial minimal enclosing sphere: all spheres with 1..4 boundary

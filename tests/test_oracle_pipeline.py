@@ -231,9 +231,12 @@ def test_generate_closed_forms(orc):
 
 # ----------------------------------------------------------------- end to end
 def brute_np(rays, tris):
-    """Independent fp64 closest-hit reference (plane + edge functions)."""
+    """Independent fp64 closest-hit reference (plane + edge functions).  Per ray:
+    (best triangle or -1, its t, the runner-up t, the best hit's smallest
+    normalised edge distance)."""
     V = tris.reshape(-1, 3, 3).astype(np.float64)
     n = np.cross(V[:, 1] - V[:, 0], V[:, 2] - V[:, 0])
+    area = np.linalg.norm(n, axis=1)
     out = []
     for r in rays.astype(np.float64):
         o, d, tmin, tmax = r[:3], r[4:7], r[3], r[7]
@@ -241,30 +244,43 @@ def brute_np(rays, tris):
         with np.errstate(divide="ignore", invalid="ignore"):
             t = ((V[:, 0] - o) * n).sum(1) / den
             p = o + t[:, None] * d
-            e = [np.einsum("ij,ij->i", np.cross(V[:, (k + 1) % 3] - V[:, k], p - V[:, k]), n) for k in range(3)]
+            e = [np.einsum("ij,ij->i", np.cross(V[:, (k + 1) % 3] - V[:, k], p - V[:, k]), n) / area
+                 for k in range(3)]
         inside = ((e[0] >= 0) & (e[1] >= 0) & (e[2] >= 0)) | ((e[0] <= 0) & (e[1] <= 0) & (e[2] <= 0))
         ok = inside & (t > tmin) & (t < tmax) & (den != 0)
-        out.append((np.argmin(np.where(ok, t, np.inf)), np.where(ok, t, np.inf).min()) if ok.any() else (-1, np.inf))
+        tt = np.where(ok, t, np.inf)
+        if not ok.any():
+            out.append((-1, np.inf, np.inf, np.inf))
+            continue
+        order = np.argsort(tt)
+        b = order[0]
+        second = tt[order[1]] if len(order) > 1 else np.inf
+        margin = min(abs(e[k][b]) for k in range(3)) / np.sqrt(area[b])
+        out.append((int(b), tt[b], second, margin))
     return out
 
 
 def test_brute_matches_fp64_reference(orc):
     """The oracle's brute force (float32 MT) agrees with an independent fp64
-    closest-hit computation except where two candidate hits are within 1e-4."""
+    closest-hit computation: the same triangle for every ray whose fp64 hit is
+    clear (runner-up more than 1e-4 farther, hit point more than 1e-4 from the
+    triangle's edges), t within 1e-4, and the same hit/miss verdict on >= 97 %
+    of all rays (the rest graze an edge)."""
     w = make_micro(11, n_tris=48, W=8, H=8)
     prep = orc.ScenePrep(w.tris, w.mesh_ids)
     rays, keys, empty = orc.generate(w, prep)
     rays = rays[empty == 0]
     tri, t = orc.unpack(orc.brute(rays, prep))
     ref = brute_np(rays, w.tris)
-    agree = 0
-    for k, (rt, rtt) in enumerate(ref):
-        if rt == -1:
-            agree += tri[k] == -1 or True   # grazing/edge hits may differ; checked below on t
+    clear = 0
+    for k, (rt, rtt, second, margin) in enumerate(ref):
+        if rt >= 0 and second - rtt > 1e-4 and margin > 1e-4:
+            assert tri[k] == rt, (k, tri[k], rt)
+            assert t[k] == pytest.approx(rtt, rel=1e-4, abs=1e-4)
+            clear += 1
         if rt >= 0 and tri[k] >= 0:
             assert t[k] == pytest.approx(rtt, rel=1e-4, abs=1e-4)
-            agree += 1
-    assert sum(1 for r in ref if r[0] >= 0) > 20
+    assert clear > 20
     assert np.mean([(r[0] >= 0) == (tri[k] >= 0) for k, r in enumerate(ref)]) > 0.97
 
 
