@@ -188,7 +188,7 @@ def oracle_sample(w, flags, target_s=12.0):
     rows = 1
     while True:
         rays, dt = oracle_band(w, flags, rows, prep)
-        if dt >= target_s / 4 or rows >= w.height:
+        if dt >= target_s / 2 or rows >= w.height:
             return rays, dt, rows, oracle.default_threads()
         rows = min(w.height, max(rows + 1, int(rows * min(8.0, target_s / max(dt, 1e-3)))))
 
