@@ -102,6 +102,9 @@ constexpr int SORT_PASSES = 32 / RADIX_BITS;
 // k_onesweep at 3 CTAs per SM (80 registers, no spills; 141 registers and 2
 // CTAs per SM without the bound): A/B at cfg4 sort 0.44 -> 0.41 ms; 4 CTAs
 // (64 registers) spill and are slower, as are 16/32-word look-back batches
+#ifndef CRSH_SORT_MATCH
+#define CRSH_SORT_MATCH 0   // 1: rank with __match_any_sync (round 1); 0: ballot-based peer masks
+#endif
 #ifndef CRSH_SORT_MINB
 #define CRSH_SORT_MINB 3
 #endif
@@ -203,8 +206,23 @@ __global__ void __launch_bounds__(SORT_THREADS, CRSH_SORT_MINB) k_onesweep(const
   for (int it = 0; it < SORT_ITEMS; ++it) {
     const uint32_t idx = wbase + it * 32 + lane;
     const bool ok = idx < n;
+#if CRSH_SORT_MATCH
     const uint32_t d = ok ? ((k[it] >> shift) & 255u) : 0x100u + lane;   // invalid lanes never match
     const uint32_t peers = __match_any_sync(CRSH_FULL, d);
+#else
+    // lanes with the same digit from RADIX_BITS ballots (short-latency votes;
+    // MATCH.ANY's latency was the stall of the ranking loop, ncu r2: sort at
+    // cfg4 0.409 -> 0.359 ms, cfg2 59.4 -> 56.0 us); invalid lanes (tile
+    // tail) are masked out of every valid lane's peers
+    const uint32_t d = (k[it] >> shift) & 255u;
+    uint32_t peers = __ballot_sync(CRSH_FULL, ok);
+#pragma unroll
+    for (int bit = 0; bit < RADIX_BITS; ++bit) {
+      const bool on = (d >> bit) & 1u;
+      const uint32_t bb = __ballot_sync(CRSH_FULL, on);
+      peers &= on ? bb : ~bb;
+    }
+#endif
     const uint32_t leader = __ffs(peers) - 1;
     uint32_t base = 0;
     if (ok && lane == leader) {
