@@ -23,6 +23,8 @@ CXXFLAGS = ["-O2", "-std=c++17", "-ffp-contract=off", "-fno-fast-math", "-fPIC",
 
 SH, RE, RR = 1, 2, 4
 F_SORT, F_MESH_CULL, F_ZORDER = 1, 2, 4
+F_OBJTREE = 64        # object sphere-tree below the mesh spheres (NEXT-4)
+CLUSTER_TRIS = 32     # triangles per object-tree cluster (reading O1)
 UINT64_MAX = np.uint64(0xFFFFFFFFFFFFFFFF)
 
 
@@ -91,7 +93,9 @@ def lib():
         L.or_build_upper.restype = C.c_int64
         L.or_build_upper.argtypes = [C.c_int64, vp, C.c_int32, vp]
         L.or_traverse.argtypes = [C.c_int32, C.c_int32, C.c_int32, vp, vp, C.c_int64, vp, vp, vp, C.c_int32, vp,
-                                  vp, C.c_uint32, C.c_int32, vp, vp]
+                                  vp, C.c_uint32, C.c_int32, vp, vp, vp, vp, C.c_int32, vp]
+        L.or_cluster_spheres.restype = C.c_int64
+        L.or_cluster_spheres.argtypes = [vp, vp, C.c_int32, C.c_int32, C.c_float, vp, vp, vp, vp]
         L.or_brute.argtypes = [C.c_int64, vp, C.c_int64, vp, C.c_int32, vp]
         L.or_mesh_cull.restype = None
         L.or_mesh_cull.argtypes = [C.c_int64, vp, C.c_int32, vp, vp, vp]
@@ -177,7 +181,7 @@ def miniball(points):
 
 
 class ScenePrep:
-    def __init__(self, tris, mesh_ids, pad=None, eps_t=None, mesh_sph=None):
+    def __init__(self, tris, mesh_ids, pad=None, eps_t=None, mesh_sph=None, cluster_order=None):
         tris = _f32(tris).reshape(-1, 9)
         mesh_ids = np.ascontiguousarray(mesh_ids, np.int32)
         M = tris.shape[0]
@@ -195,6 +199,16 @@ class ScenePrep:
                                  _p(ms_in) if ms_in is not None else None)
         if rc != 0:
             raise ValueError("mesh ids must be non-decreasing and dense from 0")
+        # object sphere-tree clusters (NEXT-4, reading O1)
+        self.cluster_sph = np.zeros((max(M, 1), 4), np.float32)
+        self.mesh_cluster_first = np.zeros(max(n_meshes, 1) + 1, np.int64)
+        self.cluster_order = np.zeros(max(M, 1), np.int32)
+        oin = np.ascontiguousarray(cluster_order, np.int32) if cluster_order is not None else None
+        nc = lib().or_cluster_spheres(_p(tris), _p(self.mesh_range), n_meshes, CLUSTER_TRIS, float(self.consts[6]),
+                                      _p(oin) if oin is not None else None, _p(self.cluster_order),
+                                      _p(self.cluster_sph), _p(self.mesh_cluster_first))
+        self.cluster_sph = self.cluster_sph[:max(nc, 1)].copy()
+        self.n_clusters = int(nc)
         self.box_min = self.consts[0:3].copy()
         self.box_max = self.consts[3:6].copy()
         self.box_ext = (self.box_max - self.box_min).astype(np.float32)
@@ -279,14 +293,15 @@ def build_levels(sorted_rays, Lv, B0, B):
 def traverse(levels, sorted_rays, prep: ScenePrep, Lv, B0, B, flags, n_threads=None):
     n = sorted_rays.shape[0]
     best = np.full(max(n, 1), UINT64_MAX, np.uint64)
-    cnt = np.zeros(20, np.uint64)
+    cnt = np.zeros(22, np.uint64)
     if n == 0:
         return best[:0], cnt
     ptrs = (vp * Lv)(*[lv.ctypes.data_as(vp) for lv in levels])
     counts = np.array([lv.shape[0] for lv in levels], np.int64)
     lib().or_traverse(Lv, B0, B, ptrs, _p(counts), n, _p(_f32(sorted_rays)), _p(prep.tri_e), _p(prep.tri_sph),
                       prep.n_meshes, _p(prep.mesh_sph), _p(prep.mesh_range), flags,
-                      n_threads or default_threads(), _p(best), _p(cnt))
+                      n_threads or default_threads(), _p(best), _p(cnt), _p(prep.cluster_sph),
+                      _p(prep.mesh_cluster_first), CLUSTER_TRIS, _p(prep.cluster_order))
     return best[:n], cnt
 
 
@@ -396,7 +411,8 @@ def _trace_core(rays, keys, empty, segs, prep: ScenePrep, Lv, B0, B, flags, n_th
     t_out = np.full(S, np.inf, np.float32)
     stats = dict(rays=[0, 0, 0], slots=[0, 0, 0], chunks=[0, 0, 0], tests=np.zeros((3, 9), np.uint64),
                  hits=np.zeros((3, 9), np.uint64), mesh_tests=[0, 0, 0], mesh_hits=[0, 0, 0],
-                 final_tests=[0, 0, 0], final_hits=[0, 0, 0], rays_hit=[0, 0, 0], brute=[0, 0, 0])
+                 final_tests=[0, 0, 0], final_hits=[0, 0, 0], rays_hit=[0, 0, 0], brute=[0, 0, 0],
+                 cluster_tests=[0, 0, 0], cluster_hits=[0, 0, 0])
     tap = dict(keys=[], vals=[], ckey=[], cbase=[], skey=[], sslot=[], levels=[])
     # trimming over the whole slot array keeps slot order, so each
     # segment's survivors stay contiguous.
@@ -431,6 +447,7 @@ def _trace_core(rays, keys, empty, segs, prep: ScenePrep, Lv, B0, B, flags, n_th
             stats["hits"][seg, kk + 1] = cnt[8 + kk]
         stats["mesh_tests"][seg], stats["mesh_hits"][seg] = int(cnt[16]), int(cnt[17])
         stats["final_tests"][seg], stats["final_hits"][seg] = int(cnt[18]), int(cnt[19])
+        stats["cluster_tests"][seg], stats["cluster_hits"][seg] = int(cnt[20]), int(cnt[21])
         tri, tt = unpack(best)
         hit_tri[sv.astype(np.int64)] = tri
         t_out[sv.astype(np.int64)] = tt
@@ -541,4 +558,5 @@ def transformed_prep(prep0: ScenePrep, tris0, mesh_ids, xforms):
     tris = transform_tris(tris0, mesh_ids, xforms)
     ms = np.stack([update_sphere(prep0.mesh_sph[m], xforms[m]) for m in range(prep0.n_meshes)]) \
         if prep0.n_meshes else np.zeros((1, 4), np.float32)
-    return ScenePrep(tris, mesh_ids, pad=prep0.pad, eps_t=prep0.eps_t, mesh_sph=ms), tris
+    return ScenePrep(tris, mesh_ids, pad=prep0.pad, eps_t=prep0.eps_t, mesh_sph=ms,
+                     cluster_order=prep0.cluster_order), tris

@@ -366,10 +366,12 @@ Ball mtf_mb(std::vector<D3>& L, size_t end, D3* R, int k) {
 struct Counters {   // per (segment) traversal counters, §4.1, Tables 1-3
   uint64_t tests[9] = {0}, hits[9] = {0};
   uint64_t mesh_tests = 0, mesh_hits = 0, final_tests = 0, final_hits = 0;
+  uint64_t cluster_tests = 0, cluster_hits = 0;   // object sphere-tree level (NEXT-4)
   void add(const Counters& o) {
     for (int k = 0; k < 9; ++k) { tests[k] += o.tests[k]; hits[k] += o.hits[k]; }
     mesh_tests += o.mesh_tests; mesh_hits += o.mesh_hits;
     final_tests += o.final_tests; final_hits += o.final_hits;
+    cluster_tests += o.cluster_tests; cluster_hits += o.cluster_hits;
   }
 };
 
@@ -669,12 +671,87 @@ EXPORT int64_t or_build_upper(int64_t n_children, const float* children, int32_t
  * receives min over packed (t, tri). counters out (uint64):
  * [tests[1..8], hits[1..8], mesh_tests, mesh_hits, final_tests, final_hits]
  * -> tests[k] at out[k-1], hits[k] at out[8+k-1], then 16..19. */
+/* Object sphere-tree ("combine our coherent ray
+ * hierarchy with a deeper object hierarchy"), reading O1: below
+ * each mesh sphere, the mesh's triangles are ordered by the 30-bit Morton code
+ * of their centroid (((v0 + v1) + v2) / 3 in double) quantised to 1024 cells
+ * per axis of the mesh's vertex bounding box (q = floor(((c - lo) / (hi - lo))
+ * * 1024) clamped to [0, 1023], 0 on a flat axis), ties by triangle index, and
+ * cut into clusters of CL consecutive triangles of that order (the last one of
+ * a mesh may be shorter). A cluster is bounded by the sphere centred at the
+ * midpoint of its vertices' bounding box (double, rounded to float) with
+ * radius = the largest distance from that float centre to a vertex (double,
+ * rounded up) + pad -- the triangle spheres' finalisation. order_in (nullable):
+ * a given order (a moved scene keeps its creation-time order, reading G2);
+ * out_order [M]: the order (triangle ids, mesh by mesh); out_sph [clusters][4];
+ * mesh_cluster_first [n_meshes + 1]. Returns the number of clusters. */
+EXPORT int64_t or_cluster_spheres(const float* tris, const int64_t* mesh_range, int32_t n_meshes, int32_t CL, float pad,
+                                  const int32_t* order_in, int32_t* out_order, float* out_sph,
+                                  int64_t* mesh_cluster_first) {
+  auto spread3 = [](uint64_t v) {   // 10 bits -> every third bit
+    uint64_t r = 0;
+    for (int b = 0; b < 10; ++b) r |= ((v >> b) & 1ull) << (3 * b);
+    return r;
+  };
+  int64_t nc = 0;
+  for (int32_t m = 0; m < n_meshes; ++m) {
+    mesh_cluster_first[m] = nc;
+    const int64_t t0 = mesh_range[2 * m], t1 = mesh_range[2 * m + 1];
+    if (order_in) {
+      for (int64_t t = t0; t < t1; ++t) out_order[t] = order_in[t];
+    } else {
+      double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+      for (int64_t i = 9 * t0; i < 9 * t1; ++i) {
+        lo[i % 3] = std::min(lo[i % 3], (double)tris[i]);
+        hi[i % 3] = std::max(hi[i % 3], (double)tris[i]);
+      }
+      std::vector<std::pair<uint64_t, int64_t>> key;
+      for (int64_t t = t0; t < t1; ++t) {
+        uint64_t code = 0;
+        for (int k = 0; k < 3; ++k) {
+          const float* v = tris + 9 * t;
+          const double c = (((double)v[k] + (double)v[3 + k]) + (double)v[6 + k]) / 3.0;
+          uint64_t q = 0;
+          if (hi[k] > lo[k]) {
+            const double u = std::floor(((c - lo[k]) / (hi[k] - lo[k])) * 1024.0);
+            q = u <= 0.0 ? 0 : (u >= 1023.0 ? 1023 : (uint64_t)u);
+          }
+          code |= spread3(q) << (2 - k);   // x highest
+        }
+        key.push_back({code, t});
+      }
+      std::sort(key.begin(), key.end());   // (code, index): ties by triangle index
+      for (int64_t i = 0; i < (int64_t)key.size(); ++i) out_order[t0 + i] = (int32_t)key[i].second;
+    }
+    for (int64_t c0 = t0; c0 < t1; c0 += CL) {
+      const int64_t c1 = std::min<int64_t>(c0 + CL, t1);
+      std::vector<D3> pts;
+      double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+      for (int64_t i = c0; i < c1; ++i)
+        for (int v = 0; v < 3; ++v) {
+          const float* p = tris + 9 * (int64_t)out_order[i] + 3 * v;
+          pts.push_back(D3{p[0], p[1], p[2]});
+          const double q[3] = {p[0], p[1], p[2]};
+          for (int k = 0; k < 3; ++k) { lo[k] = std::min(lo[k], q[k]); hi[k] = std::max(hi[k], q[k]); }
+        }
+      const D3 c = {(lo[0] + hi[0]) * 0.5, (lo[1] + hi[1]) * 0.5, (lo[2] + hi[2]) * 0.5};
+      finalize_sphere(c, pts.data(), pts.size(), out_sph + 4 * nc);
+      out_sph[4 * nc + 3] += pad;
+      ++nc;
+    }
+  }
+  mesh_cluster_first[n_meshes] = nc;
+  return nc;
+}
+
 EXPORT void or_traverse(int32_t Lv, int32_t B0, int32_t B, const float* const* level_nodes,
                         const int64_t* level_count, int64_t n_rays, const float* rays, const float* tri_e,
                         const float* tri_sph, int32_t n_meshes, const float* mesh_sph,
                         const int64_t* mesh_range, uint32_t flags, int32_t n_threads, uint64_t* best,
-                        uint64_t* counters_out) {
+                        uint64_t* counters_out, const float* cluster_sph, const int64_t* mesh_cluster_first,
+                        int32_t CL, const int32_t* cluster_order) {
   const bool mesh_cull = (flags & 2u) != 0;
+  const bool objtree = (flags & 64u) != 0 && cluster_sph && cluster_order && CL > 0;   // CRSH_F_OBJTREE
   const int64_t n_top = level_count[Lv - 1];
   std::atomic<int64_t> next{0};
   std::vector<Counters> per_thread(std::max(1, n_threads));
@@ -718,13 +795,31 @@ EXPORT void or_traverse(int32_t Lv, int32_t B0, int32_t B, const float* const* l
           if (!cull_test(top, v3(ms[0], ms[1], ms[2]), ms[3])) continue;
           C.mesh_hits++;
         }
-        for (int64_t t = mesh_range[2 * m]; t < mesh_range[2 * m + 1]; ++t) {
-          const float* sp = tri_sph + 4 * t;
-          C.tests[Lv - 1]++;
-          if (cull_test(top, v3(sp[0], sp[1], sp[2]), sp[3])) {
-            C.hits[Lv - 1]++;
-            descend(Lv, n, t);
+        // top-level tests of the triangles at [ta, tb) of the mesh's index order
+        // (objtree: of its cluster order)
+        auto triangles = [&](int64_t ta, int64_t tb) {
+          for (int64_t i = ta; i < tb; ++i) {
+            const int64_t t = objtree ? (int64_t)cluster_order[i] : i;
+            const float* sp = tri_sph + 4 * t;
+            C.tests[Lv - 1]++;
+            if (cull_test(top, v3(sp[0], sp[1], sp[2]), sp[3])) {
+              C.hits[Lv - 1]++;
+              descend(Lv, n, t);
+            }
           }
+        };
+        if (!objtree) {
+          triangles(mesh_range[2 * m], mesh_range[2 * m + 1]);
+          continue;
+        }
+        // the object sphere-tree level: Eq 9 against each cluster sphere of the mesh
+        for (int64_t c = mesh_cluster_first[m]; c < mesh_cluster_first[m + 1]; ++c) {
+          C.cluster_tests++;
+          const float* cs = cluster_sph + 4 * c;
+          if (!cull_test(top, v3(cs[0], cs[1], cs[2]), cs[3])) continue;
+          C.cluster_hits++;
+          const int64_t ta = mesh_range[2 * m] + (c - mesh_cluster_first[m]) * CL;
+          triangles(ta, std::min<int64_t>(ta + CL, mesh_range[2 * m + 1]));
         }
       }
     }
@@ -738,6 +833,7 @@ EXPORT void or_traverse(int32_t Lv, int32_t B0, int32_t B, const float* const* l
   for (int k = 0; k < 8; ++k) { counters_out[k] = tot.tests[k]; counters_out[8 + k] = tot.hits[k]; }
   counters_out[16] = tot.mesh_tests; counters_out[17] = tot.mesh_hits;
   counters_out[18] = tot.final_tests; counters_out[19] = tot.final_hits;
+  counters_out[20] = tot.cluster_tests; counters_out[21] = tot.cluster_hits;
 }
 
 /* Whole-mesh culling alone, the first step of
