@@ -277,8 +277,8 @@ def measure(w, flags, args, local, world, flush, clocks=None):
                 launches=launches, merge=merge)
 
 
-def config_dict(w, zorder, world, merge):
-    return {"workload": w.name, "pixels": w.width * w.height, "triangles": int(w.tris.shape[0]),
+def config_dict(w, zorder, world, merge, objtree=False):
+    return {"workload": w.name, "object_tree": bool(objtree), "pixels": w.width * w.height, "triangles": int(w.tris.shape[0]),
             "meshes": int(w.n_meshes), "ray_types": w.ray_types, "lights": int(w.lights.shape[0]),
             "levels": w.levels, "leaf_size": w.leaf_size, "branching": w.branching,
             "hash": "zorder" if zorder else "R6 (SPEC layout)",
@@ -300,7 +300,7 @@ def run_crsh(args):
         # host plumbing only (NCCL id broadcast, barriers, max over ranks): the
         # data path is libcrsh's own NCCL communicator (crsh_dist_init)
         dist.init_process_group("gloo")
-    base = crsh.F_SORT | crsh.F_MESH_CULL
+    base = crsh.F_SORT | crsh.F_MESH_CULL | (crsh.F_OBJTREE if args.objtree else 0)
     w = make_workload(args.config)
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device="cuda")
     clk = ClockSampler(local)
@@ -377,7 +377,7 @@ def run_crsh(args):
         "warmup": args.warmup, "ms_per_step": round(m["ms"], 4), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded procedural scene + rasterised G-buffer, workloads/)",
-        "config": config_dict(w, main_z, world, crsh.MERGE.get(m["merge"], str(m["merge"]))),
+        "config": config_dict(w, main_z, world, crsh.MERGE.get(m["merge"], str(m["merge"])), args.objtree),
         "rays_per_step": rays,
         "tests_per_ray": round((tests_all + final_all) / max(rays, 1), 2),
         "tests_by_level": {f"L{k}": int(np.asarray(st["tests"])[:, k].sum()) for k in range(w.levels, 0, -1)},
@@ -442,7 +442,7 @@ def run_reference(args):
     from workloads import make_workload
     oracle.build()
     w = make_workload(args.config)
-    flags = 3 | (4 if args.zorder else 0)
+    flags = 3 | (4 if args.zorder else 0) | (64 if args.objtree else 0)
     budget = 150.0 / max(1, args.steps + args.warmup)      # whole run within a few minutes
     rows_probe = oracle_sample(w, flags, target_s=min(budget, 8.0))[2]
     prep = oracle.ScenePrep(w.tris, w.mesh_ids)
@@ -456,7 +456,7 @@ def run_reference(args):
     out = {"metric": METRIC, "value": round(v, 5), "unit": "Mrays/s", "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": round(1e3 * sum(times) / len(times), 2), "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
-           "config": config_dict(w, bool(args.zorder), 1, "none"),
+           "config": config_dict(w, bool(args.zorder), 1, "none", args.objtree),
            "cpu_baseline": {"value": round(v, 5), "unit": "Mrays/s", "cores": oracle.default_threads(),
                             "kind": "oracle", "sample": f"{rows_probe} of {w.height} image rows per step"},
            "e2e": {"value": round(v, 5), "unit": "Mrays/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -489,7 +489,8 @@ def run_table4(args):
     w = make_workload(args.config)
     stream = torch.cuda.current_stream()
     rows = {}
-    for name, flags in (("brute", crsh.F_BRUTE), ("rah", 0), ("crsh", 3), ("crsh_zorder", 7)):
+    for name, flags in (("brute", crsh.F_BRUTE), ("rah", 0), ("crsh", 3), ("crsh_zorder", 7),
+                        ("crsh_objtree", 3 | crsh.F_OBJTREE), ("crsh_zorder_objtree", 7 | crsh.F_OBJTREE)):
         tr = tracer_for(w, flags=flags)
         tr.run(stream)
         torch.cuda.synchronize()
@@ -500,13 +501,13 @@ def run_table4(args):
                       "tests_per_ray": round(total / max(1, sum(st["rays"])), 2),
                       "mrays_per_s": round(sum(st["rays"]) / (ms * 1e-3) / 1e6, 3),
                       "by_level": {f"L{k}": int(np.asarray(st["tests"])[:, k].sum()) for k in range(w.levels, 0, -1)},
-                      "final_tests": int(sum(st["final_tests"]))}
+                      "final_tests": int(sum(st["final_tests"])), "cluster_tests": int(sum(st["cluster_tests"]))}
     bt = rows["brute"]["total_tests"]
     for r in rows.values():
         r["relative_pct"] = round(100.0 * r["total_tests"] / bt, 4)
     rows["crsh_reduction_vs_rah_pct"] = round(100.0 * (1 - rows["crsh"]["total_tests"] / rows["rah"]["total_tests"]), 2)
-    rows["crsh_zorder_reduction_vs_rah_pct"] = round(
-        100.0 * (1 - rows["crsh_zorder"]["total_tests"] / rows["rah"]["total_tests"]), 2)
+    for k in ("crsh_zorder", "crsh_objtree", "crsh_zorder_objtree"):
+        rows[f"{k}_reduction_vs_rah_pct"] = round(100.0 * (1 - rows[k]["total_tests"] / rows["rah"]["total_tests"]), 2)
     print(json.dumps({"mode": "table4", "workload": w.name, "rays": int(sum(tr.stats()["rays"])), "M": tr.M,
                       "engines": rows}), flush=True)
 
@@ -534,7 +535,7 @@ def run_sweep(args):
                               "mrays_per_s": round(sum(st["rays"]) / (ms * 1e-3) / 1e6, 3),
                               "tests_per_ray": round(total / max(1, sum(st["rays"])), 2),
                               "by_level": {f"L{k}": int(np.asarray(st["tests"])[:, k].sum()) for k in range(lv, 0, -1)},
-                              "final_tests": int(sum(st["final_tests"]))}), flush=True)
+                              "final_tests": int(sum(st["final_tests"])), "cluster_tests": int(sum(st["cluster_tests"]))}), flush=True)
             del tr
 
 
@@ -671,6 +672,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--nccl-merge", action="store_true", help="N > 1: NCCL MIN all-reduce merge instead of the fused peer stores")
     ap.add_argument("--single-hash", action="store_true", help="skip the second hash layout's extra keys")
+    ap.add_argument("--objtree", action="store_true", help="object sphere-tree below the mesh spheres (NEXT-4)")
     ap.add_argument("--table4", action="store_true", help="CRSH vs RAH vs N x M report (not the contract line)")
     ap.add_argument("--sweep", action="store_true", help="cfg5 depth/bundle sweep (not the contract line)")
     ap.add_argument("--whitted", type=int, default=None, metavar="D",

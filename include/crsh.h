@@ -58,7 +58,13 @@ enum {
   CRSH_F_STAGE_TIMING = 8u,
   CRSH_F_BRUTE = 16u,  /* naive N x M ray tracing: every ray
                           against every triangle, no hierarchy; same outputs */
-  CRSH_F_KERNEL_TIMING = 32u /* time only the traversal kernel (stage_ms[6]) */
+  CRSH_F_KERNEL_TIMING = 32u, /* time only the traversal kernel (stage_ms[6]) */
+  CRSH_F_OBJTREE = 64u  /* object sphere-tree below the mesh spheres ("combine our
+                           coherent ray hierarchy with a deeper object hierarchy"): each mesh's triangles in
+                           Morton order of their centroids, in clusters of 32 with a bounding sphere each
+                           (reading O1); a top node tests a kept mesh's cluster spheres (Eq 9) before
+                           the triangles of the clusters that pass. Same hits; cluster_tests / cluster_hits
+                           count the extra level and tests[Lv] only the triangles of passing clusters. */
 };
 
 /* Build a scene (untimed preparation): copies the geometry, computes
@@ -135,6 +141,7 @@ typedef struct {
                         2 fused peer stores into the symmetric window (crsh_dist_init) */
   float stage_ms[8]; /* generate+trim, compress, sort, decompress, build,
                         mesh-cull+plan, traverse+final, output */
+  uint64_t cluster_tests[3], cluster_hits[3];   /* CRSH_F_OBJTREE: node-vs-cluster-sphere tests / passes */
 } crsh_stats_t;
 
 /* Number of ray slots: P * (n_lights*[SH] + [RE] + [RR]). Slot order (the ray
@@ -340,7 +347,9 @@ enum {
   CRSH_TAP_MESH_SPHERES = 10,/* float[4] padded mesh spheres (scene) */
   CRSH_TAP_SCENE_CONSTS = 11,/* float[8]: aabb min.xyz, max.xyz, pad, eps_t */
   CRSH_TAP_GROUP_RANGE = 12, /* u32[3]: this rank's groups [g_lo, g_hi) and G (frame-wide) */
-  CRSH_TAP_GROUP_WORK = 13   /* u64[G]: per-group work the cut balanced (shard_world > 1 only) */
+  CRSH_TAP_GROUP_WORK = 13,  /* u64[G]: per-group work the cut balanced (shard_world > 1 only) */
+  CRSH_TAP_CLUSTER_SPHERES = 14, /* float[4] padded object-tree cluster spheres, mesh by mesh (scene) */
+  CRSH_TAP_CLUSTER_ORDER = 15    /* i32[M] triangle ids in cluster order (Morton within each mesh; scene) */
 };
 crsh_status crsh_debug_tap(crsh_scene_t scene, int32_t tap, int32_t segment, int32_t level, void* host_dst,
                            size_t cap_bytes, size_t* n_out);

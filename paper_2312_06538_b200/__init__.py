@@ -20,10 +20,10 @@ LIB_PATH = os.environ.get("CRSH_LIB_PATH") or os.path.join(HERE, "libcrsh.so")  
 HEADER = os.path.join(os.path.dirname(HERE), "include", "crsh.h")
 
 SHADOW, REFLECT, REFRACT = 1, 2, 4
-F_SORT, F_MESH_CULL, F_ZORDER, F_STAGE_TIMING, F_BRUTE, F_KERNEL_TIMING = 1, 2, 4, 8, 16, 32
+F_SORT, F_MESH_CULL, F_ZORDER, F_STAGE_TIMING, F_BRUTE, F_KERNEL_TIMING, F_OBJTREE = 1, 2, 4, 8, 16, 32, 64
 TAP_KEYS, TAP_VALS, TAP_CHUNK_KEYS, TAP_CHUNK_BASE, TAP_SORTED_KEYS, TAP_SORTED_SLOTS = 1, 2, 3, 4, 5, 6
 TAP_NODES, TAP_SORTED_RAYS, TAP_TRI_SPHERES, TAP_MESH_SPHERES, TAP_SCENE_CONSTS = 7, 8, 9, 10, 11
-TAP_GROUP_RANGE, TAP_GROUP_WORK = 12, 13
+TAP_GROUP_RANGE, TAP_GROUP_WORK, TAP_CLUSTER_SPHERES, TAP_CLUSTER_ORDER = 12, 13, 14, 15
 STATUS = {0: "OK", 2: "EINVAL", 3: "EIO", 4: "ELIMIT", 5: "ENOMEM", 6: "ECUDA", 7: "ENCCL"}
 MERGE = {0: "none", 1: "nccl-allreduce-min", 2: "fused-peer-stores"}
 STAGES = ["generate+trim", "compress", "sort", "decompress", "build", "mesh-cull+plan", "traverse+final", "output"]
@@ -71,7 +71,7 @@ class Stats(C.Structure):
                 ("tests", (C.c_uint64 * 9) * 3), ("hits", (C.c_uint64 * 9) * 3),
                 ("final_tests", C.c_uint64 * 3), ("final_hits", C.c_uint64 * 3), ("rays_hit", C.c_uint64 * 3),
                 ("brute", C.c_uint64 * 3), ("levels", C.c_int32), ("merge", C.c_int32),
-                ("stage_ms", C.c_float * 8)]
+                ("stage_ms", C.c_float * 8), ("cluster_tests", C.c_uint64 * 3), ("cluster_hits", C.c_uint64 * 3)]
 
 
 _lib = None
@@ -271,7 +271,8 @@ def stats(scene: Scene) -> dict:
                 mesh_hits=list(s.mesh_hits), tests=np.array([list(r) for r in s.tests], np.uint64),
                 hits=np.array([list(r) for r in s.hits], np.uint64), final_tests=list(s.final_tests),
                 final_hits=list(s.final_hits), rays_hit=list(s.rays_hit), brute=list(s.brute), levels=s.levels,
-                merge=s.merge, stage_ms=list(s.stage_ms))
+                merge=s.merge, stage_ms=list(s.stage_ms), cluster_tests=list(s.cluster_tests),
+                cluster_hits=list(s.cluster_hits))
 
 
 def launch_count(scene: Scene) -> int:
@@ -279,7 +280,8 @@ def launch_count(scene: Scene) -> int:
 
 
 _TAP_DTYPE = {TAP_NODES: (np.float32, 8), TAP_SORTED_RAYS: (np.float32, 8), TAP_TRI_SPHERES: (np.float32, 4),
-              TAP_MESH_SPHERES: (np.float32, 4), TAP_SCENE_CONSTS: (np.float32, 1), TAP_GROUP_WORK: (np.uint64, 1)}
+              TAP_MESH_SPHERES: (np.float32, 4), TAP_SCENE_CONSTS: (np.float32, 1), TAP_GROUP_WORK: (np.uint64, 1),
+              TAP_CLUSTER_SPHERES: (np.float32, 4), TAP_CLUSTER_ORDER: (np.int32, 1)}
 
 
 def debug_tap(scene: Scene, tap: int, segment: int = 0, level: int = 1) -> np.ndarray:

@@ -180,6 +180,59 @@ void mesh_sphere(const float* tris, int64_t t0, int64_t t1, float pad, float out
   out[0] = cf[0]; out[1] = cf[1]; out[2] = cf[2]; out[3] = rf + pad;
 }
 
+// Object sphere-tree order (reading O1): per mesh, triangles sorted by the
+// 30-bit Morton code of their centroid (((v0 + v1) + v2) / 3, double) in 1024
+// cells per axis of the mesh's vertex box (x most significant), ties by
+// index; clusters of 32 consecutive triangles of that order.
+void cluster_order(const float* tris, const std::vector<uint32_t>& first, const std::vector<uint32_t>& count,
+                   std::vector<int32_t>& order, std::vector<uint32_t>& cl_first, std::vector<uint32_t>& cl_range) {
+  const size_t nm = first.size();
+  size_t M = 0;
+  for (size_t m = 0; m < nm; ++m) M += count[m];
+  order.assign(M, 0);
+  cl_first.assign(nm + 1, 0);
+  cl_range.clear();
+  auto spread = [](uint64_t v) {
+    uint64_t r = 0;
+    for (int b = 0; b < 10; ++b) r |= ((v >> b) & 1ull) << (3 * b);
+    return r;
+  };
+  uint32_t nc = 0;
+  for (size_t m = 0; m < nm; ++m) {
+    cl_first[m] = nc;
+    const uint32_t t0 = first[m], n = count[m];
+    if (!n) continue;
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (size_t i = 9 * (size_t)t0; i < 9 * (size_t)(t0 + n); ++i) {
+      lo[i % 3] = std::min(lo[i % 3], (double)tris[i]);
+      hi[i % 3] = std::max(hi[i % 3], (double)tris[i]);
+    }
+    std::vector<std::pair<uint64_t, uint32_t>> key(n);
+    for (uint32_t j = 0; j < n; ++j) {
+      const float* v = tris + 9 * (size_t)(t0 + j);
+      uint64_t code = 0;
+      for (int k = 0; k < 3; ++k) {
+        uint64_t q = 0;
+        if (hi[k] > lo[k]) {
+          const double c = (((double)v[k] + (double)v[3 + k]) + (double)v[6 + k]) / 3.0;
+          const double u = std::floor(((c - lo[k]) / (hi[k] - lo[k])) * 1024.0);
+          q = u <= 0.0 ? 0 : (u >= 1023.0 ? 1023 : (uint64_t)u);
+        }
+        code |= spread(q) << (2 - k);
+      }
+      key[j] = {code, t0 + j};
+    }
+    std::sort(key.begin(), key.end());
+    for (uint32_t j = 0; j < n; ++j) order[t0 + j] = (int32_t)key[j].second;
+    for (uint32_t c0 = 0; c0 < n; c0 += 32) {
+      cl_range.push_back(t0 + c0);
+      cl_range.push_back(t0 + std::min(c0 + 32, n));
+      ++nc;
+    }
+  }
+  cl_first[nm] = nc;
+}
+
 }  // namespace
 
 // ============================================================== scene
@@ -237,6 +290,9 @@ struct crsh_scene {
   Buf tris0, mesh_ids, tris_cur, xf, boxk;
   std::vector<float> h_mesh_sph0;
   Dist* dist = nullptr;                 // crsh_dist_init: NCCL communicator, window, merge mode
+  // object sphere-tree (CRSH_F_OBJTREE, reading O1): cluster order, ranges, spheres
+  Buf cl_order, cl_range, cl_first, cl_sph, tri_sph_ord;
+  int64_t n_clusters = 0;
 };
 
 namespace {
@@ -539,6 +595,7 @@ crsh_status enqueue_frame(crsh_scene* sc, const FrameInfo& fi, const crsh_primar
         w.fd = fd; w.K = fi.K; w.W = W; w.n_meshes = sc->n_meshes;
         w.masks = sc->masks.as<uint32_t>(); w.mesh_count = sc->mesh_count.as<uint32_t>();
         w.trav_top = trav + 3 * fi.level_off[Lv]; w.cull_on = a.cull_on; w.n_nonempty = sc->n_nonempty;
+        w.objtree = (fi.flags & CRSH_F_OBJTREE) ? 1 : 0;
         w.work = sc->gwork.as<unsigned long long>(); w.gstat = sc->gstat.as<uint4>();
         k_group_work<<<cdiv(std::max<uint64_t>(fi.G_max, 1), 8), 256, 0, st>>>(w);
         CK(cudaGetLastError());
@@ -572,6 +629,10 @@ crsh_status enqueue_frame(crsh_scene* sc, const FrameInfo& fi, const crsh_primar
       t.tri_sph = sc->tri_sph.as<float4>();
       t.masks = sc->masks.as<uint32_t>(); t.W = W; t.n_meshes = sc->n_meshes;
       t.mesh_first = sc->mesh_first.as<uint32_t>(); t.mesh_count = sc->mesh_count.as<uint32_t>();
+      if (fi.flags & CRSH_F_OBJTREE) {
+        t.tri_order = sc->cl_order.as<int32_t>(); t.tri_sph_ord = sc->tri_sph_ord.as<float4>();
+        t.mesh_cluster_first = sc->cl_first.as<uint32_t>(); t.cluster_sph = sc->cl_sph.as<float4>();
+      }
       t.items = sc->items.as<uint4>(); t.fd = fd; t.ticket = tickets + T_TRAV;
       t.best = sc->best.as<unsigned long long>(); t.counters = counters; t.n_seg = fi.n_seg;
       const bool small = fi.GR <= SMALL_GROUP_RAYS;
@@ -586,9 +647,15 @@ crsh_status enqueue_frame(crsh_scene* sc, const FrameInfo& fi, const crsh_primar
         kern<<<per_sm * sc->sm_count, TRAV_THREADS, L.total, st>>>(t, L);
         return cudaGetLastError();
       };
-      if (B == 8 && B0 == 8 && Lv == 2 && fi.K == 8) CK(small ? launch(k_traverse<true, 8, 8, 2>) : launch(k_traverse<false, 8, 8, 2>));
-      else if (B == 8 && B0 == 8) CK(small ? launch(k_traverse<true, 8, 8, 0>) : launch(k_traverse<false, 8, 8, 0>));
-      else CK(small ? launch(k_traverse<true, 0, 0, 0>) : launch(k_traverse<false, 0, 0, 0>));
+      auto pick = [&](auto obj) -> cudaError_t {
+        constexpr bool O = decltype(obj)::value;
+        if (B == 8 && B0 == 8 && Lv == 2 && fi.K == 8)
+          return small ? launch(k_traverse<true, 8, 8, 2, O>) : launch(k_traverse<false, 8, 8, 2, O>);
+        if (B == 8 && B0 == 8) return small ? launch(k_traverse<true, 8, 8, 0, O>) : launch(k_traverse<false, 8, 8, 0, O>);
+        return small ? launch(k_traverse<true, 0, 0, 0, O>) : launch(k_traverse<false, 0, 0, 0, O>);
+      };
+      if (fi.flags & CRSH_F_OBJTREE) CK(pick(std::true_type()));
+      else CK(pick(std::false_type()));
       ++nl;
     }
     CK(mark(7));
@@ -657,7 +724,7 @@ crsh_status trace_impl(crsh_scene* sc, const crsh_primary_hits* h, const float* 
     world = dist->world;
   }
   PeerOut peer = peer_in;
-  if ((o->flags & ~63u) != 0) return fail(CRSH_EINVAL, "unknown flags");
+  if ((o->flags & ~127u) != 0) return fail(CRSH_EINVAL, "unknown flags");
   if (!peer.n && !out_packed && (!out_hit || !out_t)) return fail(CRSH_EINVAL, "null output");
   if (dist && (peer.n || out_packed || in_rays)) return fail(CRSH_EINVAL, "internal: dist merge with explicit outputs");
 
@@ -984,6 +1051,30 @@ crsh_status crsh_scene_create(const float* tris, const int32_t* mesh_ids, int64_
   ck(cudaMemcpy(sc->mesh_first.p, first.data(), 4 * (size_t)n_meshes, cudaMemcpyHostToDevice), "copy first");
   ck(cudaMemcpy(sc->mesh_count.p, count.data(), 4 * (size_t)n_meshes, cudaMemcpyHostToDevice), "copy count");
   for (int32_t m = 0; m < n_meshes; ++m) sc->n_nonempty += count[m] ? 1 : 0;
+  {   // object sphere-tree (CRSH_F_OBJTREE): cluster order on the host, spheres on the device
+    std::vector<int32_t> order;
+    std::vector<uint32_t> cfirst, crange;
+    cluster_order(ht.data(), first, count, order, cfirst, crange);
+    sc->n_clusters = (int64_t)(crange.size() / 2);
+    ck(ensure(sc->cl_order, 4 * (size_t)M), "alloc cl_order");
+    ck(ensure(sc->cl_first, 4 * ((size_t)n_meshes + 1)), "alloc cl_first");
+    ck(ensure(sc->cl_range, 8 * (size_t)std::max<int64_t>(sc->n_clusters, 1)), "alloc cl_range");
+    ck(ensure(sc->cl_sph, 16 * (size_t)std::max<int64_t>(sc->n_clusters, 1)), "alloc cl_sph");
+    ck(ensure(sc->tri_sph_ord, 16 * (size_t)M), "alloc tri_sph_ord");
+    if (rc == CRSH_OK) {
+      ck(cudaMemcpy(sc->cl_order.p, order.data(), 4 * (size_t)M, cudaMemcpyHostToDevice), "copy cl_order");
+      ck(cudaMemcpy(sc->cl_first.p, cfirst.data(), 4 * cfirst.size(), cudaMemcpyHostToDevice), "copy cl_first");
+      if (!crange.empty())
+        ck(cudaMemcpy(sc->cl_range.p, crange.data(), 4 * crange.size(), cudaMemcpyHostToDevice), "copy cl_range");
+    }
+    if (rc == CRSH_OK) {
+      const int grid = (int)std::min<int64_t>((std::max<int64_t>(sc->n_clusters, M) + 255) / 256, 8 * sc->sm_count);
+      k_cluster_prep<<<grid, 256>>>(tris, sc->cl_order.as<int32_t>(), sc->cl_range.as<uint2>(), sc->n_clusters, sc->pad,
+                                    sc->cl_sph.as<float4>());
+      k_permute_sph<<<grid, 256>>>(sc->tri_sph.as<float4>(), sc->cl_order.as<int32_t>(), M, sc->tri_sph_ord.as<float4>());
+      ck(cudaGetLastError(), "k_cluster_prep");
+    }
+  }
   ck(cudaDeviceSynchronize(), "scene prep");
   if (rc != CRSH_OK) return bail(rc);
   *out = sc;
@@ -1001,6 +1092,7 @@ void crsh_scene_destroy(crsh_scene_t sc) {
   for (auto& w : sc->wb) for (auto& b : w) b.release();
   sc->w_hit.release(); sc->w_t.release(); sc->w_zero.release(); sc->prim_rays.release();
   sc->tris0.release(); sc->mesh_ids.release(); sc->tris_cur.release(); sc->xf.release(); sc->boxk.release();
+  sc->cl_order.release(); sc->cl_range.release(); sc->cl_first.release(); sc->cl_sph.release(); sc->tri_sph_ord.release();
   if (sc->dist) {
     Dist* d = sc->dist;
     if (d->win) ncclCommWindowDeregister(d->comm, d->win);
@@ -1107,6 +1199,11 @@ crsh_status crsh_scene_transform(crsh_scene_t sc, const float* xforms) {
                              sc->tris_cur.as<float>(), sc->boxk.as<float>());
   CK(cudaGetLastError());
   k_tri_prep<<<grid, 256>>>(sc->tris_cur.as<float>(), sc->M, sc->pad, sc->tri_e.as<float4>(), sc->tri_sph.as<float4>());
+  CK(cudaGetLastError());
+  // object-tree clusters: creation-time order, spheres of the moved vertices
+  k_cluster_prep<<<grid, 256>>>(sc->tris_cur.as<float>(), sc->cl_order.as<int32_t>(), sc->cl_range.as<uint2>(),
+                                sc->n_clusters, sc->pad, sc->cl_sph.as<float4>());
+  k_permute_sph<<<grid, 256>>>(sc->tri_sph.as<float4>(), sc->cl_order.as<int32_t>(), sc->M, sc->tri_sph_ord.as<float4>());
   CK(cudaGetLastError());
   int box[6];
   CK(cudaMemcpy(box, sc->boxk.p, sizeof box, cudaMemcpyDeviceToHost));
@@ -1346,6 +1443,8 @@ crsh_status crsh_stats(crsh_scene_t sc, crsh_stats_t* out) {
     out->final_tests[ty] = c[CTR_FINAL_TESTS];
     out->final_hits[ty] = c[CTR_FINAL_HITS];
     out->rays_hit[ty] = c[CTR_RAYS_HIT];
+    out->cluster_tests[ty] = c[CTR_CL_TESTS];
+    out->cluster_hits[ty] = c[CTR_CL_HITS];
     out->brute[ty] = (uint64_t)fi.fd.seg_n[s] * (uint64_t)sc->M;
   }
   if ((fi.timed || fi.ktimed) && fi.fd.N > 0) {
@@ -1375,6 +1474,8 @@ crsh_status crsh_debug_tap(crsh_scene_t sc, int32_t tap, int32_t seg_type, int32
   std::vector<uint32_t> rel;
   if (tap == CRSH_TAP_TRI_SPHERES) { src = sc->tri_sph.p; n = (size_t)sc->M; esz = 16; }
   else if (tap == CRSH_TAP_MESH_SPHERES) { src = sc->mesh_sph.p; n = (size_t)sc->n_meshes; esz = 16; }
+  else if (tap == CRSH_TAP_CLUSTER_SPHERES) { src = sc->cl_sph.p; n = (size_t)sc->n_clusters; esz = 16; }
+  else if (tap == CRSH_TAP_CLUSTER_ORDER) { src = sc->cl_order.p; n = (size_t)sc->M; esz = 4; }
   else if (tap == CRSH_TAP_SCENE_CONSTS) {
     float c[8] = {sc->box_min[0], sc->box_min[1], sc->box_min[2], sc->box_max[0], sc->box_max[1], sc->box_max[2], sc->pad, sc->eps_t};
     *n_out = 8;

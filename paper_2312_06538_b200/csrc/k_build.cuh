@@ -70,6 +70,46 @@ __global__ void k_tri_prep(const float* __restrict__ tris, int64_t M, float pad,
   }
 }
 
+// Object sphere-tree clusters (CRSH_F_OBJTREE, NEXT-4, reading O1): cluster i
+// covers positions [rng.x, rng.y) of the cluster order; its sphere is centred
+// at the midpoint of its vertices' bounding box (double, rounded to float),
+// radius = the largest distance from that float centre (double, rounded up),
+// plus pad. Also the triangle spheres permuted into cluster order.
+__global__ void k_cluster_prep(const float* __restrict__ tris, const int32_t* __restrict__ order,
+                               const uint2* __restrict__ rng, int64_t n_clusters, float pad, float4* __restrict__ cl_sph) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n_clusters; c += (int64_t)gridDim.x * blockDim.x) {
+    const uint2 r = rng[c];
+    double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+    for (uint32_t i = r.x; i < r.y; ++i) {
+      const float* v = tris + 9 * (size_t)order[i];
+      for (int k = 0; k < 9; ++k) {
+        const double q = (double)v[k];
+        lo[k % 3] = fmin(lo[k % 3], q);
+        hi[k % 3] = fmax(hi[k % 3], q);
+      }
+    }
+    const float fx = (float)((lo[0] + hi[0]) * 0.5), fy = (float)((lo[1] + hi[1]) * 0.5), fz = (float)((lo[2] + hi[2]) * 0.5);
+    double r2 = 0.0;
+    for (uint32_t i = r.x; i < r.y; ++i) {
+      const float* v = tris + 9 * (size_t)order[i];
+      for (int k = 0; k < 3; ++k) {
+        const double dx = (double)v[3 * k] - (double)fx, dy = (double)v[3 * k + 1] - (double)fy,
+                     dz = (double)v[3 * k + 2] - (double)fz;
+        r2 = fmax(r2, dx * dx + dy * dy + dz * dz);
+      }
+    }
+    const double rd = sqrt(r2);
+    float rf = (float)rd;
+    if ((double)rf < rd) rf = nextafterf(rf, __int_as_float(0x7f800000));
+    cl_sph[c] = make_float4(fx, fy, fz, rf + pad);
+  }
+}
+__global__ void k_permute_sph(const float4* __restrict__ tri_sph, const int32_t* __restrict__ order, int64_t M,
+                              float4* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < M; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = tri_sph[order[i]];
+}
+
 // ------------------------------------------------------------ nodes
 // so: (leaves) every ray of the bundle starts at the node centre, bit for bit
 __device__ __forceinline__ void store_node(float4* nodes, float4* trav, size_t j, const NodeV& n, bool so = false) {

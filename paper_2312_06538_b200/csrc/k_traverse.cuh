@@ -34,7 +34,10 @@ constexpr int CTR_MESH_HITS = 19;
 constexpr int CTR_FINAL_TESTS = 20;
 constexpr int CTR_FINAL_HITS = 21;
 constexpr int CTR_RAYS_HIT = 22;
+constexpr int CTR_CL_TESTS = 23;     // object sphere-tree (CRSH_F_OBJTREE): node vs cluster sphere
+constexpr int CTR_CL_HITS = 24;
 constexpr int CTR_STRIDE = 32;
+constexpr uint32_t CLUSTER_TRIS = 32;   // triangles per object-tree cluster (reading O1): one warp slice
 
 constexpr unsigned long long BEST_NONE = 0xFFFFFFFFFFFFFFFFull;
 constexpr unsigned long long PACK_MISS = 0x7F800000FFFFFFFFull;
@@ -95,6 +98,7 @@ struct WorkArgs {
   const uint32_t* mesh_count;
   const float4* trav_top;      // node existence (radius >= 0)
   int32_t cull_on, n_nonempty;
+  int32_t objtree;             // CRSH_F_OBJTREE: a mesh's triangles count in whole clusters (slices)
   unsigned long long* work;    // [G] top-level tests of the group (the cut's work)
   uint4* gstat;                // [G] {triangles of the meshes any node kept, mesh tests, mesh passes, 0}
 };
@@ -119,7 +123,8 @@ __global__ void __launch_bounds__(256) k_group_work(const WorkArgs a) {
       nb = ((int)lane == b) ? c : nb;
     }
     const int m = w * 32 + (int)lane;
-    const uint32_t cnt = (m < a.n_meshes) ? __ldg(a.mesh_count + m) : 0u;
+    uint32_t cnt = (m < a.n_meshes) ? __ldg(a.mesh_count + m) : 0u;
+    if (a.objtree) cnt = (cnt + CLUSTER_TRIS - 1) / CLUSTER_TRIS * CLUSTER_TRIS;   // cluster-aligned virtual range
     T += ((u >> lane) & 1u) ? cnt : 0u;
     work += (unsigned long long)nb * cnt;
   }
@@ -331,6 +336,12 @@ struct TravArgs {
   int32_t W, n_meshes;
   const uint32_t* mesh_first;
   const uint32_t* mesh_count;
+  // CRSH_F_OBJTREE (null otherwise): triangle ids in cluster order, the
+  // triangle spheres in that order, first cluster of each mesh, cluster spheres
+  const int32_t* tri_order;
+  const float4* tri_sph_ord;
+  const uint32_t* mesh_cluster_first;
+  const float4* cluster_sph;
   const uint4* items;
   const FrameDesc* fd;                // n_items, seg_pad_base (group starts)
   uint32_t* ticket;
@@ -341,7 +352,8 @@ struct TravArgs {
 
 // dynamic shared-memory layout (bytes), shared by host and device
 struct TravSmem {
-  uint32_t off_top, off_tpairs, off_exm, off_act_nmask, off_act_prefix, off_act_first, off_q, off_best, off_nodes, off_rays,
+  uint32_t off_top, off_tpairs, off_exm, off_act_nmask, off_act_prefix, off_act_first, off_act_cnt, off_act_cfirst, off_q,
+      off_best, off_nodes, off_rays,
       off_pairs, node_off[MAX_LEVELS + 1], q_off[MAX_LEVELS + 1], q_warp, total;
   __host__ __device__ static TravSmem make(int K, int B, int n_meshes, int Lv, bool small, const uint32_t* per_group,
                                            uint32_t group_rays) {
@@ -354,6 +366,8 @@ struct TravSmem {
     s.off_act_nmask = take(4u * n_meshes);
     s.off_act_prefix = take(4u * (n_meshes + 1));
     s.off_act_first = take(4u * n_meshes);
+    s.off_act_cnt = take(4u * n_meshes);
+    s.off_act_cfirst = take(4u * n_meshes);
     // per-warp queues of uint2 (node_local, triangle): Lv == 1: the top (=
     // bundle) level holds one slice (32 K) plus a partial step; Lv >= 2:
     // level Lv-1 receives the dense child tests of one top node (32 B) plus
@@ -395,7 +409,9 @@ struct TravSmem {
 #ifndef CRSH_TRAV_MINB_LV2
 #define CRSH_TRAV_MINB_LV2 4
 #endif
-template <bool SMALL, int BT, int B0T, int LVT>
+// OBJ: the object sphere-tree path (CRSH_F_OBJTREE) as its own instantiation,
+// so the plain path keeps its single slice loop (register allocation)
+template <bool SMALL, int BT, int B0T, int LVT, bool OBJ>
 __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : CRSH_TRAV_MINB)
     k_traverse(const TravArgs a, const TravSmem L) {
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -403,6 +419,10 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
   uint32_t* s_act_nmask = reinterpret_cast<uint32_t*>(smraw + L.off_act_nmask);
   uint32_t* s_act_prefix = reinterpret_cast<uint32_t*>(smraw + L.off_act_prefix);
   uint32_t* s_act_first = reinterpret_cast<uint32_t*>(smraw + L.off_act_first);
+  uint32_t* s_act_cnt = reinterpret_cast<uint32_t*>(smraw + L.off_act_cnt);
+  uint32_t* s_act_cfirst = reinterpret_cast<uint32_t*>(smraw + L.off_act_cfirst);
+  constexpr bool objtree = OBJ;
+  const float4* tsph = objtree ? a.tri_sph_ord : a.tri_sph;
   unsigned long long* s_best = reinterpret_cast<unsigned long long*>(smraw + L.off_best);
   const float4* s_nodes = reinterpret_cast<const float4*>(smraw + L.off_nodes);
   const float4* s_rays = reinterpret_cast<const float4*>(smraw + L.off_rays);
@@ -554,6 +574,8 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
           for (int j = 0; j < K; ++j) nm |= ((__ldg(a.masks + ((size_t)g * K + j) * a.W + w) >> b) & 1u) << j;
           cnt = nm ? __ldg(a.mesh_count + m) : 0u;
         }
+        const uint32_t real_cnt = cnt;
+        if (objtree) cnt = (cnt + CLUSTER_TRIS - 1) / CLUSTER_TRIS * CLUSTER_TRIS;   // whole clusters (slices)
         const uint32_t act = nm ? 1u : 0u;
         uint32_t tot_a, tot_c;
         const uint32_t ea = block_excl_scan<TRAV_WARPS>(act, s_warp, &tot_a);
@@ -563,6 +585,8 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
           s_act_nmask[base_a + ea] = nm;
           s_act_prefix[base_a + ea] = base_c + ec;
           s_act_first[base_a + ea] = __ldg(a.mesh_first + m);
+          s_act_cnt[base_a + ea] = real_cnt;
+          if (objtree) s_act_cfirst[base_a + ea] = __ldg(a.mesh_cluster_first + m);
         }
         __syncthreads();
         if (tid == 0) { s_carry = base_a + tot_a; s_carry_c = base_c + tot_c; }
@@ -578,6 +602,7 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
     const uint32_t n_act = s_n_act;
     const size_t rbase = (size_t)g * a.group_rays;
     uint32_t c_top_t = 0, c_top_h = 0, c_ch_t = 0, c_ch_h = 0, c_mt_t = 0, c_mt_h = 0;   // item counters (all but c_ch_t per lane)
+    uint32_t c_cl_t = 0, c_cl_h = 0;   // object-tree cluster tests / passes (lane 0 of each slice)
 
     // final tests: one step = up to 32 (bundle, triangle) entries
     // from the end of Q[1], one per lane; the lane loads its triangle once
@@ -716,28 +741,27 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
       }
     };
 
-    uint32_t mlo = 0xFFFFFFFFu;   // the lane's active-mesh index in its previous slice (v only grows)
-    for (uint32_t s = item.y + warp * 32u; s < item.z; s += TRAV_THREADS) {
-      const uint32_t v = s + lane;
-      uint32_t nm = 0, tri = 0;
-      float4 sph = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (v < item.z) {
-        uint32_t lo = 0;   // largest p with prefix[p] <= v
-        if (mlo == 0xFFFFFFFFu) {   // first slice of the item: binary search
-          uint32_t hi = n_act;
-          while (hi - lo > 1) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if (s_act_prefix[mid] <= v) lo = mid; else hi = mid;
-          }
-        } else {                    // then forward from the previous slice's mesh
-          lo = mlo;
-          while (lo + 1 < n_act && s_act_prefix[lo + 1] <= v) ++lo;
+    uint32_t mlo = 0xFFFFFFFFu;   // the lane's active-mesh index in its previous lookup (v only grows)
+    // active mesh of virtual triangle index v: largest p with prefix[p] <= v
+    // (binary search for the first lookup of the item, then forward walks)
+    auto mesh_of = [&](uint32_t v) -> uint32_t {
+      uint32_t lo = 0;
+      if (mlo == 0xFFFFFFFFu) {
+        uint32_t hi = n_act;
+        while (hi - lo > 1) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (s_act_prefix[mid] <= v) lo = mid; else hi = mid;
         }
-        mlo = lo;
-        tri = s_act_first[lo] + (v - s_act_prefix[lo]);
-        sph = __ldg(a.tri_sph + tri);
-        nm = s_act_nmask[lo];
+      } else {
+        lo = mlo;
+        while (lo + 1 < n_act && s_act_prefix[lo + 1] <= v) ++lo;
       }
+      mlo = lo;
+      return lo;
+    };
+    // one 32-triangle slice, lane = triangle (tri, sph), nm = the lane's top
+    // nodes to test: the top-level tests, the dense child tests, the queues
+    auto slice_body = [&](uint32_t tri, float4 sph, uint32_t nm) {
       const f2 Px = pk2(sph.x, sph.x), Py = pk2(sph.y, sph.y), Pz = pk2(sph.z, sph.z), Pr = pk2(sph.w, sph.w);
       // top level, all K nodes first: nodes (j, j+1) per packed test (paired
       // records); a lane tests node j only if its triangle's mesh survived
@@ -816,6 +840,64 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
         if (!QREG || k1 != 1) __syncwarp();
         drain(false);
       }
+    };
+    if constexpr (!OBJ) {
+      for (uint32_t s0 = item.y + warp * 32u; s0 < item.z; s0 += TRAV_THREADS) {
+        const uint32_t v = s0 + lane;
+        uint32_t nm = 0, tri = 0;
+        float4 sph = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (v < item.z) {
+          const uint32_t lo = mesh_of(v);
+          tri = s_act_first[lo] + (v - s_act_prefix[lo]);
+          sph = __ldg(a.tri_sph + tri);
+          nm = s_act_nmask[lo];
+        }
+        slice_body(tri, sph, nm);
+      }
+    } else {
+      // object sphere-tree (NEXT-4, reading O1): the item's virtual range is
+      // cluster-aligned (each kept mesh padded to whole clusters), so cluster
+      // c is the slice [32 c, 32 c + 32). A warp takes blocks of CPB = 32 / K
+      // consecutive clusters and tests every (cluster, top node) pair of the
+      // block at once, lane = (cluster lane / K, node lane % K): Eq 9 of the
+      // cluster sphere against the node if the node kept the cluster's mesh.
+      // Then only the clusters that passed some node are streamed as slices,
+      // each lane testing its triangle against the nodes its cluster passed.
+      const uint32_t cy = item.y / CLUSTER_TRIS, cz = (item.z + CLUSTER_TRIS - 1) / CLUSTER_TRIS;
+      const uint32_t CPB = 32u / (uint32_t)K;   // K <= 32
+      const uint32_t ci = lane / (uint32_t)K, jn = lane - ci * (uint32_t)K;
+      const uint32_t kmask = K == 32 ? 0xFFFFFFFFu : ((1u << K) - 1u);
+      for (uint32_t b0 = cy + warp * CPB; b0 < cz; b0 += TRAV_WARPS * CPB) {
+        const uint32_t c = b0 + ci;
+        uint32_t lo = 0;
+        bool tst = false, pass = false;
+        if (ci < CPB && c < cz) {
+          lo = mesh_of(c * CLUSTER_TRIS);
+          tst = (s_act_nmask[lo] >> jn) & 1u;
+          if (tst) {
+            const float4 cs = __ldg(a.cluster_sph + s_act_cfirst[lo] + (c * CLUSTER_TRIS - s_act_prefix[lo]) / CLUSTER_TRIS);
+            const float4 t0 = s_top[3 * jn], t1 = s_top[3 * jn + 1], t2 = s_top[3 * jn + 2];
+            pass = cull_ns(mk3(t0.x, t0.y, t0.z), t0.w, mk3(t1.x, t1.y, t1.z), t1.w, t2.x, cs);
+          }
+        }
+        const uint32_t bt = __ballot_sync(CRSH_FULL, tst), bp = __ballot_sync(CRSH_FULL, pass);
+        if (lane == 0) { c_cl_t += __popc(bt); c_cl_h += __popc(bp); }
+        for (uint32_t q = 0; q < CPB; ++q) {
+          const uint32_t cmk = (bp >> (q * (uint32_t)K)) & kmask;
+          if (!cmk) continue;   // uniform: this cluster passed no node
+          const uint32_t lok = __shfl_sync(CRSH_FULL, lo, q * (uint32_t)K);
+          const uint32_t loc = (b0 + q) * CLUSTER_TRIS + lane - s_act_prefix[lok];
+          uint32_t tri = 0, nm = 0;
+          float4 sph = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (loc < s_act_cnt[lok]) {   // else a padding lane of the mesh's last cluster
+            const uint32_t pidx = s_act_first[lok] + loc;
+            tri = (uint32_t)__ldg(a.tri_order + pidx);
+            sph = __ldg(tsph + pidx);
+            nm = cmk;
+          }
+          slice_body(tri, sph, nm);
+        }
+      }
     }
     drain(true);
     // item counters -> CTA counters (one shared atomic per counter per warp)
@@ -825,6 +907,8 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
     c_mt_h = __reduce_add_sync(CRSH_FULL, c_mt_h);
     c_ch_h = __reduce_add_sync(CRSH_FULL, c_ch_h);
     if (lane == 0) {
+      if (c_cl_t) atomicAdd(&ctr[CTR_CL_TESTS], (unsigned long long)c_cl_t);
+      if (c_cl_h) atomicAdd(&ctr[CTR_CL_HITS], (unsigned long long)c_cl_h);
       if (c_top_t) atomicAdd(&ctr[CTR_TESTS + Lv], (unsigned long long)c_top_t);
       if (c_top_h) atomicAdd(&ctr[CTR_HITS + Lv], (unsigned long long)c_top_h);
       if (Lv >= 2 && c_ch_t) atomicAdd(&ctr[CTR_TESTS + Lv - 1], (unsigned long long)c_ch_t);

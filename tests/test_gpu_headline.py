@@ -45,7 +45,7 @@ def _report(hit, t, ref):
     return f"ids equal {same_id:.6%}, max rel t err {rel.max() if rel.size else 0:.3g}"
 
 
-@pytest.mark.parametrize("cfg,flags", [(3, 3), (3, 7), (4, 7)])
+@pytest.mark.parametrize("cfg,flags", [(3, 3), (3, 7), (4, 7), (3, 71)])
 def test_headline_full_frame_parity(cfg, flags):
     w = make_workload(cfg)
     tr = tracer_for(w, flags=flags)
@@ -60,7 +60,8 @@ def test_headline_full_frame_parity(cfg, flags):
         assert st["rays"][seg] == rs["rays"][seg] and st["chunks"][seg] == rs["chunks"][seg], seg
         assert np.array_equal(st["tests"][seg], rs["tests"][seg]), (seg, st["tests"][seg], rs["tests"][seg])
         assert np.array_equal(st["hits"][seg], rs["hits"][seg]), (seg, st["hits"][seg], rs["hits"][seg])
-        for k in ("mesh_tests", "mesh_hits", "final_tests", "final_hits", "rays_hit", "brute"):
+        for k in ("mesh_tests", "mesh_hits", "final_tests", "final_hits", "rays_hit", "brute", "cluster_tests",
+                  "cluster_hits"):
             assert st[k][seg] == rs[k][seg], (k, seg, st[k][seg], rs[k][seg])
     segs = [s for s, _, _ in oracle.segments(w.P, w.lights.shape[0], w.ray_types)]
     tp = ref["taps"]

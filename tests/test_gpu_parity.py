@@ -42,7 +42,8 @@ def assert_counts_equal(st, ref):
         assert st["rays"][seg] == ref["stats"]["rays"][seg]
         assert np.array_equal(st["tests"][seg], ref["stats"]["tests"][seg]), (seg, st["tests"][seg], ref["stats"]["tests"][seg])
         assert np.array_equal(st["hits"][seg], ref["stats"]["hits"][seg]), (seg, st["hits"][seg], ref["stats"]["hits"][seg])
-        for k in ("mesh_tests", "mesh_hits", "final_tests", "final_hits", "rays_hit", "brute"):
+        for k in ("mesh_tests", "mesh_hits", "final_tests", "final_hits", "rays_hit", "brute", "cluster_tests",
+                  "cluster_hits"):
             assert st[k][seg] == ref["stats"][k][seg], (k, seg, st[k][seg], ref["stats"][k][seg])
 
 
@@ -73,9 +74,13 @@ def test_scene_prep_matches_oracle():
     assert np.array_equal(ts.view(np.uint32), prep.tri_sph.view(np.uint32))
     ms = crsh.debug_tap(tr.scene, crsh.TAP_MESH_SPHERES)
     assert np.array_equal(ms, prep.mesh_sph[:w.n_meshes])
+    # object sphere-tree (NEXT-4, reading O1): cluster order and spheres
+    assert np.array_equal(crsh.debug_tap(tr.scene, crsh.TAP_CLUSTER_ORDER), prep.cluster_order[:prep.M])
+    cs = crsh.debug_tap(tr.scene, crsh.TAP_CLUSTER_SPHERES)
+    assert np.array_equal(cs.view(np.uint32), prep.cluster_sph[:prep.n_clusters].view(np.uint32))
 
 
-@pytest.mark.parametrize("flags", [3, 7, 0, 1])
+@pytest.mark.parametrize("flags", [3, 7, 0, 1, 67, 71])
 def test_cfg1_full_parity(flags):
     """cfg1 (128x128 SH, ~1k-tri Cornell box, Lv 3): every intermediate tap,
     all counts and every hit bit-exact; CRSH, Z-order, RAH and sort-only."""
@@ -95,11 +100,13 @@ def test_micro_scenes(seed):
                    n_meshes=int(r.integers(1, 40)), n_lights=int(r.integers(0, 5)), ray_types=int(r.integers(1, 8)),
                    levels=int(r.integers(1, 5)), leaf_size=int(2 ** r.integers(1, 7)),
                    branching=int(2 ** r.integers(1, 5)), empty_frac=float(r.uniform(0, 0.6)))
-    flags = int(r.choice([3, 7, 0, 2, 1]))
+    flags = int(r.choice([3, 7, 0, 2, 1, 67, 71, 66]))
     tr, hit, t, ref = run_both(w, flags)
     prep = oracle.ScenePrep(w.tris, w.mesh_ids)
     assert np.array_equal(crsh.debug_tap(tr.scene, crsh.TAP_SCENE_CONSTS), prep.consts)
     assert np.array_equal(crsh.debug_tap(tr.scene, crsh.TAP_MESH_SPHERES), prep.mesh_sph[:w.n_meshes])
+    assert np.array_equal(crsh.debug_tap(tr.scene, crsh.TAP_CLUSTER_SPHERES).view(np.uint32),
+                          prep.cluster_sph[:prep.n_clusters].view(np.uint32))
     assert np.array_equal(hit, ref["hit_tri"]) and np.array_equal(t.view(np.uint32), ref["t"].view(np.uint32))
     assert_counts_equal(crsh.stats(tr.scene), ref)
     assert_taps_equal(tr, ref, w)
@@ -109,10 +116,11 @@ def test_micro_scenes(seed):
     assert np.array_equal(hit[ok], bt)
 
 
+@pytest.mark.parametrize("flags", [3, 71])
 @pytest.mark.parametrize("item_tris", [None, "16384"])
 @pytest.mark.parametrize("levels,leaf,branch", [(1, 8, 8), (1, 64, 4), (3, 4, 4), (3, 16, 8), (4, 8, 8), (2, 32, 2),
                                                 (2, 2, 16)])
-def test_option_space_many_triangles(levels, leaf, branch, item_tris, monkeypatch):
+def test_option_space_many_triangles(levels, leaf, branch, item_tris, flags, monkeypatch):
     """cfg2's 70k-triangle scene at 96x96 over the option space: work items
     of thousands of triangles (several slices per warp, queues refilled and
     drained many times), both the shared-memory (group <= 512 rays) and the
@@ -122,12 +130,12 @@ def test_option_space_many_triangles(levels, leaf, branch, item_tris, monkeypatc
     if item_tris:
         monkeypatch.setenv("CRSH_ITEM_TRIS", item_tris)
     w = make_workload(2, width=96, height=96, levels=levels, leaf_size=leaf, branching=branch)
-    tr, hit, t, ref = run_both(w, crsh.F_SORT | crsh.F_MESH_CULL, taps=False)
+    tr, hit, t, ref = run_both(w, flags, taps=False)
     assert np.array_equal(hit, ref["hit_tri"]) and np.array_equal(t.view(np.uint32), ref["t"].view(np.uint32))
     assert_counts_equal(crsh.stats(tr.scene), ref)
 
 
-@pytest.mark.parametrize("flags", [3, 7])
+@pytest.mark.parametrize("flags", [3, 7, 71])
 def test_cfg2_full_parity(flags):
     """cfg2 (512x512 SH+RE, ~70k tris / 16 meshes, Lv 2) at full size: all
     hits, counts and the sort permutation exact against the oracle."""
@@ -426,7 +434,8 @@ def test_dynamic_scene_parity(cfg, seed):
         assert np.array_equal(crsh.debug_tap(scene, crsh.TAP_TRI_SPHERES).view(np.uint32), prep.tri_sph.view(np.uint32))
         assert np.array_equal(crsh.debug_tap(scene, crsh.TAP_MESH_SPHERES), prep.mesh_sph[:prep.n_meshes])
         # primary pass on the moved scene, then its secondary frame
-        opts = crsh.make_opts(w.levels, w.leaf_size, w.branching, 3)
+        fl = 3 if k == 0 else 3 | crsh.F_OBJTREE
+        opts = crsh.make_opts(w.levels, w.leaf_size, w.branching, fl)
         pos = torch.empty(3 * P, dtype=torch.float32, device="cuda")
         nrm = torch.empty(3 * P, dtype=torch.float32, device="cuda")
         mat = torch.empty(P, dtype=torch.int32, device="cuda")
@@ -434,7 +443,7 @@ def test_dynamic_scene_parity(cfg, seed):
         pt = torch.empty(P, dtype=torch.float32, device="cuda")
         crsh.primary_gbuffer(scene, cam, W, H, tm, opts, pos, nrm, mat, ph, pt)
         rpos, rnrm, rmat, rhit, rt, _ = oracle.primary_gbuffer(tris, w.mesh_ids, w.tri_mat, cam, W, H, w.levels,
-                                                               w.leaf_size, w.branching, 3, prep=prep)
+                                                               w.leaf_size, w.branching, fl, prep=prep)
         assert np.array_equal(ph.cpu().numpy(), rhit) and np.array_equal(mat.cpu().numpy(), rmat)
         wm = dataclasses.replace(w, tris=tris, width=W, height=H, pos=rpos, nrm=rnrm, mat=rmat)
         hits = crsh.make_hits(W, H, pos, nrm, mat, torch.as_tensor(w.materials).cuda(), w.materials.shape[0], w.eye)
@@ -443,7 +452,9 @@ def test_dynamic_scene_parity(cfg, seed):
         t = torch.empty(slots, dtype=torch.float32, device="cuda")
         crsh.trace_secondary(scene, hits, w.lights, w.ray_types, opts, hit, t)
         torch.cuda.synchronize()
-        ref = oracle.trace(wm, prep)
+        ref = oracle.trace(wm, prep, flags=fl)
+        assert np.array_equal(crsh.debug_tap(scene, crsh.TAP_CLUSTER_SPHERES).view(np.uint32),
+                              prep.cluster_sph[:prep.n_clusters].view(np.uint32))
         assert np.array_equal(hit.cpu().numpy(), ref["hit_tri"])
         assert np.array_equal(t.cpu().numpy().view(np.uint32), ref["t"].view(np.uint32))
         assert_counts_equal(crsh.stats(scene), ref)
@@ -463,7 +474,7 @@ def test_option_extremes(levels, leaf, branch, lights, item_tris, monkeypatch):
     w = make_workload(1, width=40, height=36, levels=levels, leaf_size=leaf, branching=branch, ray_types=1)
     r = np.random.default_rng(lights)
     w.lights = np.stack([r.uniform(1, 9, lights), r.uniform(8.5, 9.5, lights), r.uniform(1, 9, lights)], 1).astype(np.float32)
-    tr, hit, t, ref = run_both(w, crsh.F_SORT | crsh.F_MESH_CULL)
+    tr, hit, t, ref = run_both(w, crsh.F_SORT | crsh.F_MESH_CULL | (crsh.F_OBJTREE if item_tris else 0))
     assert len(ref["stats"]["tests"]) == 3 and ref["stats"]["rays"][0] > 0
     assert np.array_equal(hit, ref["hit_tri"]) and np.array_equal(t.view(np.uint32), ref["t"].view(np.uint32))
     assert_counts_equal(crsh.stats(tr.scene), ref)
