@@ -9,6 +9,20 @@
 
 namespace crsh {
 
+// Checked build (-DCRSH_CHECKED=1, tools/build_ab.sh checked -DCRSH_CHECKED=1):
+// device-side bounds checks of every indexed write of the hot kernels; the
+// first failing check's id is kept in g_crsh_check and reported by crsh_stats
+// as CRSH_ECUDA. The stand-in for compute-sanitizer memcheck, which is closed
+// on this GPU pool (B200_PROFILING.md); compiled out otherwise.
+#ifndef CRSH_CHECKED
+#define CRSH_CHECKED 0
+#endif
+__device__ unsigned int g_crsh_check = 0u;
+#define CRSH_CHECK(cond, id)                                                     \
+  do {                                                                           \
+    if (CRSH_CHECKED && !(cond)) atomicCAS(&::crsh::g_crsh_check, 0u, (unsigned)(id)); \
+  } while (0)
+
 constexpr int MAX_SEG = 3;
 constexpr int MAX_LEVELS = 8;
 

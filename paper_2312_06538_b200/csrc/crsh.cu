@@ -611,6 +611,7 @@ crsh_status enqueue_frame(crsh_scene* sc, const FrameInfo& fi, const crsh_primar
       PlanArgs p{};
       p.fd = fd; p.group_rays = fi.GR; p.n_seg = fi.n_seg; p.gstat = sc->gstat.as<uint4>(); p.counters = counters;
       p.item_tris = fi.item_tris;
+      p.items_cap = (uint32_t)std::min<uint64_t>(sc->items.cap / 16, 0xFFFFFFFFull);
       p.items = sc->items.as<uint4>();
       p.status = reinterpret_cast<unsigned long long*>(zb + Z.st_plan); p.ticket = tickets + T_PLAN;
       k_plan<<<cdiv(std::max<uint64_t>(fi.G_max, 1), SCAN_TILE), SCAN_THREADS, 0, st>>>(p);
@@ -633,7 +634,7 @@ crsh_status enqueue_frame(crsh_scene* sc, const FrameInfo& fi, const crsh_primar
         t.tri_order = sc->cl_order.as<int32_t>(); t.tri_sph_ord = sc->tri_sph_ord.as<float4>();
         t.mesh_cluster_first = sc->cl_first.as<uint32_t>(); t.cluster_sph = sc->cl_sph.as<float4>();
       }
-      t.items = sc->items.as<uint4>(); t.fd = fd; t.ticket = tickets + T_TRAV;
+      t.items = sc->items.as<uint4>(); t.fd = fd; t.ticket = tickets + T_TRAV; t.M = (uint32_t)sc->M;
       t.best = sc->best.as<unsigned long long>(); t.counters = counters; t.n_seg = fi.n_seg;
       const bool small = fi.GR <= SMALL_GROUP_RAYS;
       const TravSmem L = TravSmem::make(fi.K, B, sc->n_meshes, Lv, small, t.per_group, fi.GR);
@@ -664,6 +665,7 @@ crsh_status enqueue_frame(crsh_scene* sc, const FrameInfo& fi, const crsh_primar
       a.fd = fd; a.group_rays = fi.GR; a.n_seg = fi.n_seg;
       a.sorted_slot = sc->sorted_slot.as<uint32_t>(); a.best = sc->best.as<unsigned long long>();
       a.out_hit = out_hit; a.out_t = out_t; a.out_packed = out_packed; a.peer = peer; a.counters = counters;
+      a.n_slots = (uint32_t)S;
       k_unpack<<<cdiv(std::max<uint64_t>(fi.Np_max, 1), 256), 256, 0, st>>>(a);
       CK(cudaGetLastError());
       ++nl;
@@ -866,6 +868,11 @@ crsh_status sync_frame(crsh_scene* sc) {
   CK(cudaSetDevice(sc->device));
   CK(cudaStreamSynchronize(sc->last_stream));
   if (sc->gstream) CK(cudaStreamSynchronize(sc->gstream));
+  if (CRSH_CHECKED) {   // checked build: the first failed device bounds check (common.cuh)
+    unsigned int chk = 0;
+    CK(cudaMemcpyFromSymbol(&chk, g_crsh_check, sizeof chk));
+    if (chk) return fail(CRSH_ECUDA, "device bounds check %u failed (checked build)", chk);
+  }
   if (sc->dist) {
     ncclResult_t ae = ncclSuccess;
     NCK(ncclCommGetAsyncError(sc->dist->comm, &ae));

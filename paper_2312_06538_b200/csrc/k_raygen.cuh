@@ -143,6 +143,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_raygen(const RaygenArgs a) {
     const uint32_t slot = tile * SCAN_TILE + it * SCAN_THREADS + threadIdx.x;
     const uint32_t pos = prefix + s_excl[it * 8 + warp] + __popc(ballot[it] & lt);
     if ((ballot[it] >> lane) & 1u) {
+      CRSH_CHECK(pos < a.n_slots, 101);
       a.keys_c[pos] = key[it];
       a.vals_c[pos] = slot;
     }

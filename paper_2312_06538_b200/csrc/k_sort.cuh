@@ -57,6 +57,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_rle(const RleArgs a) {
     const uint32_t i = tile * SCAN_TILE + it * SCAN_THREADS + threadIdx.x;
     if ((ballot[it] >> lane) & 1u) {
       const uint32_t c = prefix + s_excl[it * 8 + warp] + __popc(ballot[it] & lt);
+      CRSH_CHECK(c < N, 201);
       a.ckey[c] = key[it];
       a.cbase[c] = i;
       for (int s = 0; s < a.n_seg; ++s)
@@ -284,6 +285,7 @@ __global__ void __launch_bounds__(SORT_THREADS, CRSH_SORT_MINB) k_onesweep(const
     if (idx < n) {
       const uint32_t d = (k[it] >> shift) & 255u;
       const uint32_t pos = s_bin_excl[d] + s_whist[warp * RADIX_BINS + d] + rank[it];
+      CRSH_CHECK(pos < (uint32_t)SORT_TILE, 302);
       s_keys[pos] = k[it];
       s_vals[pos] = v[it];
     }
@@ -294,6 +296,7 @@ __global__ void __launch_bounds__(SORT_THREADS, CRSH_SORT_MINB) k_onesweep(const
     const uint32_t key = s_keys[j];
     const uint32_t d = (key >> shift) & 255u;
     const uint32_t out = seg0 + s_base[d] + (j - s_bin_excl[d]);
+    CRSH_CHECK(out < seg0 + n && j >= s_bin_excl[d], 301);
     a.keys_out[out] = key;
     a.vals_out[out] = s_vals[j];
   }
@@ -399,6 +402,7 @@ __global__ void __launch_bounds__(256) k_expand(const ExpandArgs a) {
     const uint32_t src = __ldg(a.cbase + __ldg(a.scidx + c)) + (o - s_pos[lo]);
     const int s = seg_of(segc, a.n_seg, o);
     const uint32_t dst = segp[s] + (o - segc[s]);
+    CRSH_CHECK(dst < a.fd->Np && src < N && c < C, 401);
     a.sorted_key[dst] = __ldg(a.skey + c);
     a.sorted_slot[dst] = __ldg(a.vals_c + src);
   }

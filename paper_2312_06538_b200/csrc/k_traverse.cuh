@@ -200,6 +200,7 @@ struct PlanArgs {
   const uint4* gstat;          // k_group_work: {triangles, mesh tests, mesh passes, 0} per group
   unsigned long long* counters;
   uint32_t item_tris;
+  uint32_t items_cap;          // capacity of items (checked builds)
   uint4* items;                // (group, v_begin, v_end, 0)
   unsigned long long* status;
   uint32_t* ticket;
@@ -263,8 +264,10 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_plan(const PlanArgs a) {
   for (int it = 0; it < SCAN_ITEMS; ++it) {
     const uint32_t g = g_lo + tile * SCAN_TILE + it * SCAN_THREADS + threadIdx.x;
     const uint32_t off = prefix + s_excl[it * 8 + warp] + wex[it];
-    for (uint32_t q = 0; q < nit[it]; ++q)
+    for (uint32_t q = 0; q < nit[it]; ++q) {
+      CRSH_CHECK(off + q < a.items_cap, 701);
       a.items[off + q] = make_uint4(g, q * a.item_tris, min(ntri[it], (q + 1) * a.item_tris), 0u);
+    }
   }
   if (tile == n_tiles - 1 && threadIdx.x == 0) {
     uint32_t t = 0;
@@ -343,6 +346,7 @@ struct TravArgs {
   const uint32_t* mesh_cluster_first;
   const float4* cluster_sph;
   const uint4* items;
+  uint32_t M;                         // triangles (checked builds)
   const FrameDesc* fd;                // n_items, seg_pad_base (group starts)
   uint32_t* ticket;
   unsigned long long* best;           // [Np]
@@ -456,6 +460,8 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
   uint2* q = reinterpret_cast<uint2*>(smraw + L.off_q) + warp * L.q_warp;
   uint32_t* qlen = s_qlen[warp];
   constexpr bool QREG = LVT != 0;
+  // queue capacity of level k per warp (TravSmem: levels packed in order, q_warp in all)
+  auto qcap = [&](int k) -> uint32_t { return (k < Lv ? s_qoff[k + 1] : L.q_warp) - s_qoff[k]; };
   uint32_t q1n = 0;   // QREG: length of Q[1]
   auto qget = [&](int k) -> uint32_t { return (QREG && k == 1) ? q1n : qlen[k]; };
   auto qset = [&](int k, uint32_t v) {   // all 32 lanes, between __syncwarp()s
@@ -627,6 +633,7 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
           return s_rays[(uint32_t)k * RAY_PLANE + ray_rix(rl >> 1)];
         };
         const uint32_t nr = min((uint32_t)B0, g_real - rl0);   // real rays of the bundle (>= 1: the bundle exists)
+        CRSH_CHECK(rl0 < g_real && rl0 + (uint32_t)B0 <= a.group_rays && e.y < a.M, 804);
         c_mt_t += nr;   // every real ray of the bundle is tested against the triangle
         // a padding ray (odd nr: the partner of the last real ray) has
         // tmin = tmax = -1 (k_leaves), so no t passes tmin < t < tmax: it
@@ -713,6 +720,7 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
       const uint32_t bt = __ballot_sync(CRSH_FULL, test);
       const uint32_t b = __ballot_sync(CRSH_FULL, pass);
       const uint32_t q1 = qget(k - 1);
+      CRSH_CHECK(!pass || q1 + __popc(b & lt) < qcap(k - 1), 801);
       if (pass) q[s_qoff[k - 1] + q1 + __popc(b & lt)] = out;
       __syncwarp();
       qset(k - 1, q1 + __popc(b));
@@ -786,6 +794,7 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
         const uint32_t b = __ballot_sync(CRSH_FULL, pass);
         if (Lv == 1) {   // the top level is the bundle level: queue for the final tests
           const uint32_t ql = qget(1);
+          CRSH_CHECK(!pass || ql + __popc(b & lt) < qcap(1), 802);
           if (pass) q[s_qoff[1] + ql + __popc(b & lt)] = make_uint2((uint32_t)j, tri);
           __syncwarp();
           qset(1, ql + __popc(b));
@@ -829,6 +838,7 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
         }
         const uint32_t tot = __shfl_sync(CRSH_FULL, incl, 31);
         const uint32_t ql0 = qget(k1);
+        CRSH_CHECK(ql0 + tot <= qcap(k1), 803);
         uint2* qd = q + s_qoff[k1] + ql0 + (incl - cnt);
         while (m) {
           const uint32_t c = __ffs(m) - 1;
@@ -1019,6 +1029,7 @@ struct UnpackArgs {
   unsigned long long* out_packed;
   PeerOut peer;                 // fused multi-GPU epilogue: store owned results into every destination
   unsigned long long* counters;
+  uint32_t n_slots;             // checked builds
 };
 
 __global__ void __launch_bounds__(256) k_unpack(const UnpackArgs a) {
@@ -1034,6 +1045,7 @@ __global__ void __launch_bounds__(256) k_unpack(const UnpackArgs a) {
     for (int q = 1; q < a.n_seg; ++q) s = (i >= a.fd->seg_pad_base[q]) ? q : s;
     if (i - a.fd->seg_pad_base[s] < a.fd->seg_n[s]) {
       const uint32_t slot = __ldg(a.sorted_slot + i);
+      CRSH_CHECK(slot < a.n_slots, 901);
       const unsigned long long b = __ldg(a.best + i);
       const bool hit = b != BEST_NONE;
       if (a.peer.n) {
