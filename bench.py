@@ -120,7 +120,10 @@ def frame_flops(st):
 
 
 def trav_flops(st):
-    return int(np.asarray(st["tests"]).sum()) * EQ9_FLOPS + int(sum(st["final_tests"])) * MT_FLOPS
+    """FP32 work of k_traverse: Eq 9 tests of every level (and of the object
+    tree's clusters) and Moller-Trumbore tests, from the frame's counters."""
+    eq9 = int(np.asarray(st["tests"]).sum()) + int(sum(st.get("cluster_tests", [0])))
+    return eq9 * EQ9_FLOPS + int(sum(st["final_tests"])) * MT_FLOPS
 
 
 def load_traffic(config, zorder, kernel="k_traverse"):
@@ -235,11 +238,24 @@ def measure(w, flags, args, local, world, flush, clocks=None):
     import paper_2312_06538_b200 as crsh
     from paper_2312_06538_b200.api import tracer_for
     tr = tracer_for(w, device=local, flags=flags | crsh.F_KERNEL_TIMING)
-    if world > 1:
+    if args.dist_on:
         tr.dist_init()
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
         tr.run(stream)
+    merge_check = None
+    if args.dist_on:   # the merged frame (every rank) equals this rank's own world-1 frame, bit for bit
+        torch.cuda.synchronize()
+        h, t = tr.hit_tri.clone(), tr.t.clone()
+        ref = tracer_for(w, device=local, flags=flags)
+        ref.run(stream)
+        torch.cuda.synchronize()
+        ok = torch.tensor([1 if (torch.equal(h, ref.hit_tri) and torch.equal(t.view(torch.int32), ref.t.view(torch.int32)))
+                           else 0], dtype=torch.int32)
+        import torch.distributed as dist
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        merge_check = "merged frame == world-1 frame on every rank" if int(ok) == 1 else "MISMATCH"
+        del ref, h, t
     _barrier(world)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     trav = 0.0
@@ -262,7 +278,7 @@ def measure(w, flags, args, local, world, flush, clocks=None):
     del tr
     # per-stage breakdown (diagnostic, outside the timed region): all stage events
     trs = tracer_for(w, device=local, flags=flags | crsh.F_STAGE_TIMING)
-    if world > 1:
+    if args.dist_on:
         trs.dist_init()
     stage = np.zeros(8)
     for k in range(4):
@@ -274,7 +290,7 @@ def measure(w, flags, args, local, world, flush, clocks=None):
     del trs
     total_ms, trav_ms, *stage = _max_over_ranks([total_ms, trav / args.steps, *stage.tolist()], world)
     return dict(total_ms=total_ms, ms=total_ms / args.steps, trav_ms=trav_ms, stage=stage, st=st,
-                launches=launches, merge=merge)
+                launches=launches, merge=merge, merge_check=merge_check)
 
 
 def config_dict(w, zorder, world, merge, objtree=False):
@@ -296,10 +312,18 @@ def run_crsh(args):
 
     rank, world, local = env_rank()
     torch.cuda.set_device(local)
+    args.dist_on = world > 1 or args.force_dist
     if world > 1:
         # host plumbing only (NCCL id broadcast, barriers, max over ranks): the
         # data path is libcrsh's own NCCL communicator (crsh_dist_init)
         dist.init_process_group("gloo")
+    elif args.force_dist:   # the N > 1 code path with a world-1 NCCL communicator (tests)
+        import socket
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+        sk.close()
+        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
     base = crsh.F_SORT | crsh.F_MESH_CULL | (crsh.F_OBJTREE if args.objtree else 0)
     w = make_workload(args.config)
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device="cuda")
@@ -307,13 +331,16 @@ def run_crsh(args):
     main_z = bool(args.zorder)
     m = measure(w, base | (crsh.F_ZORDER if main_z else 0), args, local, world, flush, clk)
     other = None if args.single_hash else measure(w, base | (0 if main_z else crsh.F_ZORDER), args, local, world, flush)
+    # NEXT-4 beside it: the Z-order hash with the object sphere-tree (reading O1)
+    ztree = None if (args.single_hash or args.objtree) else measure(
+        w, base | crsh.F_ZORDER | crsh.F_OBJTREE, args, local, world, flush)
     st = m["st"]
     rays = int(sum(st["rays"]))
     mrays = rays * args.steps / (m["total_ms"] * 1e-3) / 1e6
     # end to end through the public API with HOST buffers (crsh_trace_secondary_host):
     # G-buffer H2D from pinned memory and hit_tri / t D2H inside the timed region
     tr = tracer_for(w, device=local, flags=base | (crsh.F_ZORDER if main_z else 0))
-    if world > 1:
+    if args.dist_on:
         tr.dist_init()
     stream = torch.cuda.current_stream()
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
@@ -341,7 +368,8 @@ def run_crsh(args):
            "api": "crsh_trace_secondary_host"}
     del tr
     if rank != 0:
-        dist.destroy_process_group()
+        if args.dist_on:
+            dist.destroy_process_group()
         return
     peaks = measured_peaks()
     clocks = clk.summary()
@@ -358,7 +386,8 @@ def run_crsh(args):
         s_ = mm["st"]
         fl = trav_flops(s_) / world          # per GPU: each rank traverses its share
         a_ = fl / (mm["trav_ms"] * 1e-3) / 1e12 if mm["trav_ms"] > 0 else 0.0
-        fl_s = (int(np.asarray(s_["tests"]).sum()) * 28 + int(sum(s_["final_tests"])) * 55) / world
+        fl_s = ((int(np.asarray(s_["tests"]).sum()) + int(sum(s_.get("cluster_tests", [0])))) * 28 +
+                int(sum(s_["final_tests"])) * 55) / world
         a_s = fl_s / (mm["trav_ms"] * 1e-3) / 1e12 if mm["trav_ms"] > 0 else 0.0
         return a_, a_s
 
@@ -404,6 +433,7 @@ def run_crsh(args):
                            "model": "t_roof = a1-a8 bytes / HBM peak + traversal flops per GPU / FP32 peak"},
         },
         "gpu_launches": m["launches"],
+        "merge_check": m["merge_check"],
         "e2e": e2e,
         "paper_context": paper_context(),
         "clocks": clocks,
@@ -424,12 +454,24 @@ def run_crsh(args):
                                   "hbm_stages_ms": round(oms, 4),
                                   "stage_ms": {n: round(v, 4) for n, v in zip(crsh.STAGES, other["stage"])}}
         out["gpu_launches"] += other["launches"]
+    if ztree is not None:
+        sz = ztree["st"]
+        rz = int(sum(sz["rays"]))
+        tz = int(np.asarray(sz["tests"]).sum()) + int(sum(sz["final_tests"]))
+        za, _ = kernel_roof(ztree)
+        out["value_zorder_objtree"] = round(rz * args.steps / (ztree["total_ms"] * 1e-3) / 1e6, 3)
+        out["ms_per_step_zorder_objtree"] = round(ztree["ms"], 4)
+        out["tests_per_ray_zorder_objtree"] = round(tz / max(rz, 1), 2)
+        out["cluster_tests_zorder_objtree"] = int(sum(sz["cluster_tests"]))
+        out["roofline_zorder_objtree"] = {"k_traverse_frac": round(za / peak_tflops, 4),
+                                          "stage_ms": {n: round(v, 4) for n, v in zip(crsh.STAGES, ztree["stage"])}}
+        out["gpu_launches"] += ztree["launches"]
     if world == 1 and not args.no_cpu_baseline:
         cr, cs, rows, cores = oracle_sample(w, base | (crsh.F_ZORDER if main_z else 0))
         out["cpu_baseline"] = {"value": round(cr / cs / 1e6, 5), "unit": "Mrays/s", "cores": cores, "kind": "oracle",
                                "sample": f"{rows} of {w.height} image rows (centre band), {cr} rays, {cs:.1f} s"}
     print(json.dumps(out), flush=True)
-    if world > 1:
+    if args.dist_on:
         dist.destroy_process_group()
 
 
@@ -673,6 +715,8 @@ def main():
     ap.add_argument("--nccl-merge", action="store_true", help="N > 1: NCCL MIN all-reduce merge instead of the fused peer stores")
     ap.add_argument("--single-hash", action="store_true", help="skip the second hash layout's extra keys")
     ap.add_argument("--objtree", action="store_true", help="object sphere-tree below the mesh spheres (NEXT-4)")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="run the N > 1 path (crsh_dist_init, in-library merge) even at N = 1 (tests)")
     ap.add_argument("--table4", action="store_true", help="CRSH vs RAH vs N x M report (not the contract line)")
     ap.add_argument("--sweep", action="store_true", help="cfg5 depth/bundle sweep (not the contract line)")
     ap.add_argument("--whitted", type=int, default=None, metavar="D",

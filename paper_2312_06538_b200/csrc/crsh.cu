@@ -555,6 +555,7 @@ crsh_status enqueue_frame(crsh_scene* sc, const FrameInfo& fi, const crsh_primar
       a.fd = fd; a.n_seg = fi.n_seg;
       a.sorted_slot = sc->sorted_slot.as<uint32_t>(); a.rays = sc->rays.as<float4>();
       a.sorted_rays = sc->sorted_rays.as<float4>(); a.nodes = nodes; a.trav = trav;
+      a.write_sorted = fi.GR <= SMALL_GROUP_RAYS ? 0 : 1;   // smem groups gather their rays in K8
       const uint32_t grid = cdiv(std::max<uint64_t>(fi.level_max[1], 1), 128);
       CK(dispatch_b0(B0, [&](auto b0) {
         k_leaves<decltype(b0)::value><<<grid, 128, 0, st>>>(a);
@@ -627,6 +628,7 @@ crsh_status enqueue_frame(crsh_scene* sc, const FrameInfo& fi, const crsh_primar
       for (int k = Lv; k >= 1; --k) { t.per_group[k] = (uint32_t)(fi.K * per); per *= B; }
       for (int k = 1; k <= Lv; ++k) t.trav[k] = trav + 3 * fi.level_off[k];
       t.sorted_rays = sc->sorted_rays.as<float4>(); t.tri_e = sc->tri_e.as<float4>();
+      t.sorted_slot = sc->sorted_slot.as<uint32_t>(); t.rays = sc->rays.as<float4>();
       t.tri_sph = sc->tri_sph.as<float4>();
       t.masks = sc->masks.as<uint32_t>(); t.W = W; t.n_meshes = sc->n_meshes;
       t.mesh_first = sc->mesh_first.as<uint32_t>(); t.mesh_count = sc->mesh_count.as<uint32_t>();
@@ -1525,7 +1527,17 @@ crsh_status crsh_debug_tap(crsh_scene_t sc, int32_t tap, int32_t seg_type, int32
       }
       case CRSH_TAP_SORTED_KEYS: src = sc->sorted_key.as<uint32_t>() + fd.seg_pad_base[s]; n = ns; break;
       case CRSH_TAP_SORTED_SLOTS: src = sc->sorted_slot.as<uint32_t>() + fd.seg_pad_base[s]; n = ns; break;
-      case CRSH_TAP_SORTED_RAYS: src = sc->sorted_rays.as<float4>() + 2 * (size_t)fd.seg_pad_base[s]; n = ns; esz = 32; break;
+      case CRSH_TAP_SORTED_RAYS:
+        src = sc->sorted_rays.as<float4>() + 2 * (size_t)fd.seg_pad_base[s]; n = ns; esz = 32;
+        if (fi.GR <= SMALL_GROUP_RAYS && ns) {   // not materialised (K8 gathers): gather them here
+          CK(ensure(sc->stage_out, 32 * ns));
+          k_gather_sorted<<<cdiv(ns, 256), 256>>>(sc->sorted_slot.as<uint32_t>() + fd.seg_pad_base[s],
+                                                  sc->rays.as<float4>(), (uint32_t)ns, sc->stage_out.as<float4>());
+          CK(cudaGetLastError());
+          CK(cudaDeviceSynchronize());
+          src = sc->stage_out.p;
+        }
+        break;
       case CRSH_TAP_NODES: {
         if (level < 1 || level > fi.Lv) return fail(CRSH_EINVAL, "bad level");
         uint64_t per = fi.B0;

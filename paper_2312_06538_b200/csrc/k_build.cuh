@@ -139,7 +139,8 @@ struct LeafArgs {
   int32_t n_seg;
   const uint32_t* sorted_slot;
   const float4* rays;                     // [slots][2]
-  float4* sorted_rays;                    // [Np][2]
+  float4* sorted_rays;                    // [Np][2]; written only if write_sorted
+  int32_t write_sorted;                   // 0: K8 gathers its groups' rays by sorted_slot itself (groups in smem)
   float4* nodes;                          // level 1, paper layout [2 per node]
   float4* trav;                           // level 1, traversal layout [3 per node]
 };
@@ -205,8 +206,10 @@ __global__ void __launch_bounds__(128) k_leaves(const LeafArgs a) {
       r0 = make_float4(0.f, 0.f, 0.f, -1.0f);   // padding ray: tmin = -1
       r1 = make_float4(0.f, 0.f, 1.f, -1.0f);
     }
-    a.sorted_rays[2 * (size_t)(p0 + i)] = r0;
-    a.sorted_rays[2 * (size_t)(p0 + i) + 1] = r1;
+    if (a.write_sorted) {
+      a.sorted_rays[2 * (size_t)(p0 + i)] = r0;
+      a.sorted_rays[2 * (size_t)(p0 + i) + 1] = r1;
+    }
     sc[i] = mk3(r0.x, r0.y, r0.z);
     sr[i] = (i < real) ? 0.0f : -1.0f;
     if (i == 0) o0 = sc[0];
@@ -239,6 +242,17 @@ __global__ void __launch_bounds__(128) k_leaves(const LeafArgs a) {
   const bool so = real > 0 && same && __float_as_uint(n.c.x) == __float_as_uint(o0.x) &&
                   __float_as_uint(n.c.y) == __float_as_uint(o0.y) && __float_as_uint(n.c.z) == __float_as_uint(o0.z);
   store_node(a.nodes, a.trav, j, n, so);
+}
+
+// sorted rays of a segment for the CRSH_TAP_SORTED_RAYS tap when K5 did not
+// write them: padded position i <- rays[sorted_slot[i]]
+__global__ void k_gather_sorted(const uint32_t* __restrict__ sorted_slot, const float4* __restrict__ rays, uint32_t n,
+                                float4* __restrict__ out) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t slot = sorted_slot[i];
+    out[2 * (size_t)i] = rays[2 * (size_t)slot];
+    out[2 * (size_t)i + 1] = rays[2 * (size_t)slot + 1];
+  }
 }
 
 struct UpperArgs {

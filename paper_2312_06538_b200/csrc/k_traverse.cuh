@@ -332,7 +332,9 @@ struct TravArgs {
   uint32_t group_rays;
   const float4* trav[MAX_LEVELS + 1]; // level k (1..Lv), traversal layout
   uint32_t per_group[MAX_LEVELS + 1]; // nodes per group at level k
-  const float4* sorted_rays;
+  const float4* sorted_rays;          // !SMALL groups: rays in sorted (padded) order
+  const uint32_t* sorted_slot;        // SMALL groups: the group's rays are gathered by slot
+  const float4* rays;                 //   from the generation order ([slots][2])
   const float4* tri_e;
   const float4* tri_sph;
   const uint32_t* masks;
@@ -433,7 +435,7 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
   uint32_t* s_exm = reinterpret_cast<uint32_t*>(smraw + L.off_exm);
   float4* s_pairs = reinterpret_cast<float4*>(smraw + L.off_pairs);
   float4* s_tpairs = reinterpret_cast<float4*>(smraw + L.off_tpairs);
-  __shared__ uint32_t s_item, s_cur_g, s_n_act, s_carry, s_carry_c;
+  __shared__ uint32_t s_item, s_cur_g, s_n_act, s_carry, s_carry_c, s_blk;
   __shared__ uint32_t s_warp[TRAV_WARPS];
   __shared__ unsigned long long s_ctr[MAX_SEG * CTR_STRIDE];
   __shared__ uint32_t s_qlen[TRAV_WARPS][MAX_LEVELS + 1];
@@ -516,12 +518,17 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
           for (uint32_t j = tid; j < n4; j += TRAV_THREADS) sn[s_noff[k] + j] = __ldg(src + j);
         }
         // the group's rays as paired records (rays 2i, 2i+1) for mt2_ns, in
-        // ray planes (ray_rix above)
+        // ray planes (ray_rix above), gathered from the generation order by
+        // the sort permutation (K5 does not write a sorted copy for these
+        // groups); padding rays (past the group's real rays) are tmin = tmax = -1
         float4* sr = reinterpret_cast<float4*>(smraw + L.off_rays);
-        const float4* rs = a.sorted_rays + 2 * (size_t)g * a.group_rays;
+        const uint32_t* ss = a.sorted_slot + (size_t)g * a.group_rays;
         for (uint32_t pp = tid; pp < a.group_rays / 2u; pp += TRAV_THREADS) {
-          const float4 a0 = __ldg(rs + 4 * pp), a1 = __ldg(rs + 4 * pp + 1), b0 = __ldg(rs + 4 * pp + 2),
-                       b1 = __ldg(rs + 4 * pp + 3);
+          float4 a0 = make_float4(0.f, 0.f, 0.f, -1.0f), a1 = make_float4(0.f, 0.f, 1.f, -1.0f), b0 = a0, b1 = a1;
+          const uint32_t r = 2u * pp;
+          const uint32_t sl0 = r < g_real ? __ldg(ss + r) : 0u, sl1 = r + 1u < g_real ? __ldg(ss + r + 1) : 0u;
+          if (r < g_real) { a0 = __ldg(a.rays + 2 * (size_t)sl0); a1 = __ldg(a.rays + 2 * (size_t)sl0 + 1); }
+          if (r + 1u < g_real) { b0 = __ldg(a.rays + 2 * (size_t)sl1); b1 = __ldg(a.rays + 2 * (size_t)sl1 + 1); }
           float4* rp = sr + ray_rix(pp);
           rp[0] = make_float4(a0.x, b0.x, a0.y, b0.y);
           rp[RAY_PLANE] = make_float4(a0.z, b0.z, a0.w, b0.w);
@@ -604,6 +611,7 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
     if (SMALL) {
       for (uint32_t r = tid; r < a.group_rays; r += TRAV_THREADS) s_best[r] = BEST_NONE;
     }
+    if (OBJ && tid == 0) s_blk = 0u;
     __syncthreads();
     const uint32_t n_act = s_n_act;
     const size_t rbase = (size_t)g * a.group_rays;
@@ -877,7 +885,14 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
       const uint32_t CPB = 32u / (uint32_t)K;   // K <= 32
       const uint32_t ci = lane / (uint32_t)K, jn = lane - ci * (uint32_t)K;
       const uint32_t kmask = K == 32 ? 0xFFFFFFFFu : ((1u << K) - 1u);
-      for (uint32_t b0 = cy + warp * CPB; b0 < cz; b0 += TRAV_WARPS * CPB) {
+      // blocks are handed out dynamically (a shared counter per item): the
+      // clusters that pass are unevenly spread, and static striding left
+      // warps waiting at the item barrier (ncu cfg4: barrier stalls)
+      for (;;) {
+        uint32_t bi = 0;
+        if (lane == 0) bi = atomicAdd(&s_blk, 1u);
+        const uint32_t b0 = cy + __shfl_sync(CRSH_FULL, bi, 0) * CPB;
+        if (b0 >= cz) break;
         const uint32_t c = b0 + ci;
         uint32_t lo = 0;
         bool tst = false, pass = false;

@@ -51,3 +51,17 @@ def test_reference_line_on_host():
     _common(d)
     assert d["impl"] == "reference"
     assert d["cpu_baseline"]["kind"] == "oracle" and d["e2e"]["h2d_bytes_per_step"] == 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode,name", [("peer", "fused-peer-stores"), ("nccl", "nccl-allreduce-min")])
+def test_product_line_dist_path(mode, name, monkeypatch):
+    """The N > 1 code path of bench.py (gloo host group, crsh_dist_init, the
+    library's merge inside every timed frame) with a world-1 NCCL communicator:
+    the line reports the merge that ran, and the merged frame equals the
+    rank's own world-1 frame bit for bit."""
+    monkeypatch.setenv("CRSH_DIST_MERGE", mode)
+    d = _run("--force-dist", "--config", "2", "--single-hash", "--no-cpu-baseline", "--steps", "3")
+    assert d["config"]["merge"] == name
+    assert d["merge_check"] == "merged frame == world-1 frame on every rank"
+    assert d["value"] > 0 and d["e2e"]["value"] > 0

@@ -58,6 +58,8 @@ def assert_taps_equal(tr, ref, w):
             assert np.array_equal(crsh.debug_tap(tr.scene, crsh.TAP_CHUNK_BASE, seg), tp["cbase"][i])
         assert np.array_equal(crsh.debug_tap(tr.scene, crsh.TAP_SORTED_KEYS, seg), tp["skey"][i])
         assert np.array_equal(crsh.debug_tap(tr.scene, crsh.TAP_SORTED_SLOTS, seg), tp["sslot"][i])
+        sr = crsh.debug_tap(tr.scene, crsh.TAP_SORTED_RAYS, seg)   # gathered by the permutation (K8's view)
+        assert np.array_equal(sr.view(np.uint32), ref["rays"][tp["sslot"][i].astype(np.int64)].view(np.uint32))
         for k in range(1, w.levels + 1):
             g = crsh.debug_tap(tr.scene, crsh.TAP_NODES, seg, k)
             o = tp["levels"][i][k - 1]
