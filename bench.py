@@ -182,7 +182,7 @@ def oracle_band(w, flags, rows, prep=None):
     return int(sum(out["stats"]["rays"])), time.perf_counter() - t0
 
 
-def oracle_sample(w, flags, target_s=12.0):
+def oracle_sample(w, flags, target_s=20.0):
     """Grow a centre band of image rows until one oracle run takes about
     target_s seconds of host CPU work (or the whole image); returns (rays,
     seconds, rows, cores)."""

@@ -267,7 +267,7 @@ struct crsh_scene {
   Buf tri_e, tri_sph, mesh_sph, mesh_first, mesh_count;
   std::vector<float> h_mesh_sph;
   // per-frame arena (grow-only; `gen` counts reallocations, which invalidate the graph)
-  Buf rays, keys_c, vals_c, ckey, cbase, k1, v1, k2, v2, pos, first_chunk, sorted_key, sorted_slot, sorted_rays,
+  Buf rays, keys_c, vals_c, ckey, cbase, k1, v1, k2, v2, pos, first_chunk, sorted_key, sorted_slot, sorted_rays, px_tiles,
       nodes, trav, masks, gwork, gstat, items, best, zero, stage_in, stage_out;
   uint64_t gen = 0;
   unsigned long long* h_counters = nullptr;   // pinned
@@ -305,7 +305,7 @@ cudaError_t grow(crsh_scene* sc, Buf& b, size_t bytes) {
 
 // zero region layout (bytes), sized by the slot bound; reset at every frame
 struct ZeroLayout {
-  size_t fd, counters, tickets, hist, st_rg, st_rle, st_scan, st_plan, st_radix, radix_tiles_cap, total;
+  size_t fd, counters, tickets, hist, st_rg, st_rle, st_scan, st_plan, st_radix, radix_tiles_cap, px_total, total;
   static ZeroLayout make(uint64_t S, uint64_t G_max) {
     ZeroLayout z;
     size_t o = 0;
@@ -322,6 +322,7 @@ struct ZeroLayout {
     z.st_scan = take(8 * scan_tiles);
     z.st_plan = take(8 * plan_tiles);
     z.st_radix = take(4 * SORT_PASSES * z.radix_tiles_cap * RADIX_BINS);
+    z.px_total = take(4 * 4);
     z.total = o;
     return z;
   }
@@ -459,11 +460,27 @@ crsh_status enqueue_frame(crsh_scene* sc, const FrameInfo& fi, const crsh_primar
     a.peer = peer;
     a.status = reinterpret_cast<unsigned long long*>(zb + Z.st_rg); a.ticket = tickets + T_RG;
     a.fd = fd;
-    k_raygen<<<cdiv(S, SCAN_TILE), SCAN_THREADS, 0, st>>>(a);
-    CK(cudaGetLastError());
+    if (fi.in_rays || std::getenv("CRSH_SLOT_MAJOR")) {   // given ray batches: slot-major with look-back
+      k_raygen<<<cdiv(S, SCAN_TILE), SCAN_THREADS, 0, st>>>(a);
+      CK(cudaGetLastError());
+      ++nl;
+    } else {   // G-buffer frames: pixel-major (count, then rank + generate)
+      PxArgs px{};
+      px.rg = a;
+      for (int t = 0; t < 3; ++t) px.seg_of_type[t] = -1;
+      for (int s = 0; s < fi.n_seg; ++s) px.seg_of_type[fi.seg_type[s]] = s;
+      px.tile_cnt = sc->px_tiles.as<uint32_t>();
+      px.total = reinterpret_cast<uint32_t*>(zb + Z.px_total);
+      const uint32_t tiles = cdiv((uint64_t)h->width * h->height, PX_TILE);
+      k_raygen_count<<<tiles, SCAN_THREADS, 0, st>>>(px);
+      CK(cudaGetLastError());
+      k_raygen_px<<<tiles, SCAN_THREADS, 0, st>>>(px);
+      CK(cudaGetLastError());
+      nl += 2;
+    }
     k_frame_plan<<<1, 32, 0, st>>>(fd, fi.n_seg, fi.GR, (uint32_t)B0, (uint32_t)B, Lv);
     CK(cudaGetLastError());
-    nl += 2;
+    ++nl;
   }
   CK(mark(1));
 
@@ -569,7 +586,7 @@ crsh_status enqueue_frame(crsh_scene* sc, const FrameInfo& fi, const crsh_primar
       a.child_nodes = nodes + 2 * fi.level_off[k - 1];
       a.nodes = nodes + 2 * fi.level_off[k];
       a.trav = trav + 3 * fi.level_off[k];
-      const uint32_t grid = cdiv(std::max<uint64_t>(fi.level_max[k], 1), 128);
+      const uint32_t grid = cdiv(std::max<uint64_t>(fi.level_max[k] * (uint64_t)B, 1), 128);   // lane per child
       CK(dispatch_b(B, [&](auto b) {
         k_upper<decltype(b)::value><<<grid, 128, 0, st>>>(a);
         return cudaGetLastError();
@@ -799,6 +816,7 @@ crsh_status trace_impl(crsh_scene* sc, const crsh_primary_hits* h, const float* 
   const uint64_t items_cap = std::max<uint64_t>(fi.G_max, 1) * cdiv(std::max<int64_t>(sc->M, 1), fi.item_tris);
   CK(grow(sc, sc->zero, Z.total));
   CK(grow(sc, sc->rays, 32 * S));
+  CK(grow(sc, sc->px_tiles, 12 * ((size_t)cdiv((uint64_t)h->width * h->height, PX_TILE) + 1)));
   CK(grow(sc, sc->keys_c, 4 * S));
   CK(grow(sc, sc->vals_c, 4 * S));
   if (!fi.brute) {
@@ -1095,7 +1113,7 @@ void crsh_scene_destroy(crsh_scene_t sc) {
   cudaSetDevice(sc->device);
   Buf* bufs[] = {&sc->tri_e, &sc->tri_sph, &sc->mesh_sph, &sc->mesh_first, &sc->mesh_count, &sc->rays, &sc->keys_c,
                  &sc->vals_c, &sc->ckey, &sc->cbase, &sc->k1, &sc->v1, &sc->k2, &sc->v2, &sc->pos, &sc->first_chunk,
-                 &sc->sorted_key, &sc->sorted_slot, &sc->sorted_rays, &sc->nodes, &sc->trav, &sc->masks, &sc->gwork, &sc->gstat, &sc->items,
+                 &sc->sorted_key, &sc->sorted_slot, &sc->sorted_rays, &sc->px_tiles, &sc->nodes, &sc->trav, &sc->masks, &sc->gwork, &sc->gstat, &sc->items,
                  &sc->best, &sc->zero, &sc->stage_in, &sc->stage_out};
   for (Buf* b : bufs) b->release();
   for (auto& w : sc->wb) for (auto& b : w) b.release();

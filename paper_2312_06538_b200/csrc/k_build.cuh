@@ -264,20 +264,36 @@ struct UpperArgs {
 };
 
 // K6: node j = balanced pairwise union (Eqs 5-8, R9, R11) of children
-// [j*B, (j+1)*B); empty children pass through.
+// [j*B, (j+1)*B); empty children pass through. A segmented warp reduction
+// (BASELINE north_star: "sphere-cone merge done as segmented warp reductions
+// per level"): lane = child (coalesced child loads), 32 / B parents per warp;
+// step w exchanges with lane ^ w and both lanes form union(lower, upper), so
+// after log2 B steps every lane of the segment holds the union in exactly the
+// balanced order ((0,1),(2,3)),((4,5),(6,7)) of R9; lane 0 of each segment
+// writes the parent. B = 32 is one parent per warp. (The leaf level, K5, stays
+// thread-per-bundle: its cone is a SEQUENTIAL fold of Eqs 1-4 over the
+// bundle's rays in sorted order, not a reduction.)
+__device__ __forceinline__ NodeV shfl_xor_node(const NodeV& n, int w) {
+  NodeV o;
+  o.c = mk3(__shfl_xor_sync(CRSH_FULL, n.c.x, w), __shfl_xor_sync(CRSH_FULL, n.c.y, w), __shfl_xor_sync(CRSH_FULL, n.c.z, w));
+  o.r = __shfl_xor_sync(CRSH_FULL, n.r, w);
+  o.a = mk3(__shfl_xor_sync(CRSH_FULL, n.a.x, w), __shfl_xor_sync(CRSH_FULL, n.a.y, w), __shfl_xor_sync(CRSH_FULL, n.a.z, w));
+  o.alpha = __shfl_xor_sync(CRSH_FULL, n.alpha, w);
+  return o;
+}
 template <int B>
 __global__ void __launch_bounds__(128) k_upper(const UpperArgs a) {
-  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= a.fd->level_n[a.level]) return;
-  NodeV st[B];
-#pragma unroll
-  for (int i = 0; i < B; ++i) st[i] = load_node(a.child_nodes, (size_t)j * B + i);
+  const uint32_t gl = blockIdx.x * blockDim.x + threadIdx.x;   // global lane = child index
+  const uint32_t n_par = a.fd->level_n[a.level];
+  if ((gl & ~31u) >= n_par * (uint32_t)B) return;   // warp-uniform: the whole warp is past the level
+  const uint32_t lane = gl & 31u;
+  NodeV v = gl < n_par * (uint32_t)B ? load_node(a.child_nodes, gl) : empty_node();
 #pragma unroll
   for (int w = 1; w < B; w *= 2) {
-#pragma unroll
-    for (int i = 0; i < B; i += 2 * w) st[i] = node_union_ns(st[i], st[i + w]);
+    const NodeV o = shfl_xor_node(v, w);
+    v = (lane & (uint32_t)w) ? node_union_ns(o, v) : node_union_ns(v, o);   // union(lower lane, upper lane)
   }
-  store_node(a.nodes, a.trav, j, st[0]);
+  if ((lane & (uint32_t)(B - 1)) == 0u && gl < n_par * (uint32_t)B) store_node(a.nodes, a.trav, gl / B, v);
 }
 
 // ---------------------------------------------------------------- dynamic scenes

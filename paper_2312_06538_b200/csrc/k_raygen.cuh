@@ -46,6 +46,65 @@ struct RaygenArgs {
   FrameDesc* fd;                      // out: seg_comp_start[0..n_seg]
 };
 
+// One G-buffer pixel: material and position, loaded once per pixel.
+struct Pix {
+  int m;
+  f3 x;
+};
+__device__ __forceinline__ bool load_pix(const RaygenArgs& a, uint32_t p, Pix& px) {
+  px.m = __ldg(a.mat + p);
+  if (px.m < 0 || px.m >= a.n_mat) return false;
+  const size_t P = (size_t)a.P;
+  px.x = mk3(__ldg(a.pos + p), __ldg(a.pos + P + p), __ldg(a.pos + 2 * P + p));
+  return true;
+}
+// shadow ray of light l, origin inverted to the light
+__device__ __forceinline__ void gen_sh(const RaygenArgs& a, const Pix& px, uint32_t l, float4& r0, float4& r1,
+                                       uint32_t& key) {
+  const f3 L = mk3(a.lights[3 * l], a.lights[3 * l + 1], a.lights[3 * l + 2]);
+  const f3 v = px.x - L;
+  const float len = len3(v);
+  const f3 d = len > 0.0f ? v * (1.0f / len) : mk3(0.0f, 0.0f, 1.0f);
+  r0 = make_float4(L.x, L.y, L.z, a.eps_t);
+  r1 = make_float4(d.x, d.y, d.z, len - a.eps_t);
+  key = hash_shadow_ns(l, d, a.zorder != 0);
+}
+// reflection (type 1) / refraction (type 2) ray of pixel p; false if the
+// material emits none (or total internal reflection). VALID_ONLY: the same
+// decision without the ray (the pixel-major generator's counting pass).
+template <bool VALID_ONLY>
+__device__ __forceinline__ bool gen_bounce(const RaygenArgs& a, const Pix& px, uint32_t p, int type, float4& r0,
+                                           float4& r1, uint32_t& key) {
+  const int m = px.m;
+  const size_t P = (size_t)a.P;
+  const float refl = __ldg(a.materials + 3 * m), trans = __ldg(a.materials + 3 * m + 1);
+  if (type == 1 && !(refl > 0.0f)) return false;     // reflection iff reflectivity > 0
+  if (type == 2 && !(trans > 0.0f)) return false;    // refraction iff transmissivity > 0 (and no TIR)
+  if (VALID_ONLY && type == 1) return true;
+  const f3 i = a.dir ? mk3(__ldg(a.dir + p), __ldg(a.dir + P + p), __ldg(a.dir + 2 * P + p))
+                     : norm3(px.x - mk3(a.eye[0], a.eye[1], a.eye[2]));
+  f3 n = mk3(__ldg(a.nrm + p), __ldg(a.nrm + P + p), __ldg(a.nrm + 2 * P + p));
+  f3 d;
+  if (type == 1) {
+    if (dot3(i, n) > 0.0f) n = neg3(n);
+    const float k2 = 2.0f * dot3(i, n);
+    d = norm3(mk3(__fmaf_rn(-k2, n.x, i.x), __fmaf_rn(-k2, n.y, i.y), __fmaf_rn(-k2, n.z, i.z)));
+  } else {   // Snell
+    const float ior = __ldg(a.materials + 3 * m + 2);
+    float c = -dot3(i, n), eta;
+    if (c < 0.0f) { n = neg3(n); c = -c; eta = ior; } else { eta = 1.0f / ior; }
+    const float k = 1.0f - (eta * eta) * (1.0f - c * c);
+    if (k < 0.0f) return false;
+    if (VALID_ONLY) return true;
+    const float t1 = eta * c - sqrtf(k);
+    d = norm3(mk3(__fmaf_rn(eta, i.x, t1 * n.x), __fmaf_rn(eta, i.y, t1 * n.y), __fmaf_rn(eta, i.z, t1 * n.z)));
+  }
+  r0 = make_float4(px.x.x, px.x.y, px.x.z, a.eps_t);
+  r1 = make_float4(d.x, d.y, d.z, __int_as_float(0x7f800000));
+  key = hash_bounce_ns(px.x, d, a.box_min, a.box_ext, a.zorder != 0);
+  return true;
+}
+
 __device__ __forceinline__ bool gen_ray(const RaygenArgs& a, uint32_t slot, float4& r0, float4& r1, uint32_t& key) {
   if (a.in_rays) {   // given rays (primary pass, external batches): bounce-type hash, empty iff !(tmax > tmin)
     r0 = __ldg(a.in_rays + 2 * (size_t)slot);
@@ -63,44 +122,13 @@ __device__ __forceinline__ bool gen_ray(const RaygenArgs& a, uint32_t slot, floa
     l = local / (uint32_t)a.P;
     p = local - l * (uint32_t)a.P;
   }
-  const int m = __ldg(a.mat + p);
-  if (m < 0 || m >= a.n_mat) return false;
-  const size_t P = (size_t)a.P;
-  const f3 x = mk3(__ldg(a.pos + p), __ldg(a.pos + P + p), __ldg(a.pos + 2 * P + p));
-  if (type == 0) {   // shadow ray, origin inverted to the light
-    const f3 L = mk3(a.lights[3 * l], a.lights[3 * l + 1], a.lights[3 * l + 2]);
-    const f3 v = x - L;
-    const float len = len3(v);
-    const f3 d = len > 0.0f ? v * (1.0f / len) : mk3(0.0f, 0.0f, 1.0f);
-    r0 = make_float4(L.x, L.y, L.z, a.eps_t);
-    r1 = make_float4(d.x, d.y, d.z, len - a.eps_t);
-    key = hash_shadow_ns(l, d, a.zorder != 0);
+  Pix px;
+  if (!load_pix(a, p, px)) return false;
+  if (type == 0) {
+    gen_sh(a, px, l, r0, r1, key);
     return true;
   }
-  const float refl = __ldg(a.materials + 3 * m), trans = __ldg(a.materials + 3 * m + 1);
-  const f3 i = a.dir ? mk3(__ldg(a.dir + p), __ldg(a.dir + P + p), __ldg(a.dir + 2 * P + p))
-                     : norm3(x - mk3(a.eye[0], a.eye[1], a.eye[2]));
-  f3 n = mk3(__ldg(a.nrm + p), __ldg(a.nrm + P + p), __ldg(a.nrm + 2 * P + p));
-  f3 d;
-  if (type == 1) {   // reflection, iff reflectivity > 0
-    if (!(refl > 0.0f)) return false;
-    if (dot3(i, n) > 0.0f) n = neg3(n);
-    const float k2 = 2.0f * dot3(i, n);
-    d = norm3(mk3(__fmaf_rn(-k2, n.x, i.x), __fmaf_rn(-k2, n.y, i.y), __fmaf_rn(-k2, n.z, i.z)));
-  } else {           // refraction (Snell), iff transmissivity > 0 and no TIR
-    if (!(trans > 0.0f)) return false;
-    const float ior = __ldg(a.materials + 3 * m + 2);
-    float c = -dot3(i, n), eta;
-    if (c < 0.0f) { n = neg3(n); c = -c; eta = ior; } else { eta = 1.0f / ior; }
-    const float k = 1.0f - (eta * eta) * (1.0f - c * c);
-    if (k < 0.0f) return false;
-    const float t1 = eta * c - sqrtf(k);
-    d = norm3(mk3(__fmaf_rn(eta, i.x, t1 * n.x), __fmaf_rn(eta, i.y, t1 * n.y), __fmaf_rn(eta, i.z, t1 * n.z)));
-  }
-  r0 = make_float4(x.x, x.y, x.z, a.eps_t);
-  r1 = make_float4(d.x, d.y, d.z, __int_as_float(0x7f800000));
-  key = hash_bounce_ns(x, d, a.box_min, a.box_ext, a.zorder != 0);
-  return true;
+  return gen_bounce<false>(a, px, p, type, r0, r1, key);
 }
 
 __global__ void __launch_bounds__(SCAN_THREADS) k_raygen(const RaygenArgs a) {
@@ -158,6 +186,167 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_raygen(const RaygenArgs a) {
       return t;
     }();
     a.fd->seg_comp_start[a.n_seg] = total;
+  }
+}
+
+}  // namespace crsh
+
+namespace crsh {
+
+// ============================================================== K1, pixel-major (G-buffer frames)
+// The same rays, keys and compaction as k_raygen, computed per PIXEL instead
+// of per slot: a pixel's G-buffer entry is read once for its L shadow rays
+// and its reflection / refraction rays (the slot-major kernel decoded every
+// slot -- an integer division -- and re-read the pixel L + 2 times). The
+// compacted position of a ray is known without a look-back: in slot order a
+// shadow ray of light l of pixel p sits at l * V_sh + rank_sh(p) (a pixel
+// emits a shadow ray for every light or none, R4), a reflection ray at the
+// segment start + rank_re(p), a refraction ray at its segment start +
+// rank_rr(p), where V are the frame's counts and rank the count of emitting
+// pixels before p. K1a counts per tile, K1b sums the preceding tiles' counts
+// (ranks) and generates. Compaction order = slot order, exactly as k_raygen.
+constexpr int PX_ITEMS = 8;
+constexpr uint32_t PX_TILE = SCAN_THREADS * PX_ITEMS;   // pixels per tile
+
+struct PxArgs {
+  RaygenArgs rg;
+  int32_t seg_of_type[3];        // segment index of SH / RE / RR, -1 if absent
+  uint32_t* tile_cnt;            // [3][n_tiles]: emitting pixels per tile and type
+  uint32_t* total;               // [3]: emitting pixels per type (zeroed per frame)
+};
+
+__device__ __forceinline__ void px_flags(const PxArgs& a, uint32_t p, bool& sh, bool& re, bool& rr) {
+  Pix px;
+  sh = re = rr = false;
+  if (!load_pix(a.rg, p, px)) return;
+  float4 r0, r1;
+  uint32_t key;
+  sh = a.seg_of_type[0] >= 0 && a.rg.n_lights > 0;
+  re = a.seg_of_type[1] >= 0 && gen_bounce<true>(a.rg, px, p, 1, r0, r1, key);
+  rr = a.seg_of_type[2] >= 0 && gen_bounce<true>(a.rg, px, p, 2, r0, r1, key);
+}
+
+// K1a: emitting pixels per tile and type
+__global__ void __launch_bounds__(SCAN_THREADS) k_raygen_count(const PxArgs a) {
+  __shared__ uint32_t s_c[3];
+  if (threadIdx.x < 3) s_c[threadIdx.x] = 0u;
+  __syncthreads();
+  uint32_t c[3] = {0u, 0u, 0u};
+  for (int it = 0; it < PX_ITEMS; ++it) {
+    const uint32_t p = blockIdx.x * PX_TILE + it * SCAN_THREADS + threadIdx.x;
+    bool f[3] = {false, false, false};
+    if (p < (uint32_t)a.rg.P) px_flags(a, p, f[0], f[1], f[2]);
+    for (int t = 0; t < 3; ++t) c[t] += __popc(__ballot_sync(CRSH_FULL, f[t]));
+  }
+  if (lane_id() == 0)
+    for (int t = 0; t < 3; ++t) atomicAdd(&s_c[t], c[t]);
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    a.tile_cnt[threadIdx.x * gridDim.x + blockIdx.x] = s_c[threadIdx.x];
+    atomicAdd(a.total + threadIdx.x, s_c[threadIdx.x]);
+  }
+}
+
+// K1b: ranks from the preceding tiles' counts, then every ray of the tile's pixels
+__global__ void __launch_bounds__(SCAN_THREADS) k_raygen_px(const PxArgs a) {
+  __shared__ uint32_t s_cnt[3][PX_ITEMS * 8], s_excl[3][PX_ITEMS * 8];
+  __shared__ uint32_t s_red[3][SCAN_THREADS / 32];
+  const RaygenArgs& g = a.rg;
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5, lt = lanemask_lt();
+  const uint32_t P = (uint32_t)g.P, tile = blockIdx.x;
+  // frame counts and segment starts (slot order: SH of all lights, RE, RR)
+  const uint32_t L = (uint32_t)g.n_lights;
+  const uint32_t vt[3] = {__ldcg(a.total), __ldcg(a.total + 1), __ldcg(a.total + 2)};
+  uint32_t seg_start[3] = {0u, 0u, 0u};
+  {
+    uint32_t acc = 0;
+    for (int s = 0; s < g.n_seg; ++s) {
+      const int t = g.seg_type[s];
+      for (int q = 0; q < 3; ++q) seg_start[q] = (q == t) ? acc : seg_start[q];
+      acc += (t == 0) ? L * vt[0] : vt[t];
+      if (tile == 0 && threadIdx.x == 0) g.fd->seg_comp_start[s + 1] = acc;
+    }
+    if (tile == 0 && threadIdx.x == 0) g.fd->seg_comp_start[0] = 0u;
+  }
+  // emitting pixels of the preceding tiles, per type
+  uint32_t pre[3] = {0u, 0u, 0u};
+  for (uint32_t q = threadIdx.x; q < tile; q += SCAN_THREADS)
+    for (int t = 0; t < 3; ++t) pre[t] += __ldcg(a.tile_cnt + t * gridDim.x + q);
+  for (int t = 0; t < 3; ++t) {
+    const uint32_t v = __reduce_add_sync(CRSH_FULL, pre[t]);
+    if (lane == 0) s_red[t][warp] = v;
+  }
+  // this tile's flags and their (item, warp) counts
+  bool f[PX_ITEMS][3];
+  uint32_t bal[PX_ITEMS][3];
+#pragma unroll
+  for (int it = 0; it < PX_ITEMS; ++it) {
+    const uint32_t p = tile * PX_TILE + it * SCAN_THREADS + threadIdx.x;
+    f[it][0] = f[it][1] = f[it][2] = false;
+    if (p < P) px_flags(a, p, f[it][0], f[it][1], f[it][2]);
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      bal[it][t] = __ballot_sync(CRSH_FULL, f[it][t]);
+      if (lane == 0) s_cnt[t][it * 8 + warp] = __popc(bal[it][t]);
+    }
+  }
+  __syncthreads();
+  if (warp < 3) {   // exclusive scan of the 64 (item, warp) counts of type `warp`
+    const uint32_t x0 = s_cnt[warp][2 * lane], x1 = s_cnt[warp][2 * lane + 1];
+    uint32_t incl = x0 + x1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(CRSH_FULL, incl, o);
+      if ((int)lane >= o) incl += y;
+    }
+    s_excl[warp][2 * lane] = incl - (x0 + x1);
+    s_excl[warp][2 * lane + 1] = incl - x1;
+  }
+  __syncthreads();
+  uint32_t base[3];
+  for (int t = 0; t < 3; ++t) {
+    uint32_t b = 0;
+    for (int w = 0; w < SCAN_THREADS / 32; ++w) b += s_red[t][w];
+    base[t] = b;
+  }
+  // generate: shadow rays of every light, then the bounce rays
+#pragma unroll 1
+  for (int it = 0; it < PX_ITEMS; ++it) {
+    const uint32_t p = tile * PX_TILE + it * SCAN_THREADS + threadIdx.x;
+    if (p >= P) break;
+    uint32_t rank[3];
+    for (int t = 0; t < 3; ++t) rank[t] = base[t] + s_excl[t][it * 8 + warp] + __popc(bal[it][t] & lt);
+    Pix px;
+    if (!load_pix(g, p, px)) px.m = -1;   // no primary hit: every slot of the pixel is empty
+    for (int t = 0; t < 3; ++t) {
+      const int s = a.seg_of_type[t];
+      if (s < 0) continue;
+      const uint32_t n_r = (t == 0) ? L : 1u;
+      for (uint32_t l = 0; l < n_r; ++l) {
+        const uint32_t slot = g.seg_slot_start[s] + l * P + p;
+        float4 r0, r1;
+        uint32_t key = 0;
+        bool ok = false;
+        if (f[it][t]) {
+          if (t == 0) { gen_sh(g, px, l, r0, r1, key); ok = true; }
+          else ok = gen_bounce<false>(g, px, p, t, r0, r1, key);
+          CRSH_CHECK(ok, 103);   // the counting pass decided with the same code
+        }
+        if (ok) {
+          g.rays[2 * (size_t)slot] = r0;
+          g.rays[2 * (size_t)slot + 1] = r1;
+          const uint32_t pos = seg_start[t] + ((t == 0) ? l * vt[0] : 0u) + rank[t];
+          CRSH_CHECK(pos < g.n_slots, 102);
+          g.keys_c[pos] = key;
+          g.vals_c[pos] = slot;
+        } else if (g.out_hit) {
+          g.out_hit[slot] = -2;
+          g.out_t[slot] = __int_as_float(0x7f800000);
+        }
+        if (g.out_packed) g.out_packed[slot] = 0x7FFFFFFFFFFFFFFFull;
+        if (g.peer.n && !ok) g.peer.store(slot, 0x7FFFFFFFFFFFFFFFull);
+      }
+    }
   }
 }
 
