@@ -114,21 +114,26 @@ __device__ __forceinline__ unsigned long long lb_load(const unsigned long long* 
 // compress 18.9 -> 16.2 us; neutral at cfg4, where the tiles are bound by
 // their own work (k_raygen: ~370 instructions per slot of IEEE div/sqrt and
 // the hash polynomial).
+// NE = (item, warp) entries of s_cnt (SCAN_ITEMS * 8 by default; a multiple of 32).
+template <int NE = SCAN_ITEMS * 8>
 __device__ __forceinline__ uint32_t tile_scan_lookback_block(const uint32_t* s_cnt, uint32_t* s_excl, uint32_t* s_prefix,
                                                              unsigned long long* status, int tile) {
   __shared__ uint32_t s_lb_total, s_lb_stop, s_lb_red[32];
   const int tid = (int)threadIdx.x, lane = (int)lane_id(), warp = tid >> 5, nw = (int)(blockDim.x >> 5);
   if (warp == 0) {
-    const uint32_t a = s_cnt[2 * lane], b = s_cnt[2 * lane + 1];
-    uint32_t incl = a + b;
+    constexpr int PER = NE / 32;
+    uint32_t x[PER], sum = 0;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) { x[q] = s_cnt[PER * lane + q]; sum += x[q]; }
+    uint32_t incl = sum;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t y = __shfl_up_sync(CRSH_FULL, incl, o);
       if (lane >= o) incl += y;
     }
-    const uint32_t ex = incl - (a + b);
-    s_excl[2 * lane] = ex;
-    s_excl[2 * lane + 1] = ex + a;
+    uint32_t run = incl - sum;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) { s_excl[PER * lane + q] = run; run += x[q]; }
     const uint32_t total = __shfl_sync(CRSH_FULL, incl, 31);
     if (lane == 0) {
       s_lb_total = total;

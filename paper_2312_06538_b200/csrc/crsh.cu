@@ -252,6 +252,8 @@ struct FrameInfo {
   uint64_t level_max[MAX_LEVELS + 1] = {0};
   uint32_t flags = 0;
   uint32_t item_tris = 2048;                // triangles per traversal work item (item_tris_for)
+  bool big_tiles = false;                   // k_rle / k_scan_sizes with 8192-entry tiles (large frames)
+  bool rle_hist = true;                     // k_rle builds the radix digit histograms (no k_radix_hist pass)
   int rank = 0, world = 1;
   bool sorted = false, timed = false, ktimed = false, brute = false;
   const float4* in_rays = nullptr;          // ray-batch mode (crsh_trace_rays)
@@ -399,6 +401,7 @@ struct CallKey {
   crsh_opts o;
   uint64_t gen;
   uint32_t item_tris;
+  uint32_t tiles;
 };
 
 // The ray-definition part of K1's arguments (G-buffer, lights, slot layout);
@@ -471,10 +474,18 @@ crsh_status enqueue_frame(crsh_scene* sc, const FrameInfo& fi, const crsh_primar
       for (int s = 0; s < fi.n_seg; ++s) px.seg_of_type[fi.seg_type[s]] = s;
       px.tile_cnt = sc->px_tiles.as<uint32_t>();
       px.total = reinterpret_cast<uint32_t*>(zb + Z.px_total);
-      const uint32_t tiles = cdiv((uint64_t)h->width * h->height, PX_TILE);
-      k_raygen_count<<<tiles, SCAN_THREADS, 0, st>>>(px);
-      CK(cudaGetLastError());
-      k_raygen_px<<<tiles, SCAN_THREADS, 0, st>>>(px);
+      const uint64_t P = (uint64_t)h->width * h->height;
+      if (P >= PX_SMALL_FRAME) {
+        const uint32_t tiles = cdiv(P, px_tile(8));
+        k_raygen_count<8><<<tiles, SCAN_THREADS, 0, st>>>(px);
+        CK(cudaGetLastError());
+        k_raygen_px<8><<<tiles, SCAN_THREADS, 0, st>>>(px);
+      } else {
+        const uint32_t tiles = cdiv(P, px_tile(2));
+        k_raygen_count<2><<<tiles, SCAN_THREADS, 0, st>>>(px);
+        CK(cudaGetLastError());
+        k_raygen_px<2><<<tiles, SCAN_THREADS, 0, st>>>(px);
+      }
       CK(cudaGetLastError());
       nl += 2;
     }
@@ -502,8 +513,11 @@ crsh_status enqueue_frame(crsh_scene* sc, const FrameInfo& fi, const crsh_primar
         RleArgs a{};
         a.fd = fd; a.keys = sc->keys_c.as<uint32_t>(); a.n_seg = fi.n_seg;
         a.ckey = sc->ckey.as<uint32_t>(); a.cbase = sc->cbase.as<uint32_t>();
+        a.hist = fi.rle_hist ? reinterpret_cast<uint32_t*>(zb + Z.hist) : nullptr;
         a.status = reinterpret_cast<unsigned long long*>(zb + Z.st_rle); a.ticket = tickets + T_RLE;
-        k_rle<<<cdiv(S, SCAN_TILE), SCAN_THREADS, 0, st>>>(a);
+        // 2048-key tiles (A/B at cfg4: 8192-key tiles 83 -> 107 us; they do pay
+        // for the decompression scan below)
+        k_rle<SCAN_ITEMS><<<cdiv(S, SCAN_TILE), SCAN_THREADS, 0, st>>>(a);
         CK(cudaGetLastError());
         k_chunk_plan<<<1, 32, 0, st>>>(fd, fi.n_seg, (uint32_t)SORT_TILE);
         CK(cudaGetLastError());
@@ -511,10 +525,12 @@ crsh_status enqueue_frame(crsh_scene* sc, const FrameInfo& fi, const crsh_primar
       }
       CK(mark(2));
       uint32_t* hist = reinterpret_cast<uint32_t*>(zb + Z.hist);
-      k_radix_hist<<<std::min<uint32_t>(cdiv(S, 256 * 8), 4 * sc->sm_count), 256, 0, st>>>(fd, fi.n_seg,
-                                                                                           sc->ckey.as<uint32_t>(), hist);
-      CK(cudaGetLastError());
-      ++nl;
+      if (!fi.rle_hist) {
+        k_radix_hist<<<std::min<uint32_t>(cdiv(S, 256 * 8), 4 * sc->sm_count), 256, 0, st>>>(fd, fi.n_seg,
+                                                                                             sc->ckey.as<uint32_t>(), hist);
+        CK(cudaGetLastError());
+        ++nl;
+      }
       const size_t sm_bytes = (2 * SORT_TILE + SORT_WARPS * RADIX_BINS) * 4;
       if (sm_bytes > 48 * 1024) CK(cudaFuncSetAttribute(k_onesweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_bytes));
       const uint32_t* kin = sc->ckey.as<uint32_t>();
@@ -538,7 +554,8 @@ crsh_status enqueue_frame(crsh_scene* sc, const FrameInfo& fi, const crsh_primar
         a.fd = fd; a.sorted_cidx = sc->v2.as<uint32_t>(); a.cbase = sc->cbase.as<uint32_t>();
         a.pos = sc->pos.as<uint32_t>(); a.first_chunk = sc->first_chunk.as<uint32_t>();
         a.status = reinterpret_cast<unsigned long long*>(zb + Z.st_scan); a.ticket = tickets + T_SCAN;
-        k_scan_sizes<<<cdiv(S, SCAN_TILE), SCAN_THREADS, 0, st>>>(a);
+        if (fi.big_tiles) k_scan_sizes<32><<<cdiv(S, SCAN_THREADS * 32), SCAN_THREADS, 0, st>>>(a);
+        else k_scan_sizes<SCAN_ITEMS><<<cdiv(S, SCAN_TILE), SCAN_THREADS, 0, st>>>(a);
         CK(cudaGetLastError());
         ++nl;
       }
@@ -812,11 +829,20 @@ crsh_status trace_impl(crsh_scene* sc, const crsh_primary_hits* h, const float* 
   for (int k = 1; k <= Lv; ++k) total_nodes += fi.level_max[k];
   const int W = (sc->n_meshes + 31) / 32;
   fi.item_tris = item_tris_for(fi.G_max, world, sc->sm_count);
+  {   // decompression-scan tile size; radix histograms built by k_rle (A/B at cfg4: scan 178 -> 162 us with
+      // 8192-entry tiles; sort 340 -> 319 us without the histogram pass). Overrides CRSH_BIG_TILES, CRSH_RLE_HIST.
+    const char* e = std::getenv("CRSH_BIG_TILES");
+    fi.big_tiles = e ? std::atoi(e) != 0 : S >= (1ull << 21);
+    const char* h2 = std::getenv("CRSH_RLE_HIST");
+    fi.rle_hist = h2 ? std::atoi(h2) != 0 : true;
+  }
+  sc->fi.big_tiles = fi.big_tiles;
+  sc->fi.rle_hist = fi.rle_hist;
   sc->fi.item_tris = fi.item_tris;
   const uint64_t items_cap = std::max<uint64_t>(fi.G_max, 1) * cdiv(std::max<int64_t>(sc->M, 1), fi.item_tris);
   CK(grow(sc, sc->zero, Z.total));
   CK(grow(sc, sc->rays, 32 * S));
-  CK(grow(sc, sc->px_tiles, 12 * ((size_t)cdiv((uint64_t)h->width * h->height, PX_TILE) + 1)));
+  CK(grow(sc, sc->px_tiles, 12 * ((size_t)cdiv((uint64_t)h->width * h->height, px_tile(2)) + 1)));
   CK(grow(sc, sc->keys_c, 4 * S));
   CK(grow(sc, sc->vals_c, 4 * S));
   if (!fi.brute) {
@@ -846,6 +872,7 @@ crsh_status trace_impl(crsh_scene* sc, const crsh_primary_hits* h, const float* 
   for (int i = 0; i < 3; ++i) key.eye[i] = h->eye[i];
   for (int i = 0; i < 3 * n_lights; ++i) key.lights[i] = lights[i];
   key.types = types; key.o = *o; key.gen = sc->gen; key.item_tris = fi.item_tris;
+  key.tiles = (fi.big_tiles ? 1u : 0u) | (fi.rle_hist ? 2u : 0u);
   std::vector<unsigned char> kb(sizeof(CallKey));
   std::memcpy(kb.data(), &key, sizeof(CallKey));
   static const bool use_graph = !std::getenv("CRSH_NO_GRAPH");

@@ -205,8 +205,11 @@ namespace crsh {
 // rank_rr(p), where V are the frame's counts and rank the count of emitting
 // pixels before p. K1a counts per tile, K1b sums the preceding tiles' counts
 // (ranks) and generates. Compaction order = slot order, exactly as k_raygen.
-constexpr int PX_ITEMS = 8;
-constexpr uint32_t PX_TILE = SCAN_THREADS * PX_ITEMS;   // pixels per tile
+// PX_ITEMS pixels per thread: 8 (2048-pixel tiles) for large frames, 2
+// (512-pixel tiles) below 2^20 pixels, where 2048-pixel tiles are fewer than
+// one wave of CTAs (cfg2: 128 tiles on 148 SMs)
+constexpr uint32_t PX_SMALL_FRAME = 1u << 20;
+__host__ __device__ constexpr uint32_t px_tile(int items) { return SCAN_THREADS * (uint32_t)items; }
 
 struct PxArgs {
   RaygenArgs rg;
@@ -227,7 +230,9 @@ __device__ __forceinline__ void px_flags(const PxArgs& a, uint32_t p, bool& sh, 
 }
 
 // K1a: emitting pixels per tile and type
+template <int PX_ITEMS>
 __global__ void __launch_bounds__(SCAN_THREADS) k_raygen_count(const PxArgs a) {
+  constexpr uint32_t PX_TILE = px_tile(PX_ITEMS);
   __shared__ uint32_t s_c[3];
   if (threadIdx.x < 3) s_c[threadIdx.x] = 0u;
   __syncthreads();
@@ -248,7 +253,9 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_raygen_count(const PxArgs a) {
 }
 
 // K1b: ranks from the preceding tiles' counts, then every ray of the tile's pixels
+template <int PX_ITEMS>
 __global__ void __launch_bounds__(SCAN_THREADS) k_raygen_px(const PxArgs a) {
+  constexpr uint32_t PX_TILE = px_tile(PX_ITEMS);
   __shared__ uint32_t s_cnt[3][PX_ITEMS * 8], s_excl[3][PX_ITEMS * 8];
   __shared__ uint32_t s_red[3][SCAN_THREADS / 32];
   const RaygenArgs& g = a.rg;
@@ -276,31 +283,46 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_raygen_px(const PxArgs a) {
     const uint32_t v = __reduce_add_sync(CRSH_FULL, pre[t]);
     if (lane == 0) s_red[t][warp] = v;
   }
-  // this tile's flags and their (item, warp) counts
-  bool f[PX_ITEMS][3];
-  uint32_t bal[PX_ITEMS][3];
+  // this tile's flags (bit 3 it + t of `fl`) and their per-warp ballots
+  // (shared memory: the generation loop below is not unrolled, and
+  // runtime-indexed register arrays would live in local memory)
+  __shared__ uint32_t s_bal[3][PX_ITEMS][SCAN_THREADS / 32];
+  uint32_t fl = 0;
 #pragma unroll
   for (int it = 0; it < PX_ITEMS; ++it) {
     const uint32_t p = tile * PX_TILE + it * SCAN_THREADS + threadIdx.x;
-    f[it][0] = f[it][1] = f[it][2] = false;
-    if (p < P) px_flags(a, p, f[it][0], f[it][1], f[it][2]);
-#pragma unroll
-    for (int t = 0; t < 3; ++t) {
-      bal[it][t] = __ballot_sync(CRSH_FULL, f[it][t]);
-      if (lane == 0) s_cnt[t][it * 8 + warp] = __popc(bal[it][t]);
+    bool f0 = false, f1 = false, f2 = false;
+    if (p < P) px_flags(a, p, f0, f1, f2);
+    fl |= (f0 ? 1u : 0u) << (3 * it) | (f1 ? 2u : 0u) << (3 * it) | (f2 ? 4u : 0u) << (3 * it);
+    const uint32_t b0 = __ballot_sync(CRSH_FULL, f0), b1 = __ballot_sync(CRSH_FULL, f1), b2 = __ballot_sync(CRSH_FULL, f2);
+    if (lane == 0) {
+      s_bal[0][it][warp] = b0; s_bal[1][it][warp] = b1; s_bal[2][it][warp] = b2;
+      s_cnt[0][it * 8 + warp] = __popc(b0); s_cnt[1][it * 8 + warp] = __popc(b1); s_cnt[2][it * 8 + warp] = __popc(b2);
     }
   }
   __syncthreads();
-  if (warp < 3) {   // exclusive scan of the 64 (item, warp) counts of type `warp`
-    const uint32_t x0 = s_cnt[warp][2 * lane], x1 = s_cnt[warp][2 * lane + 1];
-    uint32_t incl = x0 + x1;
+  if (warp < 3) {   // exclusive scan of the PX_ITEMS * 8 (item, warp) counts of type `warp`
+    constexpr int PER = PX_ITEMS * 8 / 32 > 0 ? PX_ITEMS * 8 / 32 : 1;   // entries per lane (2 or 1 with 4 unused lanes)
+    uint32_t x[PER], sum = 0;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int e = (int)lane * PER + q;
+      x[q] = e < PX_ITEMS * 8 ? s_cnt[warp][e] : 0u;
+      sum += x[q];
+    }
+    uint32_t incl = sum;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t y = __shfl_up_sync(CRSH_FULL, incl, o);
       if ((int)lane >= o) incl += y;
     }
-    s_excl[warp][2 * lane] = incl - (x0 + x1);
-    s_excl[warp][2 * lane + 1] = incl - x1;
+    uint32_t run = incl - sum;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int e = (int)lane * PER + q;
+      if (e < PX_ITEMS * 8) s_excl[warp][e] = run;
+      run += x[q];
+    }
   }
   __syncthreads();
   uint32_t base[3];
@@ -314,20 +336,21 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_raygen_px(const PxArgs a) {
   for (int it = 0; it < PX_ITEMS; ++it) {
     const uint32_t p = tile * PX_TILE + it * SCAN_THREADS + threadIdx.x;
     if (p >= P) break;
-    uint32_t rank[3];
-    for (int t = 0; t < 3; ++t) rank[t] = base[t] + s_excl[t][it * 8 + warp] + __popc(bal[it][t] & lt);
     Pix px;
     if (!load_pix(g, p, px)) px.m = -1;   // no primary hit: every slot of the pixel is empty
+#pragma unroll
     for (int t = 0; t < 3; ++t) {
       const int s = a.seg_of_type[t];
       if (s < 0) continue;
+      const bool emits = (fl >> (3 * it + t)) & 1u;
+      const uint32_t rank = base[t] + s_excl[t][it * 8 + warp] + __popc(s_bal[t][it][warp] & lt);
       const uint32_t n_r = (t == 0) ? L : 1u;
       for (uint32_t l = 0; l < n_r; ++l) {
         const uint32_t slot = g.seg_slot_start[s] + l * P + p;
         float4 r0, r1;
         uint32_t key = 0;
         bool ok = false;
-        if (f[it][t]) {
+        if (emits) {
           if (t == 0) { gen_sh(g, px, l, r0, r1, key); ok = true; }
           else ok = gen_bounce<false>(g, px, p, t, r0, r1, key);
           CRSH_CHECK(ok, 103);   // the counting pass decided with the same code
@@ -335,7 +358,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_raygen_px(const PxArgs a) {
         if (ok) {
           g.rays[2 * (size_t)slot] = r0;
           g.rays[2 * (size_t)slot + 1] = r1;
-          const uint32_t pos = seg_start[t] + ((t == 0) ? l * vt[0] : 0u) + rank[t];
+          const uint32_t pos = seg_start[t] + ((t == 0) ? l * vt[0] : 0u) + rank;
           CRSH_CHECK(pos < g.n_slots, 102);
           g.keys_c[pos] = key;
           g.vals_c[pos] = slot;

@@ -15,64 +15,96 @@ struct RleArgs {
   int32_t n_seg;
   uint32_t* ckey;                       // [C]
   uint32_t* cbase;                      // [C + 1], global compacted index of each chunk head
+  uint32_t* hist;                       // optional [3][4][256]: digit histograms of the chunk keys (zeroed)
   unsigned long long* status;
   uint32_t* ticket;
 };
+constexpr int RLE_HIST_WORDS = MAX_SEG * 4 * 256;
 
 // Head flag: 1 where the key differs from the previous pair; also at
 // every segment start so chunks never straddle two hierarchies (R5).
+// RLE_ITEMS keys per thread (32 for large frames: a quarter of the tiles, so
+// a quarter of the look-back chain). With `hist` (all segments' digit
+// histograms of the chunk keys, the radix sort's first step) the tile also
+// counts its chunk keys' digits in shared memory and adds them to the global
+// histograms -- the separate histogram pass over the chunk keys is gone.
+template <int RLE_ITEMS>
 __global__ void __launch_bounds__(SCAN_THREADS) k_rle(const RleArgs a) {
+  constexpr int NE = RLE_ITEMS * 8;
   __shared__ uint32_t s_tile, s_prefix;
-  __shared__ uint32_t s_cnt[SCAN_ITEMS * 8], s_excl[SCAN_ITEMS * 8];
+  __shared__ uint32_t s_cnt[NE], s_excl[NE];
+  __shared__ uint32_t s_hist[RLE_HIST_WORDS];
   if (threadIdx.x == 0) s_tile = atomicAdd(a.ticket, 1u);
+  if (a.hist)
+    for (int i = threadIdx.x; i < RLE_HIST_WORDS; i += SCAN_THREADS) s_hist[i] = 0u;
   __syncthreads();
   const uint32_t tile = s_tile;
   const uint32_t N = a.fd->N;
-  const uint32_t n_tiles = (N + SCAN_TILE - 1) / SCAN_TILE;
+  constexpr uint32_t TILE = (uint32_t)SCAN_THREADS * RLE_ITEMS;
+  const uint32_t n_tiles = (N + TILE - 1) / TILE;
   if (tile >= n_tiles) return;   // surplus block (grid sized from the slot bound)
+  // segment starts in registers: every loop over them is unrolled to MAX_SEG
+  // with a bound check (a runtime-indexed array would live in local memory)
   uint32_t segst[MAX_SEG + 1];
-  for (int s = 0; s <= a.n_seg; ++s) segst[s] = a.fd->seg_comp_start[s];
-  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
-  uint32_t key[SCAN_ITEMS], ballot[SCAN_ITEMS];
 #pragma unroll
-  for (int it = 0; it < SCAN_ITEMS; ++it) {
-    const uint32_t i = tile * SCAN_TILE + it * SCAN_THREADS + threadIdx.x;
+  for (int s = 0; s <= MAX_SEG; ++s) segst[s] = s <= a.n_seg ? a.fd->seg_comp_start[s] : 0xFFFFFFFFu;
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  uint32_t key[RLE_ITEMS], ballot[RLE_ITEMS];
+#pragma unroll
+  for (int it = 0; it < RLE_ITEMS; ++it) {
+    const uint32_t i = tile * TILE + it * SCAN_THREADS + threadIdx.x;
     bool head = false;
     uint32_t k = 0;
     if (i < N) {
       k = __ldg(a.keys + i);
       head = (i == 0) || (k != __ldg(a.keys + i - 1));
-      for (int s = 0; s < a.n_seg; ++s) head |= (i == segst[s]);
+#pragma unroll
+      for (int s = 0; s < MAX_SEG; ++s) head |= (s < a.n_seg) & (i == segst[s]);
     }
     key[it] = k;
     ballot[it] = __ballot_sync(CRSH_FULL, head);
     if (lane == 0) s_cnt[it * 8 + warp] = __popc(ballot[it]);
   }
   __syncthreads();
-  tile_scan_lookback_block(s_cnt, s_excl, &s_prefix, a.status, (int)tile);
+  tile_scan_lookback_block<NE>(s_cnt, s_excl, &s_prefix, a.status, (int)tile);
   __syncthreads();
   const uint32_t prefix = s_prefix, lt = lanemask_lt();
 #pragma unroll
-  for (int it = 0; it < SCAN_ITEMS; ++it) {
-    const uint32_t i = tile * SCAN_TILE + it * SCAN_THREADS + threadIdx.x;
+  for (int it = 0; it < RLE_ITEMS; ++it) {
+    const uint32_t i = tile * TILE + it * SCAN_THREADS + threadIdx.x;
     if ((ballot[it] >> lane) & 1u) {
       const uint32_t c = prefix + s_excl[it * 8 + warp] + __popc(ballot[it] & lt);
       CRSH_CHECK(c < N, 201);
       a.ckey[c] = key[it];
       a.cbase[c] = i;
-      for (int s = 0; s < a.n_seg; ++s)
-        if (i == segst[s]) a.fd->seg_chunk_start[s] = c;
+      int sg = 0;
+#pragma unroll
+      for (int s = 0; s < MAX_SEG; ++s) {
+        if (s < a.n_seg && i == segst[s]) a.fd->seg_chunk_start[s] = c;
+        sg = (s < a.n_seg && i >= segst[s]) ? s : sg;
+      }
+      if (a.hist) {
+        const uint32_t k = key[it];
+#pragma unroll
+        for (int p = 0; p < 4; ++p) atomicAdd(&s_hist[(sg * 4 + p) * 256 + ((k >> (8 * p)) & 255u)], 1u);
+      }
     }
   }
   if (tile == n_tiles - 1 && threadIdx.x == 0) {
     uint32_t t = 0;
-    for (int q = 0; q < SCAN_ITEMS * 8; ++q) t += s_cnt[q];
+    for (int q = 0; q < NE; ++q) t += s_cnt[q];
     const uint32_t C = prefix + t;
     a.cbase[C] = N;
     a.fd->seg_chunk_start[a.n_seg] = C;
     a.fd->C = C;
-    for (int s = 0; s < a.n_seg; ++s)
-      if (segst[s] >= N) a.fd->seg_chunk_start[s] = C;   // empty trailing segment
+#pragma unroll
+    for (int s = 0; s < MAX_SEG; ++s)
+      if (s < a.n_seg && segst[s] >= N) a.fd->seg_chunk_start[s] = C;   // empty trailing segment
+  }
+  if (a.hist) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < a.n_seg * 4 * 256; i += SCAN_THREADS)
+      if (s_hist[i]) atomicAdd(a.hist + i, s_hist[i]);
   }
 }
 
@@ -117,15 +149,30 @@ struct SegChunks {   // per-segment chunk ranges, loaded from the FrameDesc
   uint32_t tile_start[MAX_SEG + 1];
   __device__ void load(const FrameDesc* fd, int ns) {
     n_seg = ns;
-    for (int s = 0; s <= ns; ++s) { start[s] = fd->seg_chunk_start[s]; tile_start[s] = fd->sort_tile_start[s]; }
-    for (int s = 0; s < ns; ++s) count[s] = fd->seg_C[s];
+#pragma unroll
+    for (int s = 0; s <= MAX_SEG; ++s) {
+      start[s] = s <= ns ? fd->seg_chunk_start[s] : 0xFFFFFFFFu;
+      tile_start[s] = s <= ns ? fd->sort_tile_start[s] : 0xFFFFFFFFu;
+    }
+#pragma unroll
+    for (int s = 0; s < MAX_SEG; ++s) count[s] = s < ns ? fd->seg_C[s] : 0u;
   }
 };
 
+// Segment lookups over register arrays: loops unrolled to MAX_SEG with a
+// bound check and selects instead of a runtime index, so the per-segment
+// arrays stay in registers (a runtime-indexed array lives in local memory).
 __device__ __forceinline__ int seg_of(const uint32_t* starts, int n, uint32_t i) {
   int s = 0;
-  for (int q = 1; q < n; ++q) s = (i >= starts[q]) ? q : s;
+#pragma unroll
+  for (int q = 1; q < MAX_SEG; ++q) s = (q < n && i >= starts[q]) ? q : s;
   return s;
+}
+__device__ __forceinline__ uint32_t seg_sel(const uint32_t* arr, int s) {
+  uint32_t r = arr[0];
+#pragma unroll
+  for (int q = 1; q <= MAX_SEG; ++q) r = (q == s) ? arr[q] : r;
+  return r;
 }
 
 // Per-segment digit histograms of all passes in one read of the keys.
@@ -187,10 +234,13 @@ __global__ void __launch_bounds__(SORT_THREADS, CRSH_SORT_MINB) k_onesweep(const
   const uint32_t tile = s_tile;
   SegChunks sc;
   sc.load(a.fd, a.n_seg);
-  if (tile >= sc.tile_start[sc.n_seg]) return;   // surplus block
+  if (tile >= seg_sel(sc.tile_start, sc.n_seg)) return;   // surplus block
   const int seg = seg_of(sc.tile_start, sc.n_seg, tile);
-  const uint32_t t_local = tile - sc.tile_start[seg];
-  const uint32_t n = sc.count[seg], seg0 = sc.start[seg];
+  const uint32_t t_local = tile - seg_sel(sc.tile_start, seg);
+  uint32_t n = sc.count[0];
+#pragma unroll
+  for (int q = 1; q < MAX_SEG; ++q) n = (q == seg) ? sc.count[q] : n;
+  const uint32_t seg0 = seg_sel(sc.start, seg);
   const int shift = RADIX_BITS * a.pass;
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5, lt = lanemask_lt();
 
@@ -254,7 +304,7 @@ __global__ void __launch_bounds__(SORT_THREADS, CRSH_SORT_MINB) k_onesweep(const
     // batched look-back: 8 predecessors' words are requested at once, so a
     // one-wave sort (every tile looking back at aggregates) costs ~1/8 of the
     // round trips of a one-by-one walk; the segment's first tile is inclusive
-    const int first = (int)sc.tile_start[seg];
+    const int first = (int)seg_sel(sc.tile_start, seg);
     int p = (int)tile - 1;
     bool done = false;
     while (!done) {
@@ -316,20 +366,23 @@ struct ScanSizeArgs {
 };
 
 // The skeleton array (sorted chunk sizes) and its exclusive scan.
+template <int SS_ITEMS>
 __global__ void __launch_bounds__(SCAN_THREADS) k_scan_sizes(const ScanSizeArgs a) {
+  constexpr int NE = SS_ITEMS * 8;
+  constexpr uint32_t TILE = (uint32_t)SCAN_THREADS * SS_ITEMS;
   __shared__ uint32_t s_tile, s_prefix;
-  __shared__ uint32_t s_cnt[SCAN_ITEMS * 8], s_excl[SCAN_ITEMS * 8];
+  __shared__ uint32_t s_cnt[NE], s_excl[NE];
   if (threadIdx.x == 0) s_tile = atomicAdd(a.ticket, 1u);
   __syncthreads();
   const uint32_t tile = s_tile;
   const uint32_t C = a.fd->C, N = a.fd->N;
-  const uint32_t n_tiles = (C + SCAN_TILE - 1) / SCAN_TILE;
+  const uint32_t n_tiles = (C + TILE - 1) / TILE;
   if (tile >= n_tiles) return;   // surplus block
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
-  uint32_t size[SCAN_ITEMS], wex[SCAN_ITEMS];
+  uint32_t size[SS_ITEMS], wex[SS_ITEMS];
 #pragma unroll
-  for (int it = 0; it < SCAN_ITEMS; ++it) {
-    const uint32_t c = tile * SCAN_TILE + it * SCAN_THREADS + threadIdx.x;
+  for (int it = 0; it < SS_ITEMS; ++it) {
+    const uint32_t c = tile * TILE + it * SCAN_THREADS + threadIdx.x;
     uint32_t sz = 0;
     if (c < C) {
       const uint32_t ci = __ldg(a.sorted_cidx + c);
@@ -346,12 +399,12 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_sizes(const ScanSizeArgs 
     if (lane == 31) s_cnt[it * 8 + warp] = incl;
   }
   __syncthreads();
-  tile_scan_lookback_block(s_cnt, s_excl, &s_prefix, a.status, (int)tile);
+  tile_scan_lookback_block<NE>(s_cnt, s_excl, &s_prefix, a.status, (int)tile);
   __syncthreads();
   const uint32_t prefix = s_prefix;
 #pragma unroll
-  for (int it = 0; it < SCAN_ITEMS; ++it) {
-    const uint32_t c = tile * SCAN_TILE + it * SCAN_THREADS + threadIdx.x;
+  for (int it = 0; it < SS_ITEMS; ++it) {
+    const uint32_t c = tile * TILE + it * SCAN_THREADS + threadIdx.x;
     if (c < C) {
       const uint32_t p = prefix + s_excl[it * 8 + warp] + wex[it];
       a.pos[c] = p;
@@ -384,7 +437,11 @@ __global__ void __launch_bounds__(256) k_expand(const ExpandArgs a) {
   const uint32_t nb = (N + EXP_TILE - 1) / EXP_TILE;
   if (blockIdx.x >= nb) return;   // surplus block
   uint32_t segc[MAX_SEG + 1], segp[MAX_SEG + 1];
-  for (int s = 0; s <= a.n_seg; ++s) { segc[s] = a.fd->seg_comp_start[s]; segp[s] = a.fd->seg_pad_base[s]; }
+#pragma unroll
+  for (int s = 0; s <= MAX_SEG; ++s) {
+    segc[s] = s <= a.n_seg ? a.fd->seg_comp_start[s] : 0xFFFFFFFFu;
+    segp[s] = s <= a.n_seg ? a.fd->seg_pad_base[s] : 0xFFFFFFFFu;
+  }
   const uint32_t o0 = blockIdx.x * EXP_TILE;
   const uint32_t o1 = min(o0 + EXP_TILE, N);
   const uint32_t c_lo = __ldg(a.first_chunk + blockIdx.x);
@@ -401,7 +458,7 @@ __global__ void __launch_bounds__(256) k_expand(const ExpandArgs a) {
     const uint32_t c = c_lo + lo;
     const uint32_t src = __ldg(a.cbase + __ldg(a.scidx + c)) + (o - s_pos[lo]);
     const int s = seg_of(segc, a.n_seg, o);
-    const uint32_t dst = segp[s] + (o - segc[s]);
+    const uint32_t dst = seg_sel(segp, s) + (o - seg_sel(segc, s));
     CRSH_CHECK(dst < a.fd->Np && src < N && c < C, 401);
     a.sorted_key[dst] = __ldg(a.skey + c);
     a.sorted_slot[dst] = __ldg(a.vals_c + src);
@@ -412,10 +469,14 @@ __global__ void __launch_bounds__(256) k_expand(const ExpandArgs a) {
 __global__ void k_copy_unsorted(const ExpandArgs a) {
   const uint32_t N = a.fd->N;
   uint32_t segc[MAX_SEG + 1], segp[MAX_SEG + 1];
-  for (int s = 0; s <= a.n_seg; ++s) { segc[s] = a.fd->seg_comp_start[s]; segp[s] = a.fd->seg_pad_base[s]; }
+#pragma unroll
+  for (int s = 0; s <= MAX_SEG; ++s) {
+    segc[s] = s <= a.n_seg ? a.fd->seg_comp_start[s] : 0xFFFFFFFFu;
+    segp[s] = s <= a.n_seg ? a.fd->seg_pad_base[s] : 0xFFFFFFFFu;
+  }
   for (uint32_t o = blockIdx.x * blockDim.x + threadIdx.x; o < N; o += gridDim.x * blockDim.x) {
     const int s = seg_of(segc, a.n_seg, o);
-    const uint32_t dst = segp[s] + (o - segc[s]);
+    const uint32_t dst = seg_sel(segp, s) + (o - seg_sel(segc, s));
     a.sorted_key[dst] = __ldg(a.skey + o);
     a.sorted_slot[dst] = __ldg(a.vals_c + o);
   }

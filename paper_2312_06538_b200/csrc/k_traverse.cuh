@@ -221,8 +221,9 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_plan(const PlanArgs a) {
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
   __shared__ unsigned long long s_mesh[MAX_SEG][2];
   if (threadIdx.x < MAX_SEG * 2) (&s_mesh[0][0])[threadIdx.x] = 0ull;
-  uint32_t seg_group_start[MAX_SEG];
-  for (int q = 0; q < a.n_seg; ++q) seg_group_start[q] = a.fd->seg_pad_base[q] / a.group_rays;
+  uint32_t seg_group_start[MAX_SEG];   // registers: every loop below is unrolled to MAX_SEG
+#pragma unroll
+  for (int q = 0; q < MAX_SEG; ++q) seg_group_start[q] = q < a.n_seg ? a.fd->seg_pad_base[q] / a.group_rays : 0xFFFFFFFFu;
   __syncthreads();
   uint32_t ntri[SCAN_ITEMS], nit[SCAN_ITEMS], wex[SCAN_ITEMS];
   uint32_t mt[MAX_SEG] = {0u, 0u, 0u}, mh[MAX_SEG] = {0u, 0u, 0u};
@@ -234,7 +235,9 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_plan(const PlanArgs a) {
       const uint4 st = __ldg(a.gstat + g);   // whole-mesh tests / passes of the group's top nodes
       T = st.x;
       int sg = 0;
-      for (int q = 1; q < a.n_seg; ++q) sg = (g >= seg_group_start[q]) ? q : sg;
+#pragma unroll
+      for (int q = 1; q < MAX_SEG; ++q) sg = (g >= seg_group_start[q]) ? q : sg;
+#pragma unroll
       for (int q = 0; q < MAX_SEG; ++q) {
         mt[q] += (sg == q) ? st.y : 0u;
         mh[q] += (sg == q) ? st.z : 0u;
@@ -252,7 +255,9 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_plan(const PlanArgs a) {
     wex[it] = incl - ni;
     if (lane == 31) s_cnt[it * 8 + warp] = incl;
   }
-  for (int q = 0; q < a.n_seg; ++q) {
+#pragma unroll
+  for (int q = 0; q < MAX_SEG; ++q) {
+    if (q >= a.n_seg) break;
     warp_seg_add(&s_mesh[0][0], 2, a.n_seg, q, mt[q]);
     warp_seg_add(&s_mesh[0][1], 2, a.n_seg, q, mh[q]);
   }
@@ -476,9 +481,13 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
   if (lane <= MAX_LEVELS) qlen[lane] = 0u;
   if (tid == 0) s_cur_g = 0xFFFFFFFFu;
   const uint32_t n_items = a.fd->n_items;
-  uint32_t seg_group_start[MAX_SEG + 1], seg_real_end[MAX_SEG];   // real rays of segment s end at seg_real_end[s]
-  for (int q = 0; q <= a.n_seg; ++q) seg_group_start[q] = a.fd->seg_pad_base[q] / a.group_rays;
-  for (int q = 0; q < a.n_seg; ++q) seg_real_end[q] = a.fd->seg_pad_base[q] + a.fd->seg_n[q];
+  // real rays of segment s end at seg_real_end[s]; registers (loops unrolled to MAX_SEG)
+  uint32_t seg_group_start[MAX_SEG], seg_real_end[MAX_SEG];
+#pragma unroll
+  for (int q = 0; q < MAX_SEG; ++q) {
+    seg_group_start[q] = q < a.n_seg ? a.fd->seg_pad_base[q] / a.group_rays : 0xFFFFFFFFu;
+    seg_real_end[q] = q < a.n_seg ? a.fd->seg_pad_base[q] + a.fd->seg_n[q] : 0u;
+  }
 
   const uint32_t chunk =
       max(1u, min((uint32_t)CRSH_ITEM_CHUNK_MAX, n_items / (gridDim.x * (uint32_t)CRSH_ITEM_CHUNK_DIV)));
@@ -496,14 +505,16 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
     const uint4 item = __ldg(a.items + it);
     const uint32_t g = item.x;
     int seg = 0;
-    for (int qq = 1; qq < a.n_seg; ++qq) seg = (g >= seg_group_start[qq]) ? qq : seg;
+#pragma unroll
+    for (int qq = 1; qq < MAX_SEG; ++qq) seg = (g >= seg_group_start[qq]) ? qq : seg;
     unsigned long long* ctr = s_ctr + seg * CTR_STRIDE;
     // rays [0, g_real) of the group are real, the rest padding (segments are
     // padded at their end): ray validity without loading the ray
     uint32_t g_real = 0;
     {
       uint32_t se = 0;
-      for (int qq = 0; qq < a.n_seg; ++qq) se = (qq == seg) ? seg_real_end[qq] : se;
+#pragma unroll
+      for (int qq = 0; qq < MAX_SEG; ++qq) se = (qq == seg) ? seg_real_end[qq] : se;
       const uint32_t g0 = g * a.group_rays;
       g_real = se > g0 ? min(se - g0, a.group_rays) : 0u;
     }
