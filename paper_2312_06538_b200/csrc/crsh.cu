@@ -603,7 +603,7 @@ crsh_status enqueue_frame(crsh_scene* sc, const FrameInfo& fi, const crsh_primar
       a.child_nodes = nodes + 2 * fi.level_off[k - 1];
       a.nodes = nodes + 2 * fi.level_off[k];
       a.trav = trav + 3 * fi.level_off[k];
-      const uint32_t grid = cdiv(std::max<uint64_t>(fi.level_max[k] * (uint64_t)B, 1), 128);   // lane per child
+      const uint32_t grid = cdiv(std::max<uint64_t>(fi.level_max[k] * (CRSH_UPPER_WARP ? (uint64_t)B : 1u), 1), 128);
       CK(dispatch_b(B, [&](auto b) {
         k_upper<decltype(b)::value><<<grid, 128, 0, st>>>(a);
         return cudaGetLastError();

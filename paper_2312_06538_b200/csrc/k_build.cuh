@@ -264,15 +264,17 @@ struct UpperArgs {
 };
 
 // K6: node j = balanced pairwise union (Eqs 5-8, R9, R11) of children
-// [j*B, (j+1)*B); empty children pass through. A segmented warp reduction
-// (BASELINE north_star: "sphere-cone merge done as segmented warp reductions
-// per level"): lane = child (coalesced child loads), 32 / B parents per warp;
-// step w exchanges with lane ^ w and both lanes form union(lower, upper), so
-// after log2 B steps every lane of the segment holds the union in exactly the
-// balanced order ((0,1),(2,3)),((4,5),(6,7)) of R9; lane 0 of each segment
-// writes the parent. B = 32 is one parent per warp. (The leaf level, K5, stays
-// thread-per-bundle: its cone is a SEQUENTIAL fold of Eqs 1-4 over the
-// bundle's rays in sorted order, not a reduction.)
+// [j*B, (j+1)*B); empty children pass through. Two forms, bit-identical:
+// thread per parent (default), and a segmented warp reduction (BASELINE
+// north_star: "sphere-cone merge done as segmented warp reductions per
+// level"; -DCRSH_UPPER_WARP=1): lane = child (coalesced child loads), 32 / B
+// parents per warp; step w exchanges with lane ^ w and both lanes form
+// union(lower, upper), so after log2 B steps every lane of the segment holds
+// the union in exactly the balanced order ((0,1),(2,3)),((4,5),(6,7)) of R9.
+// Measured at cfg4: 57 us for the warp form vs 19 us thread-per-parent (every
+// lane forms each union: 3.5x the union work, each two atan2 + a division).
+// (The leaf level, K5, is thread-per-bundle either way: its cone is a
+// SEQUENTIAL fold of Eqs 1-4 over the bundle's rays, not a reduction.)
 __device__ __forceinline__ NodeV shfl_xor_node(const NodeV& n, int w) {
   NodeV o;
   o.c = mk3(__shfl_xor_sync(CRSH_FULL, n.c.x, w), __shfl_xor_sync(CRSH_FULL, n.c.y, w), __shfl_xor_sync(CRSH_FULL, n.c.z, w));
@@ -281,6 +283,25 @@ __device__ __forceinline__ NodeV shfl_xor_node(const NodeV& n, int w) {
   o.alpha = __shfl_xor_sync(CRSH_FULL, n.alpha, w);
   return o;
 }
+#ifndef CRSH_UPPER_WARP
+#define CRSH_UPPER_WARP 0   // 1: segmented warp reduction (A/B at cfg4: k_upper 19 -> 57 us, every lane forms each union)
+#endif
+#if !CRSH_UPPER_WARP
+template <int B>
+__global__ void __launch_bounds__(128) k_upper(const UpperArgs a) {   // thread per parent (A/B)
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= a.fd->level_n[a.level]) return;
+  NodeV st[B];
+#pragma unroll
+  for (int i = 0; i < B; ++i) st[i] = load_node(a.child_nodes, (size_t)j * B + i);
+#pragma unroll
+  for (int w = 1; w < B; w *= 2) {
+#pragma unroll
+    for (int i = 0; i < B; i += 2 * w) st[i] = node_union_ns(st[i], st[i + w]);
+  }
+  store_node(a.nodes, a.trav, j, st[0]);
+}
+#else
 template <int B>
 __global__ void __launch_bounds__(128) k_upper(const UpperArgs a) {
   const uint32_t gl = blockIdx.x * blockDim.x + threadIdx.x;   // global lane = child index
@@ -295,6 +316,7 @@ __global__ void __launch_bounds__(128) k_upper(const UpperArgs a) {
   }
   if ((lane & (uint32_t)(B - 1)) == 0u && gl < n_par * (uint32_t)B) store_node(a.nodes, a.trav, gl / B, v);
 }
+#endif
 
 // ---------------------------------------------------------------- dynamic scenes
 // (§3.3.1): creation-time vertices -> per-mesh

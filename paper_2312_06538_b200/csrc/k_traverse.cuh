@@ -313,6 +313,9 @@ constexpr int LOWQ = 64;                     // capacity of a warp queue below l
 // (CTAs x ITEM_CHUNK_DIV)), at least 1 (A/B, fixed chunks of 1 / 2 / 4: cfg2
 // R6 103.4 / 100.7 / 93.6 Mrays/s, 46 items per CTA; cfg3 R6 53.2 / - / 55.6;
 // adaptive: cfg2 unchanged, cfg3 R6 53.2 -> 55.0, cfg3 Z-order 510 -> 550)
+#ifndef CRSH_TRAV_PREFETCH
+#define CRSH_TRAV_PREFETCH 0
+#endif
 #ifndef CRSH_ITEM_CHUNK_MAX
 #define CRSH_ITEM_CHUNK_MAX 4
 #endif
@@ -871,6 +874,33 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
       }
     };
     if constexpr (!OBJ) {
+#if CRSH_TRAV_PREFETCH
+      // software-pipelined slices: the next slice's mesh lookup and triangle
+      // sphere load are issued before the current slice's tests, so the L2
+      // latency of the sphere load overlaps them (ncu cfg4 Z-order: the first
+      // use of the sphere was a top stall)
+      auto fetch = [&](uint32_t s0, uint32_t& tri, float4& sph, uint32_t& nm) {
+        const uint32_t v = s0 + lane;
+        nm = 0; tri = 0;
+        sph = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (v < item.z) {
+          const uint32_t lo = mesh_of(v);
+          tri = s_act_first[lo] + (v - s_act_prefix[lo]);
+          sph = __ldg(a.tri_sph + tri);
+          nm = s_act_nmask[lo];
+        }
+      };
+      uint32_t s0 = item.y + warp * 32u;
+      uint32_t tri_n = 0, nm_n = 0;
+      float4 sph_n;
+      if (s0 < item.z) fetch(s0, tri_n, sph_n, nm_n);
+      for (; s0 < item.z; s0 += TRAV_THREADS) {
+        const uint32_t tri = tri_n, nm = nm_n;
+        const float4 sph = sph_n;
+        if (s0 + TRAV_THREADS < item.z) fetch(s0 + TRAV_THREADS, tri_n, sph_n, nm_n);
+        slice_body(tri, sph, nm);
+      }
+#else
       for (uint32_t s0 = item.y + warp * 32u; s0 < item.z; s0 += TRAV_THREADS) {
         const uint32_t v = s0 + lane;
         uint32_t nm = 0, tri = 0;
@@ -883,6 +913,7 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
         }
         slice_body(tri, sph, nm);
       }
+#endif
     } else {
       // object sphere-tree (NEXT-4, reading O1): the item's virtual range is
       // cluster-aligned (each kept mesh padded to whole clusters), so cluster

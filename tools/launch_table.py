@@ -3,7 +3,7 @@
 [,dram__bytes_read.sum,dram__bytes_write.sum] --csv --log-file X.csv).
 
 Groups launches by kernel name over the frames of the timed region (the last
-`--frames` occurrences of k_raygen start a frame) and prints mean duration,
+`--frames` occurrences of k_raygen or k_raygen_count start a frame) and prints mean duration,
 share of the frame and DRAM bytes per launch.  ncu times are cold-cache and
 serialised: compare shares, not absolutes (B200_PROFILING.md)."""
 import argparse
@@ -45,7 +45,7 @@ def main():
         elif name.startswith("dram__bytes"):
             d[name] = v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
     ids = list(launches)
-    starts = [i for i in ids if launches[i]["name"] == "k_raygen"]
+    starts = [i for i in ids if launches[i]["name"] in ("k_raygen", "k_raygen_count")]
     frames = starts[-a.frames:]
     agg = collections.OrderedDict()
     nf = 0
