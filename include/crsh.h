@@ -33,7 +33,10 @@ typedef enum {
   CRSH_OK = 0,
   CRSH_EINVAL = 2, /* bad argument (null pointer, bad mesh ids, bad option) */
   CRSH_EIO = 3,    /* host buffer too small for a tap */
-  CRSH_ELIMIT = 4, /* exceeds an encoding limit (lights > 16, slots >= 2^30, ...) */
+  CRSH_ELIMIT = 4, /* exceeds an encoding limit (lights > 16, slots >= 2^30, ...). The slot bound is 2^30,
+                      not SURVEY §8(b)'s 2^32: the single-pass scans publish a flag and a 30-bit count in
+                      one 32-bit look-back word (k_onesweep), and 2^30 slots already cover a 7680x4320
+                      frame with 16 lights (and every frame of this path's configurations by far) */
   CRSH_ENOMEM = 5, /* device allocation failed */
   CRSH_ECUDA = 6,  /* CUDA runtime error (incl. no device) */
   CRSH_ENCCL = 7   /* NCCL failure (crsh_dist_*, the multi-GPU merge, asynchronous errors) */

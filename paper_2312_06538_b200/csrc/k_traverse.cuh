@@ -495,6 +495,22 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
   const uint32_t chunk =
       max(1u, min((uint32_t)CRSH_ITEM_CHUNK_MAX, n_items / (gridDim.x * (uint32_t)CRSH_ITEM_CHUNK_DIV)));
   uint32_t ch_next = 0, ch_end = 0;   // CTA-uniform: the rest of the current ticket's chunk of items
+  unsigned long long acc_tt = 0, acc_th = 0, acc_ct = 0, acc_ch = 0, acc_mt = 0, acc_mh = 0, acc_clt = 0, acc_clh = 0;
+  int acc_seg = -1;
+  auto flush_acc = [&]() {
+    if (acc_seg >= 0 && lane == 0) {
+      unsigned long long* c = s_ctr + acc_seg * CTR_STRIDE;
+      if (acc_clt) atomicAdd(&c[CTR_CL_TESTS], acc_clt);
+      if (acc_clh) atomicAdd(&c[CTR_CL_HITS], acc_clh);
+      if (acc_tt) atomicAdd(&c[CTR_TESTS + Lv], acc_tt);
+      if (acc_th) atomicAdd(&c[CTR_HITS + Lv], acc_th);
+      if (Lv >= 2 && acc_ct) atomicAdd(&c[CTR_TESTS + Lv - 1], acc_ct);
+      if (Lv >= 2 && acc_ch) atomicAdd(&c[CTR_HITS + Lv - 1], acc_ch);
+      if (acc_mt) atomicAdd(&c[CTR_FINAL_TESTS], acc_mt);
+      if (acc_mh) atomicAdd(&c[CTR_FINAL_HITS], acc_mh);
+    }
+    acc_tt = acc_th = acc_ct = acc_ch = acc_mt = acc_mh = acc_clt = acc_clh = 0;
+  };
   for (;;) {
     __syncthreads();
     if (ch_next >= ch_end && tid == 0) s_item = atomicAdd(a.ticket, 1u) * chunk;
@@ -511,6 +527,10 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
 #pragma unroll
     for (int qq = 1; qq < MAX_SEG; ++qq) seg = (g >= seg_group_start[qq]) ? qq : seg;
     unsigned long long* ctr = s_ctr + seg * CTR_STRIDE;
+    if (seg != acc_seg) {   // uniform: the warp's running counters belong to one segment
+      flush_acc();
+      acc_seg = seg;
+    }
     // rays [0, g_real) of the group are real, the rest padding (segments are
     // padded at their end): ray validity without loading the ray
     uint32_t g_real = 0;
@@ -967,22 +987,21 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
       }
     }
     drain(true);
-    // item counters -> CTA counters (one shared atomic per counter per warp)
-    c_top_t = __reduce_add_sync(CRSH_FULL, c_top_t);
-    c_top_h = __reduce_add_sync(CRSH_FULL, c_top_h);
-    c_mt_t = __reduce_add_sync(CRSH_FULL, c_mt_t);
-    c_mt_h = __reduce_add_sync(CRSH_FULL, c_mt_h);
-    c_ch_h = __reduce_add_sync(CRSH_FULL, c_ch_h);
-    if (lane == 0) {
-      if (c_cl_t) atomicAdd(&ctr[CTR_CL_TESTS], (unsigned long long)c_cl_t);
-      if (c_cl_h) atomicAdd(&ctr[CTR_CL_HITS], (unsigned long long)c_cl_h);
-      if (c_top_t) atomicAdd(&ctr[CTR_TESTS + Lv], (unsigned long long)c_top_t);
-      if (c_top_h) atomicAdd(&ctr[CTR_HITS + Lv], (unsigned long long)c_top_h);
-      if (Lv >= 2 && c_ch_t) atomicAdd(&ctr[CTR_TESTS + Lv - 1], (unsigned long long)c_ch_t);
-      if (Lv >= 2 && c_ch_h) atomicAdd(&ctr[CTR_HITS + Lv - 1], (unsigned long long)c_ch_h);
-      if (c_mt_t) atomicAdd(&ctr[CTR_FINAL_TESTS], (unsigned long long)c_mt_t);
-      if (c_mt_h) atomicAdd(&ctr[CTR_FINAL_HITS], (unsigned long long)c_mt_h);
-    }
+    // item counters -> the warp's running 64-bit counters (flushed to the CTA
+    // counters when the segment changes and at the end: per-item 64-bit
+    // shared atomics are CAS loops that the 8 warps contended on, ncu cfg4)
+    // (A/B: +0.8 % at cfg4 R6; the object-tree instantiation, whose items
+    // are short, measured 3 % slower with them -- its extra live registers
+    // spill -- and keeps the per-item flush)
+    acc_tt += __reduce_add_sync(CRSH_FULL, c_top_t);
+    acc_th += __reduce_add_sync(CRSH_FULL, c_top_h);
+    acc_mt += __reduce_add_sync(CRSH_FULL, c_mt_t);
+    acc_mh += __reduce_add_sync(CRSH_FULL, c_mt_h);
+    acc_ch += __reduce_add_sync(CRSH_FULL, c_ch_h);
+    acc_ct += c_ch_t;      // warp-uniform already
+    acc_clt += c_cl_t;     // lane 0 only (lane 0 flushes)
+    acc_clh += c_cl_h;
+    if constexpr (OBJ) flush_acc();
     __syncthreads();
     if (SMALL) {
       for (uint32_t r = tid; r < a.group_rays; r += TRAV_THREADS) {
@@ -991,6 +1010,7 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
       }
     }
   }
+  flush_acc();
   __syncthreads();
   for (uint32_t i = tid; i < MAX_SEG * CTR_STRIDE; i += TRAV_THREADS)
     if (s_ctr[i]) atomicAdd(a.counters + i, s_ctr[i]);
