@@ -64,6 +64,30 @@ for flags in (3, 7):
         mismatch = e.status
     out[flags] = dict(hits_equal=ok, counts_equal=bool(cnt), merge=st["merge"], second=second, mismatch=mismatch,
                       launches=tr.launches())
+# window growth (a collective re-registration) and the host-buffer call on a dist scene
+tr = tracer_for(make_workload(2, width=64, height=64), flags=3)
+dist.init(tr.scene, dist.unique_id(), 0, 1)
+tr.run()
+small_ok = bool(np.array_equal(tr.results()[0], oracle.trace(make_workload(2, width=64, height=64))["hit_tri"]))
+w2 = make_workload(2, width=160, height=120)
+tr.set_gbuffer(w2.width, w2.height, w2.pos, w2.nrm, w2.mat, w2.materials, w2.eye)
+tr.configure(w2.lights, w2.ray_types, w2.levels, w2.leaf_size, w2.branching, 3)
+tr.run()
+ref2 = oracle.trace(w2)
+grow_ok = bool(np.array_equal(tr.results()[0], ref2["hit_tri"]))
+hh = np.empty(tr.slots, np.int32); th = np.empty(tr.slots, np.float32)
+tr.run_host(np.ascontiguousarray(w2.pos), np.ascontiguousarray(w2.nrm), np.ascontiguousarray(w2.mat),
+            np.ascontiguousarray(w2.materials), hh, th)
+host_ok = bool(np.array_equal(hh, ref2["hit_tri"]) and np.array_equal(th.view(np.uint32), ref2["t"].view(np.uint32)))
+errs = []
+for args in ((0, 0), (1, 1), (-1, 1)):
+    t3 = tracer_for(make_workload(1, width=8, height=8))
+    try:
+        dist.init(t3.scene, dist.unique_id(), *args)
+        errs.append("accepted")
+    except crsh.CrshError as e:
+        errs.append(e.status)
+out["extra"] = dict(small=small_ok, grow=grow_ok, host=host_ok, bad_rank_world=errs)
 print("RESULT " + json.dumps(out))
 '''
 
@@ -76,6 +100,9 @@ def test_dist_world1_merge_equals_oracle(mode, code):
     assert r.returncode == 0 and line, r.stdout[-3000:] + r.stderr[-3000:]
     import json
     res = json.loads(line[0][7:])
+    extra = res.pop("extra")
+    assert extra["small"] and extra["grow"] and extra["host"], extra
+    assert extra["bad_rank_world"] == [2, 2, 2], extra   # EINVAL before any NCCL call
     for flags, v in res.items():
         assert v["hits_equal"], (mode, flags)
         assert v["counts_equal"], (mode, flags)
