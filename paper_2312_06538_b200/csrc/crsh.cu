@@ -372,6 +372,9 @@ cudaError_t dispatch_b(int B, F&& f) {
 //   cfg4 Z-order  234 /  261 /  275 /  284 /  289 /  292 /  219;
 // cfg2 R6 at 2048 / 3072 / 4096: 109.6 / 109.1 / 107.1).
 constexpr uint64_t ITEM_BIG_GROUPS_PER_SM = 16;   // G_max at or above 16 groups per SM -> ITEM_TRIS_BIG
+#ifndef CRSH_ITEM_TRIS_SMALL_OBJ
+#define CRSH_ITEM_TRIS_SMALL_OBJ 2048u
+#endif
 #ifndef CRSH_ITEM_TRIS_BIG
 #define CRSH_ITEM_TRIS_BIG 16384
 #endif
@@ -380,14 +383,20 @@ constexpr uint64_t ITEM_BIG_GROUPS_PER_SM = 16;   // G_max at or above 16 groups
 // share needs the small items to balance. CRSH_ITEM_TRIS=<n> (environment,
 // read per call) forces n triangles per item -- a test hook that runs the
 // large-item path on small frames.
-inline uint32_t item_tris_for(uint64_t G_max, int world, int sm_count) {
+// With the object sphere-tree (CRSH_F_OBJTREE) most of an item's clusters are
+// culled by one lane-parallel test each, so an item costs less and large
+// frames take twice the triangles per item (A/B, Z-order + tree, 16384 /
+// 32768 / 65536: cfg3 984 / 1020 / 892, cfg4 547 / 577 / 593 Mrays/s).
+inline uint32_t item_tris_for(uint64_t G_max, int world, int sm_count, bool objtree = false) {
   if (CRSH_ITEM_TRIS) return CRSH_ITEM_TRIS;
   if (const char* e = std::getenv("CRSH_ITEM_TRIS")) {
     const long v = std::strtol(e, nullptr, 10);
     if (v >= 32 && v <= (1l << 24) && (v % 32) == 0) return (uint32_t)v;
   }
   const uint64_t share = G_max / (uint64_t)std::max(world, 1);
-  return share >= ITEM_BIG_GROUPS_PER_SM * (uint64_t)std::max(sm_count, 1) ? (uint32_t)CRSH_ITEM_TRIS_BIG : 2048u;
+  const bool big = share >= ITEM_BIG_GROUPS_PER_SM * (uint64_t)std::max(sm_count, 1);
+  if (objtree) return big ? 2u * (uint32_t)CRSH_ITEM_TRIS_BIG : CRSH_ITEM_TRIS_SMALL_OBJ;
+  return big ? (uint32_t)CRSH_ITEM_TRIS_BIG : 2048u;
 }
 
 // Everything a frame's launch sequence depends on: if the key of a call equals
@@ -828,7 +837,7 @@ crsh_status trace_impl(crsh_scene* sc, const crsh_primary_hits* h, const float* 
   size_t total_nodes = 0;
   for (int k = 1; k <= Lv; ++k) total_nodes += fi.level_max[k];
   const int W = (sc->n_meshes + 31) / 32;
-  fi.item_tris = item_tris_for(fi.G_max, world, sc->sm_count);
+  fi.item_tris = item_tris_for(fi.G_max, world, sc->sm_count, (fi.flags & CRSH_F_OBJTREE) != 0);
   {   // decompression-scan tile size; radix histograms built by k_rle (A/B at cfg4: scan 178 -> 162 us with
       // 8192-entry tiles; sort 340 -> 319 us without the histogram pass). Overrides CRSH_BIG_TILES, CRSH_RLE_HIST.
     const char* e = std::getenv("CRSH_BIG_TILES");
