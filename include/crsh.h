@@ -15,6 +15,13 @@
  *  - One scene is used by one host thread and one stream at a time.
  *  - There is no CPU fallback: without a usable CUDA device every compute call
  *    fails with CRSH_ECUDA.
+ *  - Environment (read when a frame is planned; A/B and test hooks, none
+ *    changes a result): CRSH_NO_GRAPH=1 launches the frame's kernels directly
+ *    instead of replaying a CUDA graph; CRSH_ITEM_TRIS=<n> fixes the
+ *    triangles per traversal work item; CRSH_BIG_TILES / CRSH_RLE_HIST = 0|1
+ *    select the decompression-scan tile size / where the radix histograms are
+ *    counted; CRSH_SLOT_MAJOR=1 selects the slot-major ray generator;
+ *    CRSH_DIST_MERGE=nccl (read by crsh_dist_init) the all-reduce merge.
  */
 #ifndef CRSH_H_
 #define CRSH_H_

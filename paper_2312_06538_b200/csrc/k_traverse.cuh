@@ -511,13 +511,32 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
     }
     acc_tt = acc_th = acc_ct = acc_ch = acc_mt = acc_mh = acc_clt = acc_clh = 0;
   };
+  // Block barriers sit at chunk boundaries (the ticket) and group changes
+  // (shared group data, the group's smem closest hits) only; consecutive items
+  // of one group run back to back per warp (queues are warp-private). The
+  // object-tree instantiation keeps a barrier per item (its per-item block
+  // counter). The group's s_best is flushed to global at the group change.
+  uint32_t cur_g = 0xFFFFFFFFu, n_act = 0;   // CTA-uniform copies of the current group
+  auto group_end = [&]() {   // all warps: the current group's closest hits to global
+    __syncthreads();
+    if (SMALL && cur_g != 0xFFFFFFFFu) {
+      const size_t rb = (size_t)cur_g * a.group_rays;
+      for (uint32_t r = tid; r < a.group_rays; r += TRAV_THREADS) {
+        const unsigned long long b = s_best[r];
+        if (b != BEST_NONE) atomicMin(a.best + rb + r, b);
+      }
+    }
+    __syncthreads();
+  };
   for (;;) {
-    __syncthreads();
-    if (ch_next >= ch_end && tid == 0) s_item = atomicAdd(a.ticket, 1u) * chunk;
-    __syncthreads();
-    if (ch_next >= ch_end) {
-      ch_next = s_item;
-      ch_end = min(ch_next + chunk, n_items);
+    if (OBJ || ch_next >= ch_end) {
+      __syncthreads();
+      if (ch_next >= ch_end && tid == 0) s_item = atomicAdd(a.ticket, 1u) * chunk;
+      __syncthreads();
+      if (ch_next >= ch_end) {
+        ch_next = s_item;
+        ch_end = min(ch_next + chunk, n_items);
+      }
     }
     const uint32_t it = ch_next++;
     if (it >= n_items) break;
@@ -542,7 +561,9 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
       g_real = se > g0 ? min(se - g0, a.group_rays) : 0u;
     }
 
-    if (g != s_cur_g) {   // uniform: group setup (top nodes, surviving meshes, group data)
+    const bool new_group = g != cur_g;   // uniform
+    if (new_group) {   // group setup (top nodes, surviving meshes, group data)
+      group_end();     // every warp is done with the previous group
       for (int j = tid; j < 3 * K; j += TRAV_THREADS) s_top[j] = __ldg(s_trav[Lv] + (size_t)g * K * 3 + j);
       if (SMALL) {
         float4* sn = reinterpret_cast<float4*>(smraw + L.off_nodes);
@@ -641,13 +662,16 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
       }
       if (tid == 0) s_act_prefix[s_carry] = s_carry_c;
       if (tid == 0) { s_n_act = s_carry; s_cur_g = g; }
-    }
-    if (SMALL) {
-      for (uint32_t r = tid; r < a.group_rays; r += TRAV_THREADS) s_best[r] = BEST_NONE;
+      if (SMALL) {
+        for (uint32_t r = tid; r < a.group_rays; r += TRAV_THREADS) s_best[r] = BEST_NONE;
+      }
+      cur_g = g;
     }
     if (OBJ && tid == 0) s_blk = 0u;
-    __syncthreads();
-    const uint32_t n_act = s_n_act;
+    if (OBJ || new_group) {
+      __syncthreads();
+      n_act = s_n_act;
+    }
     const size_t rbase = (size_t)g * a.group_rays;
     uint32_t c_top_t = 0, c_top_h = 0, c_ch_t = 0, c_ch_h = 0, c_mt_t = 0, c_mt_h = 0;   // item counters (all but c_ch_t per lane)
     uint32_t c_cl_t = 0, c_cl_h = 0;   // object-tree cluster tests / passes (lane 0 of each slice)
@@ -1002,14 +1026,8 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
     acc_clt += c_cl_t;     // lane 0 only (lane 0 flushes)
     acc_clh += c_cl_h;
     if constexpr (OBJ) flush_acc();
-    __syncthreads();
-    if (SMALL) {
-      for (uint32_t r = tid; r < a.group_rays; r += TRAV_THREADS) {
-        const unsigned long long b = s_best[r];
-        if (b != BEST_NONE) atomicMin(a.best + rbase + r, b);
-      }
-    }
   }
+  group_end();
   flush_acc();
   __syncthreads();
   for (uint32_t i = tid; i < MAX_SEG * CTR_STRIDE; i += TRAV_THREADS)
