@@ -395,8 +395,12 @@ inline uint32_t item_tris_for(uint64_t G_max, int world, int sm_count, bool objt
   }
   const uint64_t share = G_max / (uint64_t)std::max(world, 1);
   const bool big = share >= ITEM_BIG_GROUPS_PER_SM * (uint64_t)std::max(sm_count, 1);
-  if (objtree) return big ? 2u * (uint32_t)CRSH_ITEM_TRIS_BIG : CRSH_ITEM_TRIS_SMALL_OBJ;
-  return big ? (uint32_t)CRSH_ITEM_TRIS_BIG : 2048u;
+  // very large frames (>= 64 groups per SM, cfg4 ~160): twice that again
+  // (A/B cfg4, 16384 -> 32768: R6 18.79 -> 18.87, Z-order 298.9 -> 301.2;
+  // cfg3, ~55 groups per SM, stays at 16384, where 32768 measured no gain)
+  const uint32_t huge = share >= 4 * ITEM_BIG_GROUPS_PER_SM * (uint64_t)std::max(sm_count, 1) ? 2u : 1u;
+  if (objtree) return big ? 2u * huge * (uint32_t)CRSH_ITEM_TRIS_BIG : CRSH_ITEM_TRIS_SMALL_OBJ;
+  return big ? huge * (uint32_t)CRSH_ITEM_TRIS_BIG : 2048u;
 }
 
 // Everything a frame's launch sequence depends on: if the key of a call equals

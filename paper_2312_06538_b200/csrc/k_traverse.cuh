@@ -313,6 +313,9 @@ constexpr int LOWQ = 64;                     // capacity of a warp queue below l
 // (CTAs x ITEM_CHUNK_DIV)), at least 1 (A/B, fixed chunks of 1 / 2 / 4: cfg2
 // R6 103.4 / 100.7 / 93.6 Mrays/s, 46 items per CTA; cfg3 R6 53.2 / - / 55.6;
 // adaptive: cfg2 unchanged, cfg3 R6 53.2 -> 55.0, cfg3 Z-order 510 -> 550)
+#ifndef CRSH_LDS32
+#define CRSH_LDS32 1   // child records through 32-bit shared addresses (A/B cfg4 R6 18.78 -> 18.85)
+#endif
 #ifndef CRSH_TRAV_PREFETCH
 #define CRSH_TRAV_PREFETCH 0
 #endif
@@ -443,6 +446,7 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
   uint32_t* s_exm = reinterpret_cast<uint32_t*>(smraw + L.off_exm);
   float4* s_pairs = reinterpret_cast<float4*>(smraw + L.off_pairs);
   float4* s_tpairs = reinterpret_cast<float4*>(smraw + L.off_tpairs);
+  const uint32_t pairs_s = (uint32_t)__cvta_generic_to_shared(s_pairs);   // 32-bit shared address (CRSH_LDS32)
   __shared__ uint32_t s_item, s_cur_g, s_n_act, s_carry, s_carry_c, s_blk;
   __shared__ uint32_t s_warp[TRAV_WARPS];
   __shared__ unsigned long long s_ctr[MAX_SEG * CTR_STRIDE];
@@ -879,7 +883,11 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
           if (!BT && c >= B) break;
           bool p0, p1;
           if (SMALL) {
+#if CRSH_LDS32
+            cull2_ns_s(pairs_s + 80u * ((cbase >> 1) + (uint32_t)(c >> 1)), Px, Py, Pz, Pr, p0, p1);
+#else
             cull2_ns(s_pairs + 5 * ((cbase >> 1) + (uint32_t)(c >> 1)), Px, Py, Pz, Pr, p0, p1);
+#endif
           } else {
             const float4* nd = s_trav[k1] + 3 * ((size_t)g * s_pg[k1] + cbase + (uint32_t)c);
             const float4 a0 = __ldg(nd), a1 = __ldg(nd + 1), a2 = __ldg(nd + 2), b0 = __ldg(nd + 3),

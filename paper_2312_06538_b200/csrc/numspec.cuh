@@ -282,6 +282,18 @@ __device__ __forceinline__ void cull2_ns(const float4* rec, f2 Px, f2 Py, f2 Pz,
   p0 = (s0 >= -d0) & (w0 <= r0);
   p1 = (s1 >= -d1) & (w1 <= r1);
 }
+// cull2_ns with the paired record read through a 32-bit shared-memory address
+// (ld.shared: no generic-to-shared window computation per record; the same
+// values, so the same decisions)
+__device__ __forceinline__ float4 lds128(uint32_t addr) {
+  float4 v;
+  asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void cull2_ns_s(uint32_t rec, f2 Px, f2 Py, f2 Pz, f2 R, bool& p0, bool& p1) {
+  const float4 r4[5] = {lds128(rec), lds128(rec + 16u), lds128(rec + 32u), lds128(rec + 48u), lds128(rec + 64u)};
+  cull2_ns(r4, Px, Py, Pz, R, p0, p1);
+}
 }  // namespace crsh
 
 namespace crsh {

@@ -523,3 +523,21 @@ def test_transform_waits_for_inflight_frame():
     tr.run()
     hit1, _ = tr.results()
     assert not np.array_equal(hit1, ref0["hit_tri"])
+
+
+@pytest.mark.parametrize("env", [{"CRSH_SLOT_MAJOR": "1"}, {"CRSH_RLE_HIST": "0"}, {"CRSH_BIG_TILES": "1"},
+                                 {"CRSH_BIG_TILES": "0", "CRSH_RLE_HIST": "0"}])
+def test_alternative_stage_kernels(env, monkeypatch):
+    """The A/B alternatives behind the environment hooks (include/crsh.h) give
+    the oracle's frame too: the slot-major generator with its look-back scan,
+    the separate radix-histogram pass, both decompression-scan tile sizes
+    (every tap, count and hit bit-exact; cfg2's scene at 128x128 and a
+    micro-scene)."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    for w, flags in ((make_workload(2, width=128, height=128), 7),
+                     (make_micro(4242, n_tris=120, W=33, H=21, n_meshes=4, n_lights=3, ray_types=7), 3)):
+        tr, hit, t, ref = run_both(w, flags)
+        assert np.array_equal(hit, ref["hit_tri"]) and np.array_equal(t.view(np.uint32), ref["t"].view(np.uint32))
+        assert_counts_equal(crsh.stats(tr.scene), ref)
+        assert_taps_equal(tr, ref, w)
