@@ -316,6 +316,9 @@ constexpr int LOWQ = 64;                     // capacity of a warp queue below l
 #ifndef CRSH_LDS32
 #define CRSH_LDS32 1   // child records through 32-bit shared addresses (A/B cfg4 R6 18.78 -> 18.85)
 #endif
+#ifndef CRSH_TOP_UNIFORM
+#define CRSH_TOP_UNIFORM 1   // top-level pair skips on a uniform mask, records through 32-bit shared addresses
+#endif
 #ifndef CRSH_TRAV_PREFETCH
 #define CRSH_TRAV_PREFETCH 0
 #endif
@@ -447,6 +450,7 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
   float4* s_pairs = reinterpret_cast<float4*>(smraw + L.off_pairs);
   float4* s_tpairs = reinterpret_cast<float4*>(smraw + L.off_tpairs);
   const uint32_t pairs_s = (uint32_t)__cvta_generic_to_shared(s_pairs);   // 32-bit shared address (CRSH_LDS32)
+  const uint32_t tpairs_s = (uint32_t)__cvta_generic_to_shared(s_tpairs);
   __shared__ uint32_t s_item, s_cur_g, s_n_act, s_carry, s_carry_c, s_blk;
   __shared__ uint32_t s_warp[TRAV_WARPS];
   __shared__ unsigned long long s_ctr[MAX_SEG * CTR_STRIDE];
@@ -845,6 +849,19 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
       // records); a lane tests node j only if its triangle's mesh survived
       // j's mesh cull. pm = the lane's passing top nodes.
       uint32_t pm = 0;
+#if CRSH_TOP_UNIFORM
+      // the nodes some lane's mesh kept, as one uniform mask: the pair skips
+      // are uniform branches, and the lane's own mesh mask is applied once
+      const uint32_t nmu = __reduce_or_sync(CRSH_FULL, nm);
+#pragma unroll
+      for (int j = 0; j < K; j += 2) {
+        if (((nmu >> j) & 3u) == 0u) continue;   // no lane's mesh kept node j or j+1
+        bool p0, p1;
+        cull2_ns_s(tpairs_s + 80u * (uint32_t)(j >> 1), Px, Py, Pz, Pr, p0, p1);
+        pm |= (p0 ? 1u << j : 0u) | (p1 ? 2u << j : 0u);
+      }
+      pm &= nm;
+#else
 #pragma unroll
       for (int j = 0; j < K; j += 2) {
         const bool n0 = (nm >> j) & 1u, n1 = (nm >> (j + 1)) & 1u;
@@ -855,6 +872,7 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
         p1 &= n1;
         pm |= ((uint32_t)p0 << j) | ((uint32_t)p1 << (j + 1));
       }
+#endif
       c_top_t += __popc(nm);   // every (node, triangle) with a surviving mesh was tested (skipped pairs have none)
       c_top_h += __popc(pm);
       // then each top node that passed for some lane

@@ -1,3 +1,2 @@
-python -m pytest tests -m gpu -q -x > gpurun_out/gpu_tests.log 2>&1; echo "rc=$?" >> gpurun_out/gpu_tests.log; tail -3 gpurun_out/gpu_tests.log
-bash tools/ab_trav.sh "2 3 4" "--zorder --objtree,--zorder, " ot4 sp 2>/dev/null
-bash tools/ab_stages.sh ot4 sp 2>/dev/null
+# A/B: sparse child tests threshold (CRSH_SPARSE_CHILD)
+bash tools/ab_trav.sh "4 3" "--zorder, ,--zorder --objtree" sp0 sp8 sp16 sp24 2>/dev/null
