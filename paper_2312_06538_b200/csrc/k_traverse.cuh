@@ -319,6 +319,9 @@ constexpr int LOWQ = 64;                     // capacity of a warp queue below l
 #ifndef CRSH_TOP_UNIFORM
 #define CRSH_TOP_UNIFORM 1   // top-level pair skips on a uniform mask, records through 32-bit shared addresses
 #endif
+#ifndef CRSH_SEL_BITS
+#define CRSH_SEL_BITS 1   // Eq 9 pair decisions as mask bits (chained setp + one select per test)
+#endif
 #ifndef CRSH_TRAV_PREFETCH
 #define CRSH_TRAV_PREFETCH 0
 #endif
@@ -856,9 +859,13 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
 #pragma unroll
       for (int j = 0; j < K; j += 2) {
         if (((nmu >> j) & 3u) == 0u) continue;   // no lane's mesh kept node j or j+1
+#if CRSH_SEL_BITS
+        pm |= cull2_bits_s(tpairs_s + 80u * (uint32_t)(j >> 1), Px, Py, Pz, Pr, 1u << j, 2u << j);
+#else
         bool p0, p1;
         cull2_ns_s(tpairs_s + 80u * (uint32_t)(j >> 1), Px, Py, Pz, Pr, p0, p1);
         pm |= (p0 ? 1u << j : 0u) | (p1 ? 2u << j : 0u);
+#endif
       }
       pm &= nm;
 #else
@@ -901,7 +908,10 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
           if (!BT && c >= B) break;
           bool p0, p1;
           if (SMALL) {
-#if CRSH_LDS32
+#if CRSH_SEL_BITS && CRSH_LDS32
+            m |= cull2_bits_s(pairs_s + 80u * ((cbase >> 1) + (uint32_t)(c >> 1)), Px, Py, Pz, Pr, 1u << c, 2u << c);
+            continue;
+#elif CRSH_LDS32
             cull2_ns_s(pairs_s + 80u * ((cbase >> 1) + (uint32_t)(c >> 1)), Px, Py, Pz, Pr, p0, p1);
 #else
             cull2_ns(s_pairs + 5 * ((cbase >> 1) + (uint32_t)(c >> 1)), Px, Py, Pz, Pr, p0, p1);

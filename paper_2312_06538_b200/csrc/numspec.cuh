@@ -261,26 +261,54 @@ __device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) { return __ffma2_rn(a, b, c
 // {Cx0,Cx1,Cy0,Cy1}, {Cz0,Cz1,d0,d1}, {ax0,ax1,ay0,ay1}, {az0,az1,tan0,tan1}, {sec0,sec1,-,-}
 // Eq 9 for both children against one target sphere (px,py,pz,r); same
 // operation order as cull_ns.
-__device__ __forceinline__ void cull2_ns(const float4* rec, f2 Px, f2 Py, f2 Pz, f2 R, bool& p0, bool& p1) {
+__device__ __forceinline__ void cull2_terms(const float4* rec, f2 Px, f2 Py, f2 Pz, f2 R, f2& s, f2& dr, f2& w2,
+                                            f2& rr) {
   const float4 A = rec[0], Bv = rec[1], Cc = rec[2], D = rec[3], E = rec[4];
   const f2 cx = pk2(A.x, A.y), cy = pk2(A.z, A.w), cz = pk2(Bv.x, Bv.y), dd = pk2(Bv.z, Bv.w);
   const f2 ax = pk2(Cc.x, Cc.y), ay = pk2(Cc.z, Cc.w), az = pk2(D.x, D.y), tn = pk2(D.z, D.w), sc = pk2(E.x, E.y);
   const f2 vx = sub2(Px, cx), vy = sub2(Py, cy), vz = sub2(Pz, cz);
-  const f2 s = fma2(vx, ax, fma2(vy, ay, mul2(vz, az)));
+  s = fma2(vx, ax, fma2(vy, ay, mul2(vz, az)));
   // w = v + s * (-a) = fma(-s, a, v) exactly (negation is exact)
   const f2 wx = fma2(s, pk2(-Cc.x, -Cc.y), vx), wy = fma2(s, pk2(-Cc.z, -Cc.w), vy), wz = fma2(s, pk2(-D.x, -D.y), vz);
-  const f2 w2 = fma2(wx, wx, fma2(wy, wy, mul2(wz, wz)));
-  const f2 dr = add2(dd, R);
+  w2 = fma2(wx, wx, fma2(wy, wy, mul2(wz, wz)));
+  dr = add2(dd, R);
   float s0, s1;
   up2(s, s0, s1);
   const f2 rhs = fma2(pk2(fmaxf(s0, 0.0f), fmaxf(s1, 0.0f)), tn, mul2(dr, sc));
-  const f2 rr = mul2(rhs, rhs);
-  float w0, w1, r0, r1, d0, d1;
+  rr = mul2(rhs, rhs);
+}
+__device__ __forceinline__ void cull2_ns(const float4* rec, f2 Px, f2 Py, f2 Pz, f2 R, bool& p0, bool& p1) {
+  f2 s, dr, w2, rr;
+  cull2_terms(rec, Px, Py, Pz, R, s, dr, w2, rr);
+  float s0, s1, w0, w1, r0, r1, d0, d1;
+  up2(s, s0, s1);
   up2(w2, w0, w1);
   up2(rr, r0, r1);
   up2(dr, d0, d1);
   p0 = (s0 >= -d0) & (w0 <= r0);
   p1 = (s1 >= -d1) & (w1 <= r1);
+}
+// the same two decisions as mask bits, (p0 ? bit0 : 0) | (p1 ? bit1 : 0): the
+// two compares of each test chained in one predicate (setp ... .and) and one
+// select per test, instead of the compiler's per-compare selects
+__device__ __forceinline__ uint32_t cull2_bits(const float4* rec, f2 Px, f2 Py, f2 Pz, f2 R, uint32_t bit0,
+                                               uint32_t bit1) {
+  f2 s, dr, w2, rr;
+  cull2_terms(rec, Px, Py, Pz, R, s, dr, w2, rr);
+  float s0, s1, w0, w1, r0, r1, d0, d1;
+  up2(s, s0, s1);
+  up2(w2, w0, w1);
+  up2(rr, r0, r1);
+  up2(dr, d0, d1);
+  uint32_t m;
+  asm("{\n\t.reg .pred q0, q1;\n\t.reg .f32 n0, n1;\n\t.reg .b32 t0, t1;\n\t"
+      "neg.f32 n0, %3;\n\tneg.f32 n1, %4;\n\t"
+      "setp.ge.f32 q0, %1, n0;\n\tsetp.le.and.f32 q0, %5, %7, q0;\n\t"
+      "setp.ge.f32 q1, %2, n1;\n\tsetp.le.and.f32 q1, %6, %8, q1;\n\t"
+      "selp.b32 t0, %9, 0, q0;\n\tselp.b32 t1, %10, 0, q1;\n\tor.b32 %0, t0, t1;\n\t}"
+      : "=r"(m)
+      : "f"(s0), "f"(s1), "f"(d0), "f"(d1), "f"(w0), "f"(w1), "f"(r0), "f"(r1), "r"(bit0), "r"(bit1));
+  return m;
 }
 // cull2_ns with the paired record read through a 32-bit shared-memory address
 // (ld.shared: no generic-to-shared window computation per record; the same
@@ -293,6 +321,11 @@ __device__ __forceinline__ float4 lds128(uint32_t addr) {
 __device__ __forceinline__ void cull2_ns_s(uint32_t rec, f2 Px, f2 Py, f2 Pz, f2 R, bool& p0, bool& p1) {
   const float4 r4[5] = {lds128(rec), lds128(rec + 16u), lds128(rec + 32u), lds128(rec + 48u), lds128(rec + 64u)};
   cull2_ns(r4, Px, Py, Pz, R, p0, p1);
+}
+__device__ __forceinline__ uint32_t cull2_bits_s(uint32_t rec, f2 Px, f2 Py, f2 Pz, f2 R, uint32_t bit0,
+                                                 uint32_t bit1) {
+  const float4 r4[5] = {lds128(rec), lds128(rec + 16u), lds128(rec + 32u), lds128(rec + 48u), lds128(rec + 64u)};
+  return cull2_bits(r4, Px, Py, Pz, R, bit0, bit1);
 }
 }  // namespace crsh
 
