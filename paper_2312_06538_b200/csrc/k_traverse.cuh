@@ -322,6 +322,9 @@ constexpr int LOWQ = 64;                     // capacity of a warp queue below l
 #ifndef CRSH_SEL_BITS
 #define CRSH_SEL_BITS 1   // Eq 9 pair decisions as mask bits (chained setp + one select per test)
 #endif
+#ifndef CRSH_DYN_SLICE
+#define CRSH_DYN_SLICE 1   // plain instantiation: slices of an item handed out by a shared counter
+#endif
 #ifndef CRSH_TRAV_PREFETCH
 #define CRSH_TRAV_PREFETCH 0
 #endif
@@ -539,8 +542,11 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
     }
     __syncthreads();
   };
+  // per-item barrier and slice counter: the object-tree instantiation (its
+  // cluster blocks) and, with CRSH_DYN_SLICE, the plain one (its slices)
+  constexpr bool PER_ITEM = OBJ || CRSH_DYN_SLICE;
   for (;;) {
-    if (OBJ || ch_next >= ch_end) {
+    if (PER_ITEM || ch_next >= ch_end) {
       __syncthreads();
       if (ch_next >= ch_end && tid == 0) s_item = atomicAdd(a.ticket, 1u) * chunk;
       __syncthreads();
@@ -678,8 +684,8 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
       }
       cur_g = g;
     }
-    if (OBJ && tid == 0) s_blk = 0u;
-    if (OBJ || new_group) {
+    if (PER_ITEM && tid == 0) s_blk = 0u;
+    if (PER_ITEM || new_group) {
       __syncthreads();
       n_act = s_n_act;
     }
@@ -978,6 +984,28 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
         const uint32_t tri = tri_n, nm = nm_n;
         const float4 sph = sph_n;
         if (s0 + TRAV_THREADS < item.z) fetch(s0 + TRAV_THREADS, tri_n, sph_n, nm_n);
+        slice_body(tri, sph, nm);
+      }
+#elif CRSH_DYN_SLICE
+      // slices handed out dynamically (a shared counter per item): the
+      // warps of an item finish within one slice of each other (static
+      // striding left them waiting at the chunk barrier, ncu cfg4 Z-order);
+      // each warp's slices still come in increasing order (mesh_of walks
+      // forward)
+      for (;;) {
+        uint32_t si = 0;
+        if (lane == 0) si = atomicAdd(&s_blk, 1u);
+        const uint32_t s0 = item.y + __shfl_sync(CRSH_FULL, si, 0) * 32u;
+        if (s0 >= item.z) break;
+        const uint32_t v = s0 + lane;
+        uint32_t nm = 0, tri = 0;
+        float4 sph = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (v < item.z) {
+          const uint32_t lo = mesh_of(v);
+          tri = s_act_first[lo] + (v - s_act_prefix[lo]);
+          sph = __ldg(a.tri_sph + tri);
+          nm = s_act_nmask[lo];
+        }
         slice_body(tri, sph, nm);
       }
 #else
