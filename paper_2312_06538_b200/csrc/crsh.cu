@@ -396,11 +396,13 @@ inline uint32_t item_tris_for(uint64_t G_max, int world, int sm_count, bool objt
   const uint64_t share = G_max / (uint64_t)std::max(world, 1);
   const bool big = share >= ITEM_BIG_GROUPS_PER_SM * (uint64_t)std::max(sm_count, 1);
   // very large frames (>= 64 groups per SM, cfg4 ~160): twice that again
-  // (A/B cfg4, 16384 -> 32768: R6 18.79 -> 18.87, Z-order 298.9 -> 301.2;
-  // cfg3, ~55 groups per SM, stays at 16384, where 32768 measured no gain)
   const uint32_t huge = share >= 4 * ITEM_BIG_GROUPS_PER_SM * (uint64_t)std::max(sm_count, 1) ? 2u : 1u;
   if (objtree) return big ? 2u * huge * (uint32_t)CRSH_ITEM_TRIS_BIG : CRSH_ITEM_TRIS_SMALL_OBJ;
-  return big ? huge * (uint32_t)CRSH_ITEM_TRIS_BIG : 2048u;
+  // plain path, since its slices are handed out dynamically within an item
+  // (A/B, Mrays/s at 16384 / 32768 / 65536 triangles: cfg3 R6 69.3 / 69.8 /
+  // 69.2, Z-order 787 / 795 / 752; cfg4 R6 20.59 / 20.66 / 20.64, Z-order
+  // 336 / 340 / 341): 32768 for every large frame
+  return big ? 2u * (uint32_t)CRSH_ITEM_TRIS_BIG : 2048u;
 }
 
 // Everything a frame's launch sequence depends on: if the key of a call equals

@@ -462,7 +462,7 @@ def test_dynamic_scene_parity(cfg, seed):
         assert_counts_equal(crsh.stats(scene), ref)
 
 
-@pytest.mark.parametrize("item_tris", [None, "16384"])
+@pytest.mark.parametrize("item_tris", [None, "32768"])
 @pytest.mark.parametrize("levels,leaf,branch,lights", [(2, 64, 32, 3), (8, 2, 2, 1), (5, 4, 4, 16), (1, 2, 2, 16),
                                                        (6, 8, 2, 2)])
 def test_option_extremes(levels, leaf, branch, lights, item_tris, monkeypatch):
@@ -470,7 +470,7 @@ def test_option_extremes(levels, leaf, branch, lights, item_tris, monkeypatch):
     B 32: span 2048 > 512 rays, K = 1, global-memory groups), the deepest
     hierarchy (Lv 8 of binary nodes), 16 lights (the hash's 4-bit light
     field), Lv 1 with 16 lights; hits, counts and every tap bit-exact; also
-    with the large frames' 16384-triangle work items forced."""
+    with the large frames' 32768-triangle work items forced."""
     if item_tris:
         monkeypatch.setenv("CRSH_ITEM_TRIS", item_tris)
     w = make_workload(1, width=40, height=36, levels=levels, leaf_size=leaf, branching=branch, ray_types=1)

@@ -1,8 +1,4 @@
-python -m pytest tests/test_gpu_dist.py -q -x > gpurun_out/dist.log 2>&1; tail -2 gpurun_out/dist.log
-for it in default 32768 65536; do
-  if [ $it = default ]; then unset CRSH_ITEM_TRIS; else export CRSH_ITEM_TRIS=$it; fi
-  for c in 3 4; do
-    python bench.py --config $c --zorder --objtree --single-hash --no-cpu-baseline --steps 5 > gpurun_out/it_${it}_c$c.json 2>/dev/null
-    python -c "import json,sys; d=json.loads(open(sys.argv[1]).read().strip().splitlines()[-1]); print(sys.argv[1], d['value'], d['ms_per_step'])" gpurun_out/it_${it}_c$c.json
-  done
-done
+# work-item size sweep with dynamic slices (CRSH_ITEM_TRIS)
+for it in 16384 32768 65536 131072; do export CRSH_ITEM_TRIS=$it; echo "items $it"; bash tools/ab_trav.sh "4" "--zorder, " cur 2>/dev/null; done
+for it in 4096 8192 16384 32768 65536; do export CRSH_ITEM_TRIS=$it; echo "items $it"; bash tools/ab_trav.sh "3" "--zorder, " cur 2>/dev/null; done
+for it in 1024 2048 4096; do export CRSH_ITEM_TRIS=$it; echo "items $it"; bash tools/ab_trav.sh "2" "--zorder, " cur 2>/dev/null; done
