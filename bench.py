@@ -126,18 +126,24 @@ def trav_flops(st):
     return eq9 * EQ9_FLOPS + int(sum(st["final_tests"])) * MT_FLOPS
 
 
-def load_traffic(config, zorder, kernel="k_traverse"):
-    """DRAM bytes per launch of `kernel` from the committed ncu launch list of
-    the same workload (profiles/ncu_summary*.json: cfg2, R6 or Z-order);
-    null for workloads without a committed capture."""
-    if config != 2:
-        return None
-    p = os.path.join(ROOT, "profiles", "ncu_summary_zorder.json" if zorder else "ncu_summary.json")
+def load_traffic(config, zorder, world=1):
+    """DRAM bytes (read + write) per launch of k_traverse from the committed
+    ncu --set full capture of the same workload (profiles/r2_ncu/
+    trav3_c4_{r6,z}_raw.csv: cfg4 on one GPU, final round-2 tree), with the
+    capture's path; (None, None) for workloads without one."""
+    if config != 4 or world != 1:
+        return None, None
+    rel = os.path.join("profiles", "r2_ncu", f"trav3_c4_{'z' if zorder else 'r6'}_raw.csv")
     try:
-        d = json.load(open(p))
-        return d.get("kernels", {}).get(kernel, {}).get("dram_bytes_per_launch")
-    except (OSError, ValueError):
-        return None
+        import csv
+        rows = list(csv.reader(open(os.path.join(ROOT, rel))))
+        h, u, v = rows[0], rows[1], rows[2]
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+        tot = sum(float(v[h.index(k)].replace(",", "")) * scale[u[h.index(k)]]
+                  for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+        return int(tot), rel
+    except (OSError, ValueError, KeyError, IndexError):
+        return None, None
 
 
 def paper_context():
@@ -398,6 +404,7 @@ def run_crsh(args):
 
     tfl, tfl_s = kernel_roof(m)
     hb, hms = hbm_roof(m)
+    traffic, traffic_src = (None, None) if args.objtree else load_traffic(args.config, main_z, world)
     t_roof = hb / (hbm_peak * 1e9) * 1e3 + trav_flops(st) / world / (peak_tflops * 1e12) * 1e3
     tests_all, final_all = int(np.asarray(st["tests"]).sum()), int(sum(st["final_tests"]))
     brute = rays * w.tris.shape[0]
@@ -417,13 +424,14 @@ def run_crsh(args):
         "stage_ms": {n: round(v, 4) for n, v in zip(crsh.STAGES, m["stage"])},
         "roofline": {
             "bound": "alu", "kernel": "k_traverse (a9-a12, the dominant kernel)", "achieved": round(tfl, 3),
-            "peak": round(peak_tflops, 2), "unit": "TFLOP/s", "frac": round(tfl / peak_tflops, 4), "traffic": None,
+            "peak": round(peak_tflops, 2), "unit": "TFLOP/s", "frac": round(tfl / peak_tflops, 4), "traffic": traffic,
             "flops_convention": f"{EQ9_FLOPS} flops per Eq 9 test and {MT_FLOPS} per Moller-Trumbore test, the "
                                 f"operations of the evaluated formulas (DESIGN.md §5); with SURVEY §8(d)'s estimates "
                                 f"(28 / 55) frac = {tfl_s / peak_tflops:.4f}",
             "frac_survey_convention": round(tfl_s / peak_tflops, 4),
             "note": f"peak: {peak_src}; kernel time from CUDA events around k_traverse on the frame's stream, "
-                    f"per GPU; traffic: see profiles/ (ncu --set full capture), not measured in this run",
+                    f"per GPU; traffic: DRAM read + write bytes per launch from "
+                    f"{traffic_src or 'no committed capture of this workload (null)'}",
             "hbm_stages": {"bound": "hbm", "stages": "a1-a8 (generate+trim, compress, sort, decompress, build)",
                            "bytes": int(hb), "ms": round(hms, 4), "achieved": round(hb / (hms * 1e-3) / 1e9, 1),
                            "peak": hbm_peak, "unit": "GB/s", "frac": round(hb / (hms * 1e-3) / 1e9 / hbm_peak, 4),

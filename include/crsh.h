@@ -21,6 +21,7 @@
  *    triangles per traversal work item; CRSH_BIG_TILES / CRSH_RLE_HIST = 0|1
  *    select the decompression-scan tile size / where the radix histograms are
  *    counted; CRSH_SLOT_MAJOR=1 selects the slot-major ray generator;
+ *    CRSH_OBJ_LIST_CAP=<n> bounds the object tree's per-round cluster list;
  *    CRSH_DIST_MERGE=nccl (read by crsh_dist_init) the all-reduce merge.
  */
 #ifndef CRSH_H_

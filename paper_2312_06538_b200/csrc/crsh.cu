@@ -252,6 +252,7 @@ struct FrameInfo {
   uint64_t level_max[MAX_LEVELS + 1] = {0};
   uint32_t flags = 0;
   uint32_t item_tris = 2048;                // triangles per traversal work item (item_tris_for)
+  uint32_t obj_list = CRSH_OBJ_LIST;        // object tree: cluster-list entries used per round (obj_list_for)
   bool big_tiles = false;                   // k_rle / k_scan_sizes with 8192-entry tiles (large frames)
   bool rle_hist = true;                     // k_rle builds the radix digit histograms (no k_radix_hist pass)
   int rank = 0, world = 1;
@@ -405,6 +406,16 @@ inline uint32_t item_tris_for(uint64_t G_max, int world, int sm_count, bool objt
   return big ? 2u * (uint32_t)CRSH_ITEM_TRIS_BIG : 2048u;
 }
 
+// Entries of K8's object-tree cluster list used per round: the compiled size,
+// or CRSH_OBJ_LIST_CAP (tests: a small list forces many rounds per item),
+// never below one block per warp (32 / K clusters each), the fill bound
+inline uint32_t obj_list_for(int K) {
+  const uint32_t lo = (32u / (uint32_t)std::max(K, 1)) * (uint32_t)TRAV_WARPS;
+  uint32_t v = CRSH_OBJ_LIST;
+  if (const char* e = std::getenv("CRSH_OBJ_LIST_CAP")) v = (uint32_t)std::max(0l, std::strtol(e, nullptr, 10));
+  return std::min<uint32_t>(std::max(v, lo), CRSH_OBJ_LIST);
+}
+
 // Everything a frame's launch sequence depends on: if the key of a call equals
 // the cached one, the cached CUDA graph is replayed.
 struct CallKey {
@@ -417,6 +428,7 @@ struct CallKey {
   uint64_t gen;
   uint32_t item_tris;
   uint32_t tiles;
+  uint32_t obj_list;
 };
 
 // The ray-definition part of K1's arguments (G-buffer, lights, slot layout);
@@ -686,6 +698,7 @@ crsh_status enqueue_frame(crsh_scene* sc, const FrameInfo& fi, const crsh_primar
         t.mesh_cluster_first = sc->cl_first.as<uint32_t>(); t.cluster_sph = sc->cl_sph.as<float4>();
       }
       t.items = sc->items.as<uint4>(); t.fd = fd; t.ticket = tickets + T_TRAV; t.M = (uint32_t)sc->M;
+      t.obj_list_cap = fi.obj_list;
       t.best = sc->best.as<unsigned long long>(); t.counters = counters; t.n_seg = fi.n_seg;
       const bool small = fi.GR <= SMALL_GROUP_RAYS;
       const TravSmem L = TravSmem::make(fi.K, B, sc->n_meshes, Lv, small, t.per_group, fi.GR);
@@ -844,6 +857,7 @@ crsh_status trace_impl(crsh_scene* sc, const crsh_primary_hits* h, const float* 
   for (int k = 1; k <= Lv; ++k) total_nodes += fi.level_max[k];
   const int W = (sc->n_meshes + 31) / 32;
   fi.item_tris = item_tris_for(fi.G_max, world, sc->sm_count, (fi.flags & CRSH_F_OBJTREE) != 0);
+  fi.obj_list = obj_list_for(fi.K);
   {   // decompression-scan tile size; radix histograms built by k_rle (A/B at cfg4: scan 178 -> 162 us with
       // 8192-entry tiles; sort 340 -> 319 us without the histogram pass). Overrides CRSH_BIG_TILES, CRSH_RLE_HIST.
     const char* e = std::getenv("CRSH_BIG_TILES");
@@ -854,6 +868,7 @@ crsh_status trace_impl(crsh_scene* sc, const crsh_primary_hits* h, const float* 
   sc->fi.big_tiles = fi.big_tiles;
   sc->fi.rle_hist = fi.rle_hist;
   sc->fi.item_tris = fi.item_tris;
+  sc->fi.obj_list = fi.obj_list;
   const uint64_t items_cap = std::max<uint64_t>(fi.G_max, 1) * cdiv(std::max<int64_t>(sc->M, 1), fi.item_tris);
   CK(grow(sc, sc->zero, Z.total));
   CK(grow(sc, sc->rays, 32 * S));
@@ -886,7 +901,7 @@ crsh_status trace_impl(crsh_scene* sc, const crsh_primary_hits* h, const float* 
   key.W = h->width; key.H = h->height; key.n_mat = h->n_mat; key.n_lights = n_lights;
   for (int i = 0; i < 3; ++i) key.eye[i] = h->eye[i];
   for (int i = 0; i < 3 * n_lights; ++i) key.lights[i] = lights[i];
-  key.types = types; key.o = *o; key.gen = sc->gen; key.item_tris = fi.item_tris;
+  key.types = types; key.o = *o; key.gen = sc->gen; key.item_tris = fi.item_tris; key.obj_list = fi.obj_list;
   key.tiles = (fi.big_tiles ? 1u : 0u) | (fi.rle_hist ? 2u : 0u);
   std::vector<unsigned char> kb(sizeof(CallKey));
   std::memcpy(kb.data(), &key, sizeof(CallKey));

@@ -325,6 +325,12 @@ constexpr int LOWQ = 64;                     // capacity of a warp queue below l
 #ifndef CRSH_DYN_SLICE
 #define CRSH_DYN_SLICE 1   // plain instantiation: slices of an item handed out by a shared counter
 #endif
+#ifndef CRSH_OBJ_TWOPHASE
+#define CRSH_OBJ_TWOPHASE 1   // object tree: cluster tests into a CTA list, then one passing cluster per claim
+#endif
+#ifndef CRSH_OBJ_LIST
+#define CRSH_OBJ_LIST 512     // entries of that list (8 bytes each)
+#endif
 #ifndef CRSH_TRAV_PREFETCH
 #define CRSH_TRAV_PREFETCH 0
 #endif
@@ -369,6 +375,7 @@ struct TravArgs {
   const float4* cluster_sph;
   const uint4* items;
   uint32_t M;                         // triangles (checked builds)
+  uint32_t obj_list_cap;              // object tree: entries of the cluster list used (<= CRSH_OBJ_LIST, >= CPB x warps)
   const FrameDesc* fd;                // n_items, seg_pad_base (group starts)
   uint32_t* ticket;
   unsigned long long* best;           // [Np]
@@ -458,6 +465,10 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
   const uint32_t pairs_s = (uint32_t)__cvta_generic_to_shared(s_pairs);   // 32-bit shared address (CRSH_LDS32)
   const uint32_t tpairs_s = (uint32_t)__cvta_generic_to_shared(s_tpairs);
   __shared__ uint32_t s_item, s_cur_g, s_n_act, s_carry, s_carry_c, s_blk;
+#if CRSH_OBJ_TWOPHASE
+  __shared__ uint32_t s_lcnt, s_lclaim, s_lexh;          // object tree: cluster list fill / claim, blocks exhausted
+  __shared__ uint2 s_list[OBJ ? CRSH_OBJ_LIST : 1];      // object tree: (cluster, node mask) of passing clusters
+#endif
   __shared__ uint32_t s_warp[TRAV_WARPS];
   __shared__ unsigned long long s_ctr[MAX_SEG * CTR_STRIDE];
   __shared__ uint32_t s_qlen[TRAV_WARPS][MAX_LEVELS + 1];
@@ -685,6 +696,9 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
       cur_g = g;
     }
     if (PER_ITEM && tid == 0) s_blk = 0u;
+#if CRSH_OBJ_TWOPHASE
+    if (OBJ && tid == 0) { s_lcnt = 0u; s_lclaim = 0u; s_lexh = 0u; }
+#endif
     if (PER_ITEM || new_group) {
       __syncthreads();
       n_act = s_n_act;
@@ -1035,6 +1049,80 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
       const uint32_t CPB = 32u / (uint32_t)K;   // K <= 32
       const uint32_t ci = lane / (uint32_t)K, jn = lane - ci * (uint32_t)K;
       const uint32_t kmask = K == 32 ? 0xFFFFFFFFu : ((1u << K) - 1u);
+#if CRSH_OBJ_TWOPHASE
+      // two phases per round: (A) blocks of clusters handed out dynamically,
+      // the cluster tests of a block at once, each cluster that passed some
+      // node appended to a CTA list (cluster, node mask); (B) the list's
+      // clusters handed out one per claim and streamed as slices. The heavy
+      // per-cluster work is then balanced to one slice (with whole blocks
+      // per claim, warps waited at the item barrier behind a few heavy
+      // blocks, ncu cfg4 Z-order + tree: 22 % of the stall samples). A round
+      // ends when the list could overflow; rounds repeat until the blocks
+      // are exhausted.
+      for (;;) {
+        mlo = 0xFFFFFFFFu;   // phase A claims increase per warp: a fresh forward walk
+        for (;;) {
+          if (*(volatile uint32_t*)&s_lcnt > a.obj_list_cap - CPB * TRAV_WARPS) break;   // list nearly full
+          uint32_t bi = 0;
+          if (lane == 0) bi = atomicAdd(&s_blk, 1u);
+          const uint32_t b0 = cy + __shfl_sync(CRSH_FULL, bi, 0) * CPB;
+          if (b0 >= cz) {
+            if (lane == 0) s_lexh = 1u;
+            break;
+          }
+          const uint32_t c = b0 + ci;
+          uint32_t lo = 0;
+          bool tst = false, pass = false;
+          if (ci < CPB && c < cz) {
+            lo = mesh_of(c * CLUSTER_TRIS);
+            tst = (s_act_nmask[lo] >> jn) & 1u;
+            if (tst) {
+              const float4 cs = __ldg(a.cluster_sph + s_act_cfirst[lo] + (c * CLUSTER_TRIS - s_act_prefix[lo]) / CLUSTER_TRIS);
+              const float4 t0 = s_top[3 * jn], t1 = s_top[3 * jn + 1], t2 = s_top[3 * jn + 2];
+              pass = cull_ns(mk3(t0.x, t0.y, t0.z), t0.w, mk3(t1.x, t1.y, t1.z), t1.w, t2.x, cs);
+            }
+          }
+          const uint32_t bt = __ballot_sync(CRSH_FULL, tst), bp = __ballot_sync(CRSH_FULL, pass);
+          if (lane == 0) { c_cl_t += __popc(bt); c_cl_h += __popc(bp); }
+          const uint32_t cmk_l = lane < CPB ? (bp >> (lane * (uint32_t)K)) & kmask : 0u;   // lane q: cluster b0+q
+          const uint32_t qm = __ballot_sync(CRSH_FULL, cmk_l != 0u);
+          if (qm) {
+            uint32_t base = 0;
+            if (lane == 0) base = atomicAdd(&s_lcnt, (uint32_t)__popc(qm));
+            base = __shfl_sync(CRSH_FULL, base, 0);
+            CRSH_CHECK(base + __popc(qm) <= a.obj_list_cap, 807);
+            if (cmk_l) s_list[base + __popc(qm & lt)] = make_uint2(b0 + lane, cmk_l);
+          }
+        }
+        __syncthreads();
+        const uint32_t n_list = s_lcnt;
+        for (;;) {
+          uint32_t ei = 0;
+          if (lane == 0) ei = atomicAdd(&s_lclaim, 1u);
+          ei = __shfl_sync(CRSH_FULL, ei, 0);
+          if (ei >= n_list) break;
+          const uint2 en = s_list[ei];
+          mlo = 0xFFFFFFFFu;   // list order is not monotone per warp: binary search
+          const uint32_t lok = mesh_of(en.x * CLUSTER_TRIS);
+          const uint32_t loc = en.x * CLUSTER_TRIS + lane - s_act_prefix[lok];
+          uint32_t tri = 0, nm = 0;
+          float4 sph = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (loc < s_act_cnt[lok]) {   // else a padding lane of the mesh's last cluster
+            const uint32_t pidx = s_act_first[lok] + loc;
+            tri = (uint32_t)__ldg(a.tri_order + pidx);
+            sph = __ldg(tsph + pidx);
+            nm = en.y;
+          }
+          slice_body(tri, sph, nm);
+        }
+        __syncthreads();
+        const bool exhausted = s_lexh != 0u;
+        __syncthreads();
+        if (exhausted) break;
+        if (tid == 0) { s_lcnt = 0u; s_lclaim = 0u; }
+        __syncthreads();
+      }
+#else
       // blocks are handed out dynamically (a shared counter per item): the
       // clusters that pass are unevenly spread, and static striding left
       // warps waiting at the item barrier (ncu cfg4: barrier stalls)
@@ -1073,6 +1161,7 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
           slice_body(tri, sph, nm);
         }
       }
+#endif
     }
     drain(true);
     // item counters -> the warp's running 64-bit counters (flushed to the CTA

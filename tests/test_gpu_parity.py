@@ -137,6 +137,23 @@ def test_option_space_many_triangles(levels, leaf, branch, item_tris, flags, mon
     assert_counts_equal(crsh.stats(tr.scene), ref)
 
 
+@pytest.mark.parametrize("cap", ["32", "96"])
+@pytest.mark.parametrize("flags", [67, 71])
+def test_objtree_cluster_list_rounds(flags, cap, monkeypatch):
+    """The object tree's two-phase items (cluster tests into a CTA list, then
+    one passing cluster per claim) with the list cut to a few dozen entries
+    (CRSH_OBJ_LIST_CAP) and 65536-triangle items, so every item needs many
+    fill / drain rounds: hits and every counter still equal the oracle's."""
+    monkeypatch.setenv("CRSH_OBJ_LIST_CAP", cap)
+    monkeypatch.setenv("CRSH_ITEM_TRIS", "65536")
+    w = make_workload(2, width=128, height=128)
+    tr, hit, t, ref = run_both(w, flags, taps=False)
+    assert np.array_equal(hit, ref["hit_tri"]) and np.array_equal(t.view(np.uint32), ref["t"].view(np.uint32))
+    st = crsh.stats(tr.scene)
+    assert_counts_equal(st, ref)
+    assert sum(st["cluster_hits"]) > 4 * int(cap)   # more passing clusters than one list holds
+
+
 @pytest.mark.parametrize("flags", [3, 7, 71])
 def test_cfg2_full_parity(flags):
     """cfg2 (512x512 SH+RE, ~70k tris / 16 meshes, Lv 2) at full size: all
