@@ -119,11 +119,19 @@ def frame_flops(st):
     return tests * EQ9_FLOPS + int(sum(st["final_tests"])) * MT_FLOPS
 
 
+def eq9_evaluated(st):
+    """Eq 9 tests k_traverse actually evaluated: the paper's counts of every
+    level (and the object tree's cluster tests), minus the counted child tests
+    the child prefilter proved failing without evaluating them, plus the
+    prefilter's own tests (crsh_stats_t child_skipped / prefilter_tests)."""
+    return (int(np.asarray(st["tests"]).sum()) + int(sum(st.get("cluster_tests", [0])))
+            - int(sum(st.get("child_skipped", [0]))) + int(sum(st.get("prefilter_tests", [0]))))
+
+
 def trav_flops(st):
-    """FP32 work of k_traverse: Eq 9 tests of every level (and of the object
-    tree's clusters) and Moller-Trumbore tests, from the frame's counters."""
-    eq9 = int(np.asarray(st["tests"]).sum()) + int(sum(st.get("cluster_tests", [0])))
-    return eq9 * EQ9_FLOPS + int(sum(st["final_tests"])) * MT_FLOPS
+    """FP32 work of k_traverse: the Eq 9 tests it evaluated and the
+    Moller-Trumbore tests, from the frame's counters."""
+    return eq9_evaluated(st) * EQ9_FLOPS + int(sum(st["final_tests"])) * MT_FLOPS
 
 
 def load_traffic(config, zorder, world=1):
@@ -392,8 +400,7 @@ def run_crsh(args):
         s_ = mm["st"]
         fl = trav_flops(s_) / world          # per GPU: each rank traverses its share
         a_ = fl / (mm["trav_ms"] * 1e-3) / 1e12 if mm["trav_ms"] > 0 else 0.0
-        fl_s = ((int(np.asarray(s_["tests"]).sum()) + int(sum(s_.get("cluster_tests", [0])))) * 28 +
-                int(sum(s_["final_tests"])) * 55) / world
+        fl_s = (eq9_evaluated(s_) * 28 + int(sum(s_["final_tests"])) * 55) / world
         a_s = fl_s / (mm["trav_ms"] * 1e-3) / 1e12 if mm["trav_ms"] > 0 else 0.0
         return a_, a_s
 
@@ -427,7 +434,10 @@ def run_crsh(args):
             "peak": round(peak_tflops, 2), "unit": "TFLOP/s", "frac": round(tfl / peak_tflops, 4), "traffic": traffic,
             "flops_convention": f"{EQ9_FLOPS} flops per Eq 9 test and {MT_FLOPS} per Moller-Trumbore test, the "
                                 f"operations of the evaluated formulas (DESIGN.md §5); with SURVEY §8(d)'s estimates "
-                                f"(28 / 55) frac = {tfl_s / peak_tflops:.4f}",
+                                f"(28 / 55) frac = {tfl_s / peak_tflops:.4f}; Eq 9 tests counted as evaluated: the "
+                                f"paper's counts - child tests skipped by the child prefilter "
+                                f"({int(sum(st.get('child_skipped', [0])))}) + prefilter tests "
+                                f"({int(sum(st.get('prefilter_tests', [0])))})",
             "frac_survey_convention": round(tfl_s / peak_tflops, 4),
             "note": f"peak: {peak_src}; kernel time from CUDA events around k_traverse on the frame's stream, "
                     f"per GPU; traffic: DRAM read + write bytes per launch from "

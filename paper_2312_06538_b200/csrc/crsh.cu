@@ -253,6 +253,7 @@ struct FrameInfo {
   uint32_t flags = 0;
   uint32_t item_tris = 2048;                // triangles per traversal work item (item_tris_for)
   uint32_t obj_list = CRSH_OBJ_LIST;        // object tree: cluster-list entries used per round (obj_list_for)
+  int32_t prefilter = 1;                    // K8 child prefilter (CRSH_NO_PREFILTER=1: off)
   bool big_tiles = false;                   // k_rle / k_scan_sizes with 8192-entry tiles (large frames)
   bool rle_hist = true;                     // k_rle builds the radix digit histograms (no k_radix_hist pass)
   int rank = 0, world = 1;
@@ -294,7 +295,7 @@ struct crsh_scene {
   std::vector<float> h_mesh_sph0;
   Dist* dist = nullptr;                 // crsh_dist_init: NCCL communicator, window, merge mode
   // object sphere-tree (CRSH_F_OBJTREE, reading O1): cluster order, ranges, spheres
-  Buf cl_order, cl_range, cl_first, cl_sph, tri_sph_ord;
+  Buf cl_order, cl_range, cl_first, cl_sph, tri_sph_ord, cl_pf;   // cl_pf: K8 child-prefilter spheres (k_cluster_pf)
   int64_t n_clusters = 0;
 };
 
@@ -429,6 +430,7 @@ struct CallKey {
   uint32_t item_tris;
   uint32_t tiles;
   uint32_t obj_list;
+  int32_t prefilter;
 };
 
 // The ray-definition part of K1's arguments (G-buffer, lights, slot layout);
@@ -641,6 +643,12 @@ crsh_status enqueue_frame(crsh_scene* sc, const FrameInfo& fi, const crsh_primar
 
     // ---------------------------------------------------------------- K7-K9: traversal
     const int W = (sc->n_meshes + 31) / 32;
+    // K8's child prefilter (the bench shape's plain instantiation): slices are
+    // the object-tree clusters (whole clusters per kept mesh, as with
+    // CRSH_F_OBJTREE), each with its prefilter sphere (k_cluster_pf)
+    const bool objt = (fi.flags & CRSH_F_OBJTREE) != 0;
+    const bool pf = fi.prefilter && !objt && sc->n_clusters > 0 && fi.GR <= SMALL_GROUP_RAYS && B == 8 && B0 == 8 &&
+                    Lv == 2 && fi.K == 8;
     CK(cudaMemsetAsync(sc->best.p, 0xFF, 8 * (size_t)fi.Np_max, st));
     {
       CullArgs a{};
@@ -657,7 +665,7 @@ crsh_status enqueue_frame(crsh_scene* sc, const FrameInfo& fi, const crsh_primar
         w.fd = fd; w.K = fi.K; w.W = W; w.n_meshes = sc->n_meshes;
         w.masks = sc->masks.as<uint32_t>(); w.mesh_count = sc->mesh_count.as<uint32_t>();
         w.trav_top = trav + 3 * fi.level_off[Lv]; w.cull_on = a.cull_on; w.n_nonempty = sc->n_nonempty;
-        w.objtree = (fi.flags & CRSH_F_OBJTREE) ? 1 : 0;
+        w.objtree = (objt || pf) ? 1 : 0;   // cluster-aligned virtual ranges
         w.work = sc->gwork.as<unsigned long long>(); w.gstat = sc->gstat.as<uint4>();
         k_group_work<<<cdiv(std::max<uint64_t>(fi.G_max, 1), 8), 256, 0, st>>>(w);
         CK(cudaGetLastError());
@@ -693,9 +701,10 @@ crsh_status enqueue_frame(crsh_scene* sc, const FrameInfo& fi, const crsh_primar
       t.tri_sph = sc->tri_sph.as<float4>();
       t.masks = sc->masks.as<uint32_t>(); t.W = W; t.n_meshes = sc->n_meshes;
       t.mesh_first = sc->mesh_first.as<uint32_t>(); t.mesh_count = sc->mesh_count.as<uint32_t>();
-      if (fi.flags & CRSH_F_OBJTREE) {
+      if (objt || pf) {
         t.tri_order = sc->cl_order.as<int32_t>(); t.tri_sph_ord = sc->tri_sph_ord.as<float4>();
         t.mesh_cluster_first = sc->cl_first.as<uint32_t>(); t.cluster_sph = sc->cl_sph.as<float4>();
+        t.cluster_pf = sc->cl_pf.as<float4>();
       }
       t.items = sc->items.as<uint4>(); t.fd = fd; t.ticket = tickets + T_TRAV; t.M = (uint32_t)sc->M;
       t.obj_list_cap = fi.obj_list;
@@ -714,6 +723,7 @@ crsh_status enqueue_frame(crsh_scene* sc, const FrameInfo& fi, const crsh_primar
       };
       auto pick = [&](auto obj) -> cudaError_t {
         constexpr bool O = decltype(obj)::value;
+        if (!O && pf) return launch(k_traverse<true, 8, 8, 2, false, true>);
         if (B == 8 && B0 == 8 && Lv == 2 && fi.K == 8)
           return small ? launch(k_traverse<true, 8, 8, 2, O>) : launch(k_traverse<false, 8, 8, 2, O>);
         if (B == 8 && B0 == 8) return small ? launch(k_traverse<true, 8, 8, 0, O>) : launch(k_traverse<false, 8, 8, 0, O>);
@@ -858,6 +868,10 @@ crsh_status trace_impl(crsh_scene* sc, const crsh_primary_hits* h, const float* 
   const int W = (sc->n_meshes + 31) / 32;
   fi.item_tris = item_tris_for(fi.G_max, world, sc->sm_count, (fi.flags & CRSH_F_OBJTREE) != 0);
   fi.obj_list = obj_list_for(fi.K);
+  {
+    const char* e = std::getenv("CRSH_NO_PREFILTER");
+    fi.prefilter = (e && std::atoi(e) != 0) ? 0 : 1;
+  }
   {   // decompression-scan tile size; radix histograms built by k_rle (A/B at cfg4: scan 178 -> 162 us with
       // 8192-entry tiles; sort 340 -> 319 us without the histogram pass). Overrides CRSH_BIG_TILES, CRSH_RLE_HIST.
     const char* e = std::getenv("CRSH_BIG_TILES");
@@ -869,6 +883,7 @@ crsh_status trace_impl(crsh_scene* sc, const crsh_primary_hits* h, const float* 
   sc->fi.rle_hist = fi.rle_hist;
   sc->fi.item_tris = fi.item_tris;
   sc->fi.obj_list = fi.obj_list;
+  sc->fi.prefilter = fi.prefilter;
   const uint64_t items_cap = std::max<uint64_t>(fi.G_max, 1) * cdiv(std::max<int64_t>(sc->M, 1), fi.item_tris);
   CK(grow(sc, sc->zero, Z.total));
   CK(grow(sc, sc->rays, 32 * S));
@@ -901,7 +916,7 @@ crsh_status trace_impl(crsh_scene* sc, const crsh_primary_hits* h, const float* 
   key.W = h->width; key.H = h->height; key.n_mat = h->n_mat; key.n_lights = n_lights;
   for (int i = 0; i < 3; ++i) key.eye[i] = h->eye[i];
   for (int i = 0; i < 3 * n_lights; ++i) key.lights[i] = lights[i];
-  key.types = types; key.o = *o; key.gen = sc->gen; key.item_tris = fi.item_tris; key.obj_list = fi.obj_list;
+  key.types = types; key.o = *o; key.gen = sc->gen; key.item_tris = fi.item_tris; key.obj_list = fi.obj_list; key.prefilter = fi.prefilter;
   key.tiles = (fi.big_tiles ? 1u : 0u) | (fi.rle_hist ? 2u : 0u);
   std::vector<unsigned char> kb(sizeof(CallKey));
   std::memcpy(kb.data(), &key, sizeof(CallKey));
@@ -1145,6 +1160,7 @@ crsh_status crsh_scene_create(const float* tris, const int32_t* mesh_ids, int64_
     ck(ensure(sc->cl_range, 8 * (size_t)std::max<int64_t>(sc->n_clusters, 1)), "alloc cl_range");
     ck(ensure(sc->cl_sph, 16 * (size_t)std::max<int64_t>(sc->n_clusters, 1)), "alloc cl_sph");
     ck(ensure(sc->tri_sph_ord, 16 * (size_t)M), "alloc tri_sph_ord");
+    ck(ensure(sc->cl_pf, 16 * (size_t)std::max<int64_t>(sc->n_clusters, 1)), "alloc cl_pf");
     if (rc == CRSH_OK) {
       ck(cudaMemcpy(sc->cl_order.p, order.data(), 4 * (size_t)M, cudaMemcpyHostToDevice), "copy cl_order");
       ck(cudaMemcpy(sc->cl_first.p, cfirst.data(), 4 * cfirst.size(), cudaMemcpyHostToDevice), "copy cl_first");
@@ -1156,6 +1172,8 @@ crsh_status crsh_scene_create(const float* tris, const int32_t* mesh_ids, int64_
       k_cluster_prep<<<grid, 256>>>(tris, sc->cl_order.as<int32_t>(), sc->cl_range.as<uint2>(), sc->n_clusters, sc->pad,
                                     sc->cl_sph.as<float4>());
       k_permute_sph<<<grid, 256>>>(sc->tri_sph.as<float4>(), sc->cl_order.as<int32_t>(), M, sc->tri_sph_ord.as<float4>());
+      k_cluster_pf<<<grid, 256>>>(sc->cl_sph.as<float4>(), sc->tri_sph_ord.as<float4>(), sc->cl_range.as<uint2>(),
+                                  sc->n_clusters, sc->cl_pf.as<float4>());
       ck(cudaGetLastError(), "k_cluster_prep");
     }
   }
@@ -1176,7 +1194,7 @@ void crsh_scene_destroy(crsh_scene_t sc) {
   for (auto& w : sc->wb) for (auto& b : w) b.release();
   sc->w_hit.release(); sc->w_t.release(); sc->w_zero.release(); sc->prim_rays.release();
   sc->tris0.release(); sc->mesh_ids.release(); sc->tris_cur.release(); sc->xf.release(); sc->boxk.release();
-  sc->cl_order.release(); sc->cl_range.release(); sc->cl_first.release(); sc->cl_sph.release(); sc->tri_sph_ord.release();
+  sc->cl_order.release(); sc->cl_range.release(); sc->cl_first.release(); sc->cl_sph.release(); sc->tri_sph_ord.release(); sc->cl_pf.release();
   if (sc->dist) {
     Dist* d = sc->dist;
     if (d->win) ncclCommWindowDeregister(d->comm, d->win);
@@ -1288,6 +1306,8 @@ crsh_status crsh_scene_transform(crsh_scene_t sc, const float* xforms) {
   k_cluster_prep<<<grid, 256>>>(sc->tris_cur.as<float>(), sc->cl_order.as<int32_t>(), sc->cl_range.as<uint2>(),
                                 sc->n_clusters, sc->pad, sc->cl_sph.as<float4>());
   k_permute_sph<<<grid, 256>>>(sc->tri_sph.as<float4>(), sc->cl_order.as<int32_t>(), sc->M, sc->tri_sph_ord.as<float4>());
+  k_cluster_pf<<<grid, 256>>>(sc->cl_sph.as<float4>(), sc->tri_sph_ord.as<float4>(), sc->cl_range.as<uint2>(),
+                              sc->n_clusters, sc->cl_pf.as<float4>());
   CK(cudaGetLastError());
   int box[6];
   CK(cudaMemcpy(box, sc->boxk.p, sizeof box, cudaMemcpyDeviceToHost));
@@ -1529,6 +1549,8 @@ crsh_status crsh_stats(crsh_scene_t sc, crsh_stats_t* out) {
     out->rays_hit[ty] = c[CTR_RAYS_HIT];
     out->cluster_tests[ty] = c[CTR_CL_TESTS];
     out->cluster_hits[ty] = c[CTR_CL_HITS];
+    out->child_skipped[ty] = c[CTR_CH_SKIP];
+    out->prefilter_tests[ty] = c[CTR_PF_TESTS];
     out->brute[ty] = (uint64_t)fi.fd.seg_n[s] * (uint64_t)sc->M;
   }
   if ((fi.timed || fi.ktimed) && fi.fd.N > 0) {

@@ -109,6 +109,26 @@ __global__ void k_permute_sph(const float4* __restrict__ tri_sph, const int32_t*
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < M; i += (int64_t)gridDim.x * blockDim.x)
     out[i] = tri_sph[order[i]];
 }
+// K8's child prefilter spheres (not the paper's arithmetic; k_traverse.cuh
+// cull_pf): per cluster, the cluster sphere's centre and a radius that
+// contains every triangle sphere of the cluster, |P_i - C| + R_i in double,
+// rounded up to float. Runs after k_permute_sph (tri_sph_ord).
+__global__ void k_cluster_pf(const float4* __restrict__ cl_sph, const float4* __restrict__ tri_sph_ord,
+                             const uint2* __restrict__ rng, int64_t n_clusters, float4* __restrict__ cl_pf) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n_clusters; c += (int64_t)gridDim.x * blockDim.x) {
+    const float4 C = cl_sph[c];
+    const uint2 r = rng[c];
+    double R = 0.0;
+    for (uint32_t i = r.x; i < r.y; ++i) {
+      const float4 t = tri_sph_ord[i];
+      const double dx = (double)t.x - (double)C.x, dy = (double)t.y - (double)C.y, dz = (double)t.z - (double)C.z;
+      R = fmax(R, sqrt(dx * dx + dy * dy + dz * dz) + (double)t.w);
+    }
+    float rf = (float)R;
+    if ((double)rf < R) rf = nextafterf(rf, __int_as_float(0x7f800000));
+    cl_pf[c] = make_float4(C.x, C.y, C.z, rf);
+  }
+}
 
 // ------------------------------------------------------------ nodes
 // so: (leaves) every ray of the bundle starts at the node centre, bit for bit

@@ -36,6 +36,8 @@ constexpr int CTR_FINAL_HITS = 21;
 constexpr int CTR_RAYS_HIT = 22;
 constexpr int CTR_CL_TESTS = 23;     // object sphere-tree (CRSH_F_OBJTREE): node vs cluster sphere
 constexpr int CTR_CL_HITS = 24;
+constexpr int CTR_CH_SKIP = 25;      // counted child tests K8 did not evaluate (child prefilter, cull_pf)
+constexpr int CTR_PF_TESTS = 26;     // child-prefilter tests evaluated
 constexpr int CTR_STRIDE = 32;
 constexpr uint32_t CLUSTER_TRIS = 32;   // triangles per object-tree cluster (reading O1): one warp slice
 
@@ -373,6 +375,7 @@ struct TravArgs {
   const float4* tri_sph_ord;
   const uint32_t* mesh_cluster_first;
   const float4* cluster_sph;
+  const float4* cluster_pf;           // PF: per cluster, a sphere containing its triangle spheres (k_cluster_pf)
   const uint4* items;
   uint32_t M;                         // triangles (checked builds)
   uint32_t obj_list_cap;              // object tree: entries of the cluster list used (<= CRSH_OBJ_LIST, >= CPB x warps)
@@ -430,6 +433,30 @@ struct TravSmem {
   }
 };
 
+// Conservative child prefilter (NOT the paper's arithmetic, and not part of
+// NUMSPEC: it only decides which Eq 9 evaluations can be skipped). Node
+// n0 = {C, d}, n1 = {a, tan}, sc = sec; S = a sphere containing the slice's
+// triangle spheres (k_cluster_pf). Eq 9 is monotone in the target sphere: if
+// (P, R) passes, so does every (P', R') with |P - P'| + R <= R' (the halfspace
+// term moves by at most the shift; the cone term by at most
+// |u_perp| + |u_par| tan <= |u| sec, Cauchy-Schwarz). The test is evaluated
+// with S's radius grown by 2^-12 of the magnitudes involved, ~200x the
+// float32 decision error of either evaluation (a few ulps of |v|, d, R: the
+// cone side is only near the boundary when rhs <= |w| <= |v|), so a false
+// here implies false for every triangle of the slice in cull2_ns.
+// Wide nodes (tan = sec = 1e30) always pass, as in Eq 9.
+__device__ __forceinline__ bool cull_pf(float4 n0, float4 n1, float sc, float4 S) {
+  const float vx = S.x - n0.x, vy = S.y - n0.y, vz = S.z - n0.z;
+  const float mag = fabsf(vx) + fabsf(vy) + fabsf(vz) + fabsf(n0.w) + S.w;
+  const float dr = n0.w + S.w + mag * 0x1p-12f;
+  const float s = vx * n1.x + vy * n1.y + vz * n1.z;
+  if (s < -dr) return false;
+  const float wx = vx - s * n1.x, wy = vy - s * n1.y, wz = vz - s * n1.z;
+  const float w2 = wx * wx + wy * wy + wz * wz;
+  const float rhs = fmaxf(s, 0.0f) * n1.w + dr * sc;
+  return w2 <= rhs * rhs;
+}
+
 // BT / B0T / LVT: compile-time branching factor / bundle size / levels (0 =
 // runtime a.B / a.B0 / a.Lv); with LVT the length of the bundle-level queue
 // Q[1] lives in a (warp-uniform) register instead of shared memory
@@ -444,7 +471,7 @@ struct TravSmem {
 #endif
 // OBJ: the object sphere-tree path (CRSH_F_OBJTREE) as its own instantiation,
 // so the plain path keeps its single slice loop (register allocation)
-template <bool SMALL, int BT, int B0T, int LVT, bool OBJ>
+template <bool SMALL, int BT, int B0T, int LVT, bool OBJ, bool PF = false>
 __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : CRSH_TRAV_MINB)
     k_traverse(const TravArgs a, const TravSmem L) {
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -454,7 +481,9 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
   uint32_t* s_act_first = reinterpret_cast<uint32_t*>(smraw + L.off_act_first);
   uint32_t* s_act_cnt = reinterpret_cast<uint32_t*>(smraw + L.off_act_cnt);
   uint32_t* s_act_cfirst = reinterpret_cast<uint32_t*>(smraw + L.off_act_cfirst);
-  constexpr bool objtree = OBJ;
+  // cluster-aligned slices: the object tree, or the child prefilter's
+  // clusters (PF: the plain traversal over the same cluster order)
+  constexpr bool objtree = OBJ || PF;
   const float4* tsph = objtree ? a.tri_sph_ord : a.tri_sph;
   unsigned long long* s_best = reinterpret_cast<unsigned long long*>(smraw + L.off_best);
   const float4* s_nodes = reinterpret_cast<const float4*>(smraw + L.off_nodes);
@@ -525,8 +554,9 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
   auto flush_acc = [&]() {
     if (acc_seg >= 0 && lane == 0) {
       unsigned long long* c = s_ctr + acc_seg * CTR_STRIDE;
-      if (acc_clt) atomicAdd(&c[CTR_CL_TESTS], acc_clt);
-      if (acc_clh) atomicAdd(&c[CTR_CL_HITS], acc_clh);
+      // (PF reuses the cluster counters for its prefilter tests / skipped child tests)
+      if (acc_clt) atomicAdd(&c[PF ? CTR_PF_TESTS : CTR_CL_TESTS], acc_clt);
+      if (acc_clh) atomicAdd(&c[PF ? CTR_CH_SKIP : CTR_CL_HITS], acc_clh);
       if (acc_tt) atomicAdd(&c[CTR_TESTS + Lv], acc_tt);
       if (acc_th) atomicAdd(&c[CTR_HITS + Lv], acc_th);
       if (Lv >= 2 && acc_ct) atomicAdd(&c[CTR_TESTS + Lv - 1], acc_ct);
@@ -866,7 +896,7 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
     };
     // one 32-triangle slice, lane = triangle (tri, sph), nm = the lane's top
     // nodes to test: the top-level tests, the dense child tests, the queues
-    auto slice_body = [&](uint32_t tri, float4 sph, uint32_t nm) {
+    auto slice_body = [&](uint32_t tri, float4 sph, uint32_t nm, float4 pfs) {
       const f2 Px = pk2(sph.x, sph.x), Py = pk2(sph.y, sph.y), Pz = pk2(sph.z, sph.z), Pr = pk2(sph.w, sph.w);
       // top level, all K nodes first: nodes (j, j+1) per packed test (paired
       // records); a lane tests node j only if its triangle's mesh survived
@@ -922,10 +952,28 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
         const int k1 = Lv - 1;
         const uint32_t cbase = (uint32_t)j << logB;
         const uint32_t exm = s_exm[j];
+        // PF: node j's children against the slice's prefilter sphere (lanes
+        // 0..7, one child each); a child pair neither of which passes is not
+        // evaluated for any lane: no triangle of the slice can pass it
+        uint32_t pfm = 0xFFFFFFFFu;
+        if constexpr (PF && SMALL && BT == 8) {
+          bool pp = false;
+          if (lane < 8u) {
+            const float4* nd = s_nodes + s_noff[k1] + 3 * (cbase + lane);
+            pp = cull_pf(nd[0], nd[1], nd[2].x, pfs);
+          }
+          pfm = __ballot_sync(CRSH_FULL, pp);
+          const uint32_t ev = (pfm | (pfm >> 1)) & 0x55u;   // pairs evaluated (bit 2p)
+          c_cl_t += __popc(exm);                              // prefilter tests (existing children)
+          c_cl_h += __popc(b) * __popc(exm & ~(ev | (ev << 1)));   // counted child tests not evaluated
+        }
         uint32_t m = 0;
 #pragma unroll
         for (int c = 0; c < (BT ? BT : 32); c += 2) {
           if (!BT && c >= B) break;
+          if constexpr (PF) {
+            if (((pfm >> c) & 3u) == 0u) continue;   // uniform
+          }
           bool p0, p1;
           if (SMALL) {
 #if CRSH_SEL_BITS && CRSH_LDS32
@@ -973,7 +1021,31 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
         drain(false);
       }
     };
-    if constexpr (!OBJ) {
+    if constexpr (PF) {
+      // child prefilter (the bench shape's plain traversal): slices are the
+      // clusters of the kept meshes (each mesh padded to whole clusters),
+      // handed out by a shared counter; lanes = the cluster's triangles in
+      // cluster order; the cluster's prefilter sphere rides along
+      for (;;) {
+        uint32_t si = 0;
+        if (lane == 0) si = atomicAdd(&s_blk, 1u);
+        const uint32_t s0 = item.y + __shfl_sync(CRSH_FULL, si, 0) * 32u;
+        if (s0 >= item.z) break;
+        const uint32_t lo = mesh_of(s0);   // a cluster-aligned slice lies in one mesh
+        const uint32_t rel = s0 - s_act_prefix[lo];
+        const uint32_t loc = rel + lane;
+        uint32_t tri = 0, nm = 0;
+        float4 sph = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (loc < s_act_cnt[lo]) {   // else a padding lane of the mesh's last cluster
+          const uint32_t pidx = s_act_first[lo] + loc;
+          tri = (uint32_t)__ldg(a.tri_order + pidx);
+          sph = __ldg(a.tri_sph_ord + pidx);
+          nm = s_act_nmask[lo];
+        }
+        const float4 pfs = __ldg(a.cluster_pf + s_act_cfirst[lo] + rel / CLUSTER_TRIS);
+        slice_body(tri, sph, nm, pfs);
+      }
+    } else if constexpr (!OBJ) {
 #if CRSH_TRAV_PREFETCH
       // software-pipelined slices: the next slice's mesh lookup and triangle
       // sphere load are issued before the current slice's tests, so the L2
@@ -998,7 +1070,7 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
         const uint32_t tri = tri_n, nm = nm_n;
         const float4 sph = sph_n;
         if (s0 + TRAV_THREADS < item.z) fetch(s0 + TRAV_THREADS, tri_n, sph_n, nm_n);
-        slice_body(tri, sph, nm);
+        slice_body(tri, sph, nm, make_float4(0.f, 0.f, 0.f, 0.f));
       }
 #elif CRSH_DYN_SLICE
       // slices handed out dynamically (a shared counter per item): the
@@ -1020,7 +1092,7 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
           sph = __ldg(a.tri_sph + tri);
           nm = s_act_nmask[lo];
         }
-        slice_body(tri, sph, nm);
+        slice_body(tri, sph, nm, make_float4(0.f, 0.f, 0.f, 0.f));
       }
 #else
       for (uint32_t s0 = item.y + warp * 32u; s0 < item.z; s0 += TRAV_THREADS) {
@@ -1033,7 +1105,7 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
           sph = __ldg(a.tri_sph + tri);
           nm = s_act_nmask[lo];
         }
-        slice_body(tri, sph, nm);
+        slice_body(tri, sph, nm, make_float4(0.f, 0.f, 0.f, 0.f));
       }
 #endif
     } else {
@@ -1113,7 +1185,7 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
             sph = __ldg(tsph + pidx);
             nm = en.y;
           }
-          slice_body(tri, sph, nm);
+          slice_body(tri, sph, nm, make_float4(0.f, 0.f, 0.f, 0.f));
         }
         __syncthreads();
         const bool exhausted = s_lexh != 0u;
@@ -1158,7 +1230,7 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
             sph = __ldg(tsph + pidx);
             nm = cmk;
           }
-          slice_body(tri, sph, nm);
+          slice_body(tri, sph, nm, make_float4(0.f, 0.f, 0.f, 0.f));
         }
       }
 #endif

@@ -154,6 +154,30 @@ def test_objtree_cluster_list_rounds(flags, cap, monkeypatch):
     assert sum(st["cluster_hits"]) > 4 * int(cap)   # more passing clusters than one list holds
 
 
+@pytest.mark.parametrize("flags", [3, 7])
+def test_child_prefilter_skips_only_failing_tests(flags, monkeypatch):
+    """K8's child prefilter (cull_pf: child nodes against a sphere containing
+    the slice's triangle spheres) only skips evaluations: hits, t and every
+    paper counter equal the oracle's with it on and off; with it on it skips
+    part of the counted child tests (child_skipped > 0) and evaluates
+    prefilter tests; off, both are zero."""
+    w = make_workload(2, width=160, height=160)
+    tr, hit, t, ref = run_both(w, flags, taps=False)
+    st_on = crsh.stats(tr.scene)
+    assert np.array_equal(hit, ref["hit_tri"]) and np.array_equal(t.view(np.uint32), ref["t"].view(np.uint32))
+    assert_counts_equal(st_on, ref)
+    assert sum(st_on["prefilter_tests"]) > 0 and sum(st_on["child_skipped"]) > 0
+    assert sum(st_on["child_skipped"]) <= int(np.asarray(st_on["tests"])[:, w.levels - 1].sum())
+    monkeypatch.setenv("CRSH_NO_PREFILTER", "1")
+    tr2 = tracer_for(w, flags=flags)
+    tr2.run()
+    hit2, t2 = tr2.results()
+    st_off = crsh.stats(tr2.scene)
+    assert np.array_equal(hit2, hit) and np.array_equal(t2.view(np.uint32), t.view(np.uint32))
+    assert_counts_equal(st_off, ref)
+    assert sum(st_off["prefilter_tests"]) == 0 and sum(st_off["child_skipped"]) == 0
+
+
 @pytest.mark.parametrize("flags", [3, 7, 71])
 def test_cfg2_full_parity(flags):
     """cfg2 (512x512 SH+RE, ~70k tris / 16 meshes, Lv 2) at full size: all
