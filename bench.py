@@ -123,9 +123,9 @@ def eq9_evaluated(st):
     """Eq 9 tests k_traverse actually evaluated: the paper's counts of every
     level (and the object tree's cluster tests), minus the counted child tests
     the child prefilter proved failing without evaluating them, plus the
-    prefilter's own tests (crsh_stats_t child_skipped / prefilter_tests)."""
+    prefilter's own tests (crsh_stats_t skipped_tests / prefilter_tests)."""
     return (int(np.asarray(st["tests"]).sum()) + int(sum(st.get("cluster_tests", [0])))
-            - int(sum(st.get("child_skipped", [0]))) + int(sum(st.get("prefilter_tests", [0]))))
+            - int(sum(st.get("skipped_tests", [0]))) + int(sum(st.get("prefilter_tests", [0]))))
 
 
 def trav_flops(st):
@@ -436,7 +436,7 @@ def run_crsh(args):
                                 f"operations of the evaluated formulas (DESIGN.md §5); with SURVEY §8(d)'s estimates "
                                 f"(28 / 55) frac = {tfl_s / peak_tflops:.4f}; Eq 9 tests counted as evaluated: the "
                                 f"paper's counts - child tests skipped by the child prefilter "
-                                f"({int(sum(st.get('child_skipped', [0])))}) + prefilter tests "
+                                f"({int(sum(st.get('skipped_tests', [0])))}) + prefilter tests "
                                 f"({int(sum(st.get('prefilter_tests', [0])))})",
             "frac_survey_convention": round(tfl_s / peak_tflops, 4),
             "note": f"peak: {peak_src}; kernel time from CUDA events around k_traverse on the frame's stream, "

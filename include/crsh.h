@@ -22,7 +22,8 @@
  *    select the decompression-scan tile size / where the radix histograms are
  *    counted; CRSH_SLOT_MAJOR=1 selects the slot-major ray generator;
  *    CRSH_OBJ_LIST_CAP=<n> bounds the object tree's per-round cluster list;
- *    CRSH_NO_PREFILTER=1 disables K8's child prefilter (crsh_stats_t);
+ *    CRSH_NO_PREFILTER=1 disables K8's child prefilter and CRSH_TOP_PREFILTER=0|1
+ *    overrides the per-hash choice of its top-level prefilter (crsh_stats_t);
  *    CRSH_DIST_MERGE=nccl (read by crsh_dist_init) the all-reduce merge.
  */
 #ifndef CRSH_H_
@@ -155,14 +156,14 @@ typedef struct {
                         mesh-cull+plan, traverse+final, output */
   uint64_t cluster_tests[3], cluster_hits[3];   /* CRSH_F_OBJTREE: node-vs-cluster-sphere tests / passes */
   /* Work K8 actually evaluated, beside the paper's counts above (which do not
-   * depend on it): of the counted child tests (the Lv-1 level of tests[][]),
-   * child_skipped were never evaluated because a conservative bound proved
-   * them failing -- the child nodes tested against a sphere containing the
-   * 32 triangle spheres of the slice, with a rounding margin (cull_pf in
-   * k_traverse.cuh); prefilter_tests counts those bound tests. Hits and every
-   * paper count are identical with and without the prefilter (set
-   * CRSH_NO_PREFILTER=1 to disable it; then child_skipped = 0). */
-  uint64_t child_skipped[3], prefilter_tests[3];
+   * depend on it): of the counted Eq 9 tests, skipped_tests were never
+   * evaluated because a conservative bound proved them failing -- the child
+   * nodes (and, with CRSH_TOP_PREFILTER=1, the top nodes) tested against a
+   * sphere containing the 32 triangle spheres of the slice, with a rounding
+   * margin (cull_pf in k_traverse.cuh); prefilter_tests counts those bound
+   * tests. Hits and every paper count are identical with and without the
+   * prefilter (CRSH_NO_PREFILTER=1 disables it; then both are 0). */
+  uint64_t skipped_tests[3], prefilter_tests[3];
 } crsh_stats_t;
 
 /* Number of ray slots: P * (n_lights*[SH] + [RE] + [RR]). Slot order (the ray

@@ -72,7 +72,7 @@ class Stats(C.Structure):
                 ("final_tests", C.c_uint64 * 3), ("final_hits", C.c_uint64 * 3), ("rays_hit", C.c_uint64 * 3),
                 ("brute", C.c_uint64 * 3), ("levels", C.c_int32), ("merge", C.c_int32),
                 ("stage_ms", C.c_float * 8), ("cluster_tests", C.c_uint64 * 3), ("cluster_hits", C.c_uint64 * 3),
-                ("child_skipped", C.c_uint64 * 3), ("prefilter_tests", C.c_uint64 * 3)]
+                ("skipped_tests", C.c_uint64 * 3), ("prefilter_tests", C.c_uint64 * 3)]
 
 
 _lib = None
@@ -273,7 +273,7 @@ def stats(scene: Scene) -> dict:
                 hits=np.array([list(r) for r in s.hits], np.uint64), final_tests=list(s.final_tests),
                 final_hits=list(s.final_hits), rays_hit=list(s.rays_hit), brute=list(s.brute), levels=s.levels,
                 merge=s.merge, stage_ms=list(s.stage_ms), cluster_tests=list(s.cluster_tests),
-                cluster_hits=list(s.cluster_hits), child_skipped=list(s.child_skipped),
+                cluster_hits=list(s.cluster_hits), skipped_tests=list(s.skipped_tests),
                 prefilter_tests=list(s.prefilter_tests))
 
 

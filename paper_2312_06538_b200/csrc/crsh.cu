@@ -254,6 +254,7 @@ struct FrameInfo {
   uint32_t item_tris = 2048;                // triangles per traversal work item (item_tris_for)
   uint32_t obj_list = CRSH_OBJ_LIST;        // object tree: cluster-list entries used per round (obj_list_for)
   int32_t prefilter = 1;                    // K8 child prefilter (CRSH_NO_PREFILTER=1: off)
+  int32_t top_prefilter = 0;                // K8 top-level prefilter (plan_frame; CRSH_TOP_PREFILTER=0|1)
   bool big_tiles = false;                   // k_rle / k_scan_sizes with 8192-entry tiles (large frames)
   bool rle_hist = true;                     // k_rle builds the radix digit histograms (no k_radix_hist pass)
   int rank = 0, world = 1;
@@ -430,7 +431,7 @@ struct CallKey {
   uint32_t item_tris;
   uint32_t tiles;
   uint32_t obj_list;
-  int32_t prefilter;
+  int32_t prefilter, top_prefilter;
 };
 
 // The ray-definition part of K1's arguments (G-buffer, lights, slot layout);
@@ -723,7 +724,8 @@ crsh_status enqueue_frame(crsh_scene* sc, const FrameInfo& fi, const crsh_primar
       };
       auto pick = [&](auto obj) -> cudaError_t {
         constexpr bool O = decltype(obj)::value;
-        if (!O && pf) return launch(k_traverse<true, 8, 8, 2, false, true>);
+        if (!O && pf)
+          return fi.top_prefilter ? launch(k_traverse<true, 8, 8, 2, false, 2>) : launch(k_traverse<true, 8, 8, 2, false, 1>);
         if (B == 8 && B0 == 8 && Lv == 2 && fi.K == 8)
           return small ? launch(k_traverse<true, 8, 8, 2, O>) : launch(k_traverse<false, 8, 8, 2, O>);
         if (B == 8 && B0 == 8) return small ? launch(k_traverse<true, 8, 8, 0, O>) : launch(k_traverse<false, 8, 8, 0, O>);
@@ -871,6 +873,11 @@ crsh_status trace_impl(crsh_scene* sc, const crsh_primary_hits* h, const float* 
   {
     const char* e = std::getenv("CRSH_NO_PREFILTER");
     fi.prefilter = (e && std::atoi(e) != 0) ? 0 : 1;
+    // the top-level prefilter pays where most top-level tests fail: with the
+    // Z-order hash (cfg4 Z-order 332 -> 408 Mrays/s), not with R6 (70 % of
+    // the top-level tests pass: 23.7 -> 22.7)
+    const char* t = std::getenv("CRSH_TOP_PREFILTER");
+    fi.top_prefilter = t ? (std::atoi(t) != 0) : ((fi.flags & CRSH_F_ZORDER) ? 1 : 0);
   }
   {   // decompression-scan tile size; radix histograms built by k_rle (A/B at cfg4: scan 178 -> 162 us with
       // 8192-entry tiles; sort 340 -> 319 us without the histogram pass). Overrides CRSH_BIG_TILES, CRSH_RLE_HIST.
@@ -884,7 +891,11 @@ crsh_status trace_impl(crsh_scene* sc, const crsh_primary_hits* h, const float* 
   sc->fi.item_tris = fi.item_tris;
   sc->fi.obj_list = fi.obj_list;
   sc->fi.prefilter = fi.prefilter;
-  const uint64_t items_cap = std::max<uint64_t>(fi.G_max, 1) * cdiv(std::max<int64_t>(sc->M, 1), fi.item_tris);
+  sc->fi.top_prefilter = fi.top_prefilter;
+  // a group's virtual range is at most M, or M + 31 per mesh when meshes are
+  // padded to whole clusters (object tree, K8-PF)
+  const int64_t M_virt = sc->M + (int64_t)(CLUSTER_TRIS - 1) * sc->n_meshes;
+  const uint64_t items_cap = std::max<uint64_t>(fi.G_max, 1) * cdiv(std::max<int64_t>(M_virt, 1), fi.item_tris);
   CK(grow(sc, sc->zero, Z.total));
   CK(grow(sc, sc->rays, 32 * S));
   CK(grow(sc, sc->px_tiles, 12 * ((size_t)cdiv((uint64_t)h->width * h->height, px_tile(2)) + 1)));
@@ -917,6 +928,7 @@ crsh_status trace_impl(crsh_scene* sc, const crsh_primary_hits* h, const float* 
   for (int i = 0; i < 3; ++i) key.eye[i] = h->eye[i];
   for (int i = 0; i < 3 * n_lights; ++i) key.lights[i] = lights[i];
   key.types = types; key.o = *o; key.gen = sc->gen; key.item_tris = fi.item_tris; key.obj_list = fi.obj_list; key.prefilter = fi.prefilter;
+  key.top_prefilter = fi.top_prefilter;
   key.tiles = (fi.big_tiles ? 1u : 0u) | (fi.rle_hist ? 2u : 0u);
   std::vector<unsigned char> kb(sizeof(CallKey));
   std::memcpy(kb.data(), &key, sizeof(CallKey));
@@ -1549,7 +1561,7 @@ crsh_status crsh_stats(crsh_scene_t sc, crsh_stats_t* out) {
     out->rays_hit[ty] = c[CTR_RAYS_HIT];
     out->cluster_tests[ty] = c[CTR_CL_TESTS];
     out->cluster_hits[ty] = c[CTR_CL_HITS];
-    out->child_skipped[ty] = c[CTR_CH_SKIP];
+    out->skipped_tests[ty] = c[CTR_CH_SKIP];
     out->prefilter_tests[ty] = c[CTR_PF_TESTS];
     out->brute[ty] = (uint64_t)fi.fd.seg_n[s] * (uint64_t)sc->M;
   }

@@ -36,7 +36,7 @@ constexpr int CTR_FINAL_HITS = 21;
 constexpr int CTR_RAYS_HIT = 22;
 constexpr int CTR_CL_TESTS = 23;     // object sphere-tree (CRSH_F_OBJTREE): node vs cluster sphere
 constexpr int CTR_CL_HITS = 24;
-constexpr int CTR_CH_SKIP = 25;      // counted child tests K8 did not evaluate (child prefilter, cull_pf)
+constexpr int CTR_CH_SKIP = 25;      // counted Eq 9 tests K8 did not evaluate (prefilter, cull_pf)
 constexpr int CTR_PF_TESTS = 26;     // child-prefilter tests evaluated
 constexpr int CTR_STRIDE = 32;
 constexpr uint32_t CLUSTER_TRIS = 32;   // triangles per object-tree cluster (reading O1): one warp slice
@@ -100,7 +100,7 @@ struct WorkArgs {
   const uint32_t* mesh_count;
   const float4* trav_top;      // node existence (radius >= 0)
   int32_t cull_on, n_nonempty;
-  int32_t objtree;             // CRSH_F_OBJTREE: a mesh's triangles count in whole clusters (slices)
+  int32_t objtree;             // CRSH_F_OBJTREE or K8-PF: a mesh's triangles count in whole clusters (slices)
   unsigned long long* work;    // [G] top-level tests of the group (the cut's work)
   uint4* gstat;                // [G] {triangles of the meshes any node kept, mesh tests, mesh passes, 0}
 };
@@ -125,10 +125,12 @@ __global__ void __launch_bounds__(256) k_group_work(const WorkArgs a) {
       nb = ((int)lane == b) ? c : nb;
     }
     const int m = w * 32 + (int)lane;
-    uint32_t cnt = (m < a.n_meshes) ? __ldg(a.mesh_count + m) : 0u;
-    if (a.objtree) cnt = (cnt + CLUSTER_TRIS - 1) / CLUSTER_TRIS * CLUSTER_TRIS;   // cluster-aligned virtual range
+    const uint32_t real = (m < a.n_meshes) ? __ldg(a.mesh_count + m) : 0u;
+    // cluster-aligned virtual range (items); the cut's work stays the
+    // group's top-level test count (real triangles only)
+    const uint32_t cnt = a.objtree ? (real + CLUSTER_TRIS - 1) / CLUSTER_TRIS * CLUSTER_TRIS : real;
     T += ((u >> lane) & 1u) ? cnt : 0u;
-    work += (unsigned long long)nb * cnt;
+    work += (unsigned long long)nb * real;
   }
   const uint32_t ex = (in && __ldg(&a.trav_top[3 * ((size_t)g * a.K + lane)].w) >= 0.0f) ? 1u : 0u;
   T = __reduce_add_sync(CRSH_FULL, T);
@@ -471,7 +473,7 @@ __device__ __forceinline__ bool cull_pf(float4 n0, float4 n1, float sc, float4 S
 #endif
 // OBJ: the object sphere-tree path (CRSH_F_OBJTREE) as its own instantiation,
 // so the plain path keeps its single slice loop (register allocation)
-template <bool SMALL, int BT, int B0T, int LVT, bool OBJ, bool PF = false>
+template <bool SMALL, int BT, int B0T, int LVT, bool OBJ, int PF = 0>
 __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : CRSH_TRAV_MINB)
     k_traverse(const TravArgs a, const TravSmem L) {
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -481,9 +483,10 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
   uint32_t* s_act_first = reinterpret_cast<uint32_t*>(smraw + L.off_act_first);
   uint32_t* s_act_cnt = reinterpret_cast<uint32_t*>(smraw + L.off_act_cnt);
   uint32_t* s_act_cfirst = reinterpret_cast<uint32_t*>(smraw + L.off_act_cfirst);
-  // cluster-aligned slices: the object tree, or the child prefilter's
-  // clusters (PF: the plain traversal over the same cluster order)
-  constexpr bool objtree = OBJ || PF;
+  // cluster-aligned slices: the object tree, or the prefilter's clusters
+  // (PF >= 1: the plain traversal over the same cluster order; PF = 1 child
+  // prefilter, PF = 2 child and top-level prefilter)
+  constexpr bool objtree = OBJ || PF > 0;
   const float4* tsph = objtree ? a.tri_sph_ord : a.tri_sph;
   unsigned long long* s_best = reinterpret_cast<unsigned long long*>(smraw + L.off_best);
   const float4* s_nodes = reinterpret_cast<const float4*>(smraw + L.off_nodes);
@@ -555,8 +558,8 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
     if (acc_seg >= 0 && lane == 0) {
       unsigned long long* c = s_ctr + acc_seg * CTR_STRIDE;
       // (PF reuses the cluster counters for its prefilter tests / skipped child tests)
-      if (acc_clt) atomicAdd(&c[PF ? CTR_PF_TESTS : CTR_CL_TESTS], acc_clt);
-      if (acc_clh) atomicAdd(&c[PF ? CTR_CH_SKIP : CTR_CL_HITS], acc_clh);
+      if (acc_clt) atomicAdd(&c[PF > 0 ? CTR_PF_TESTS : CTR_CL_TESTS], acc_clt);
+      if (acc_clh) atomicAdd(&c[PF > 0 ? CTR_CH_SKIP : CTR_CL_HITS], acc_clh);
       if (acc_tt) atomicAdd(&c[CTR_TESTS + Lv], acc_tt);
       if (acc_th) atomicAdd(&c[CTR_HITS + Lv], acc_th);
       if (Lv >= 2 && acc_ct) atomicAdd(&c[CTR_TESTS + Lv - 1], acc_ct);
@@ -905,10 +908,28 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
 #if CRSH_TOP_UNIFORM
       // the nodes some lane's mesh kept, as one uniform mask: the pair skips
       // are uniform branches, and the lane's own mesh mask is applied once
-      const uint32_t nmu = __reduce_or_sync(CRSH_FULL, nm);
+      uint32_t nmu = __reduce_or_sync(CRSH_FULL, nm);
+      if constexpr (PF == 2 && KT > 0 && KT <= 32) {
+        // top-level prefilter (PF = 2): the K top nodes against the slice's
+        // prefilter sphere, lanes 0..K-1; a node pair neither of which passes
+        // is not evaluated (its counted tests are reported as skipped)
+        {
+          bool pp = false;
+          if (lane < (uint32_t)KT) {
+            const float4* t = s_top + 3 * lane;
+            pp = cull_pf(t[0], t[1], t[2].x, pfs);
+          }
+          const uint32_t tp = __ballot_sync(CRSH_FULL, pp);
+          const uint32_t ev = (tp | (tp >> 1)) & 0x55555555u;   // pairs evaluated (bit 2p)
+          const uint32_t keep = ev | (ev << 1);
+          c_cl_t += lane == 0 ? (uint32_t)__popc(nmu) : 0u;   // prefilter tests: nodes some lane's mesh kept
+          c_cl_h += __popc(nm & ~keep);                        // this lane's counted top tests not evaluated
+          nmu &= keep;
+        }
+      }
 #pragma unroll
       for (int j = 0; j < K; j += 2) {
-        if (((nmu >> j) & 3u) == 0u) continue;   // no lane's mesh kept node j or j+1
+        if (((nmu >> j) & 3u) == 0u) continue;   // no lane's mesh kept node j or j+1 (or the prefilter rejected both)
 #if CRSH_SEL_BITS
         pm |= cull2_bits_s(tpairs_s + 80u * (uint32_t)(j >> 1), Px, Py, Pz, Pr, 1u << j, 2u << j);
 #else
@@ -956,7 +977,7 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
         // 0..7, one child each); a child pair neither of which passes is not
         // evaluated for any lane: no triangle of the slice can pass it
         uint32_t pfm = 0xFFFFFFFFu;
-        if constexpr (PF && SMALL && BT == 8) {
+        if constexpr (PF > 0 && SMALL && BT == 8) {
           bool pp = false;
           if (lane < 8u) {
             const float4* nd = s_nodes + s_noff[k1] + 3 * (cbase + lane);
@@ -964,14 +985,18 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
           }
           pfm = __ballot_sync(CRSH_FULL, pp);
           const uint32_t ev = (pfm | (pfm >> 1)) & 0x55u;   // pairs evaluated (bit 2p)
-          c_cl_t += __popc(exm);                              // prefilter tests (existing children)
-          c_cl_h += __popc(b) * __popc(exm & ~(ev | (ev << 1)));   // counted child tests not evaluated
+          // PF = 1: warp-uniform sums (lane 0's copy is flushed); PF = 2: sums
+          // over the lanes (the top-level skips are per lane), lane 0 adds here
+          if (PF == 1 || lane == 0) {
+            c_cl_t += __popc(exm);                                   // prefilter tests (existing children)
+            c_cl_h += __popc(b) * __popc(exm & ~(ev | (ev << 1)));   // counted child tests not evaluated
+          }
         }
         uint32_t m = 0;
 #pragma unroll
         for (int c = 0; c < (BT ? BT : 32); c += 2) {
           if (!BT && c >= B) break;
-          if constexpr (PF) {
+          if constexpr (PF > 0) {
             if (((pfm >> c) & 3u) == 0u) continue;   // uniform
           }
           bool p0, p1;
@@ -1021,7 +1046,7 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
         drain(false);
       }
     };
-    if constexpr (PF) {
+    if constexpr (PF > 0) {
       // child prefilter (the bench shape's plain traversal): slices are the
       // clusters of the kept meshes (each mesh padded to whole clusters),
       // handed out by a shared counter; lanes = the cluster's triangles in
@@ -1248,8 +1273,13 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
     acc_mh += __reduce_add_sync(CRSH_FULL, c_mt_h);
     acc_ch += __reduce_add_sync(CRSH_FULL, c_ch_h);
     acc_ct += c_ch_t;      // warp-uniform already
-    acc_clt += c_cl_t;     // lane 0 only (lane 0 flushes)
-    acc_clh += c_cl_h;
+    if constexpr (PF == 2) {   // per-lane sums
+      acc_clt += __reduce_add_sync(CRSH_FULL, c_cl_t);
+      acc_clh += __reduce_add_sync(CRSH_FULL, c_cl_h);
+    } else {
+      acc_clt += c_cl_t;     // lane 0 only (lane 0 flushes)
+      acc_clh += c_cl_h;
+    }
     if constexpr (OBJ) flush_acc();
   }
   group_end();

@@ -154,20 +154,23 @@ def test_objtree_cluster_list_rounds(flags, cap, monkeypatch):
     assert sum(st["cluster_hits"]) > 4 * int(cap)   # more passing clusters than one list holds
 
 
+@pytest.mark.parametrize("top", ["0", "1"])
 @pytest.mark.parametrize("flags", [3, 7])
-def test_child_prefilter_skips_only_failing_tests(flags, monkeypatch):
-    """K8's child prefilter (cull_pf: child nodes against a sphere containing
-    the slice's triangle spheres) only skips evaluations: hits, t and every
-    paper counter equal the oracle's with it on and off; with it on it skips
-    part of the counted child tests (child_skipped > 0) and evaluates
-    prefilter tests; off, both are zero."""
+def test_child_prefilter_skips_only_failing_tests(flags, top, monkeypatch):
+    """K8's prefilter (cull_pf: child nodes -- and with CRSH_TOP_PREFILTER=1
+    the top nodes -- against a sphere containing the slice's triangle
+    spheres) only skips evaluations: hits, t and every paper counter equal
+    the oracle's with it on and off; with it on it skips part of the counted
+    tests (skipped_tests > 0) and evaluates prefilter tests; off, both are
+    zero."""
+    monkeypatch.setenv("CRSH_TOP_PREFILTER", top)
     w = make_workload(2, width=160, height=160)
     tr, hit, t, ref = run_both(w, flags, taps=False)
     st_on = crsh.stats(tr.scene)
     assert np.array_equal(hit, ref["hit_tri"]) and np.array_equal(t.view(np.uint32), ref["t"].view(np.uint32))
     assert_counts_equal(st_on, ref)
-    assert sum(st_on["prefilter_tests"]) > 0 and sum(st_on["child_skipped"]) > 0
-    assert sum(st_on["child_skipped"]) <= int(np.asarray(st_on["tests"])[:, w.levels - 1].sum())
+    assert sum(st_on["prefilter_tests"]) > 0 and sum(st_on["skipped_tests"]) > 0
+    assert sum(st_on["skipped_tests"]) <= int(np.asarray(st_on["tests"]).sum())
     monkeypatch.setenv("CRSH_NO_PREFILTER", "1")
     tr2 = tracer_for(w, flags=flags)
     tr2.run()
@@ -175,7 +178,7 @@ def test_child_prefilter_skips_only_failing_tests(flags, monkeypatch):
     st_off = crsh.stats(tr2.scene)
     assert np.array_equal(hit2, hit) and np.array_equal(t2.view(np.uint32), t.view(np.uint32))
     assert_counts_equal(st_off, ref)
-    assert sum(st_off["prefilter_tests"]) == 0 and sum(st_off["child_skipped"]) == 0
+    assert sum(st_off["prefilter_tests"]) == 0 and sum(st_off["skipped_tests"]) == 0
 
 
 @pytest.mark.parametrize("flags", [3, 7, 71])
