@@ -137,11 +137,11 @@ def trav_flops(st):
 def load_traffic(config, zorder, world=1):
     """DRAM bytes (read + write) per launch of k_traverse from the committed
     ncu --set full capture of the same workload (profiles/r2_ncu/
-    trav3_c4_{r6,z}_raw.csv: cfg4 on one GPU, final round-2 tree), with the
+    trav4_c4_{r6,z}_raw.csv: cfg4 on one GPU, the prefilter tree), with the
     capture's path; (None, None) for workloads without one."""
     if config != 4 or world != 1:
         return None, None
-    rel = os.path.join("profiles", "r2_ncu", f"trav3_c4_{'z' if zorder else 'r6'}_raw.csv")
+    rel = os.path.join("profiles", "r2_ncu", f"trav4_c4_{'z' if zorder else 'r6'}_raw.csv")
     try:
         import csv
         rows = list(csv.reader(open(os.path.join(ROOT, rel))))
