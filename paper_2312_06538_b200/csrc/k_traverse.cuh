@@ -459,6 +459,37 @@ __device__ __forceinline__ bool cull_pf(float4 n0, float4 n1, float sc, float4 S
   return w2 <= rhs * rhs;
 }
 
+// cull_pf for the two children of a paired child record (cull2_ns layout:
+// {Cx0,Cx1,Cy0,Cy1} {Cz0,Cz1,d0,d1} {ax0,ax1,ay0,ay1} {az0,az1,tan0,tan1}
+// {sec0,sec1,-,-}) in packed f32x2 arithmetic: the same bound and margin as
+// cull_pf (the FMA forms only round less). Returns bit 0 / bit 1: child 0 / 1
+// may pass.
+__device__ __forceinline__ uint32_t cull2_pf_s(uint32_t rec, float4 S) {
+  const float4 A = lds128(rec), Bv = lds128(rec + 16u), Cc = lds128(rec + 32u), D = lds128(rec + 48u),
+               E = lds128(rec + 64u);
+  const f2 vx = sub2(pk2(S.x, S.x), pk2(A.x, A.y)), vy = sub2(pk2(S.y, S.y), pk2(A.z, A.w)),
+           vz = sub2(pk2(S.z, S.z), pk2(Bv.x, Bv.y));
+  float x0, x1, y0, y1, z0, z1;
+  up2(vx, x0, x1);
+  up2(vy, y0, y1);
+  up2(vz, z0, z1);
+  const f2 mag = pk2(fabsf(x0) + fabsf(y0) + fabsf(z0) + fabsf(Bv.z) + S.w,
+                     fabsf(x1) + fabsf(y1) + fabsf(z1) + fabsf(Bv.w) + S.w);
+  const f2 dr = fma2(mag, pk2(0x1p-12f, 0x1p-12f), add2(pk2(Bv.z, Bv.w), pk2(S.w, S.w)));
+  const f2 s = fma2(vx, pk2(Cc.x, Cc.y), fma2(vy, pk2(Cc.z, Cc.w), mul2(vz, pk2(D.x, D.y))));
+  const f2 wx = fma2(s, pk2(-Cc.x, -Cc.y), vx), wy = fma2(s, pk2(-Cc.z, -Cc.w), vy), wz = fma2(s, pk2(-D.x, -D.y), vz);
+  const f2 w2 = fma2(wx, wx, fma2(wy, wy, mul2(wz, wz)));
+  float s0, s1;
+  up2(s, s0, s1);
+  const f2 rhs = fma2(pk2(fmaxf(s0, 0.0f), fmaxf(s1, 0.0f)), pk2(D.z, D.w), mul2(dr, pk2(E.x, E.y)));
+  const f2 rr = mul2(rhs, rhs);
+  float w0, w1, r0, r1, d0, d1;
+  up2(w2, w0, w1);
+  up2(rr, r0, r1);
+  up2(dr, d0, d1);
+  return ((s0 >= -d0) & (w0 <= r0) ? 1u : 0u) | ((s1 >= -d1) & (w1 <= r1) ? 2u : 0u);
+}
+
 // BT / B0T / LVT: compile-time branching factor / bundle size / levels (0 =
 // runtime a.B / a.B0 / a.Lv); with LVT the length of the bundle-level queue
 // Q[1] lives in a (warp-uniform) register instead of shared memory
@@ -909,6 +940,8 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
       // the nodes some lane's mesh kept, as one uniform mask: the pair skips
       // are uniform branches, and the lane's own mesh mask is applied once
       uint32_t nmu = __reduce_or_sync(CRSH_FULL, nm);
+      uint32_t pa = 0xFFFFFFFFu;   // PF: child pairs that may pass (lane-l bit: node l/4, pair l%4)
+      bool pa_done = false;
       if constexpr (PF == 2 && KT > 0 && KT <= 32) {
         // top-level prefilter (PF = 2): the K top nodes against the slice's
         // prefilter sphere, lanes 0..K-1; a node pair neither of which passes
@@ -973,31 +1006,31 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
         const int k1 = Lv - 1;
         const uint32_t cbase = (uint32_t)j << logB;
         const uint32_t exm = s_exm[j];
-        // PF: node j's children against the slice's prefilter sphere (lanes
-        // 0..7, one child each); a child pair neither of which passes is not
-        // evaluated for any lane: no triangle of the slice can pass it
-        uint32_t pfm = 0xFFFFFFFFu;
-        if constexpr (PF > 0 && SMALL && BT == 8) {
-          bool pp = false;
-          if (lane < 8u) {
-            const float4* nd = s_nodes + s_noff[k1] + 3 * (cbase + lane);
-            pp = cull_pf(nd[0], nd[1], nd[2].x, pfs);
+        // PF: the child pairs of node j that may pass for some triangle of
+        // the slice (all K x B children were tested once per slice against
+        // its prefilter sphere, below); a pair neither of whose children
+        // passes is not evaluated for any lane
+        uint32_t pfm = 0xFFFFFFFFu;   // bit 2p: child pair p may pass
+        if constexpr (PF > 0 && SMALL && BT == 8 && KT == 8) {
+          if (!pa_done) {   // uniform: the slice's first child iteration
+            pa = __ballot_sync(CRSH_FULL, cull2_pf_s(pairs_s + 80u * lane, pfs) != 0u);   // lane l: node l/4, pair l%4
+            pa_done = true;
+            if (PF == 1 || lane == 0) c_cl_t += (uint32_t)(KT * BT);   // prefilter tests evaluated
           }
-          pfm = __ballot_sync(CRSH_FULL, pp);
-          const uint32_t ev = (pfm | (pfm >> 1)) & 0x55u;   // pairs evaluated (bit 2p)
+          uint32_t x = (pa >> (4u * (uint32_t)j)) & 0xFu;   // pairs 0..3 of node j
+          x = (x | (x << 2)) & 0x33u;
+          x = (x | (x << 1)) & 0x55u;                       // pair p -> bit 2p
+          pfm = x;
           // PF = 1: warp-uniform sums (lane 0's copy is flushed); PF = 2: sums
           // over the lanes (the top-level skips are per lane), lane 0 adds here
-          if (PF == 1 || lane == 0) {
-            c_cl_t += __popc(exm);                                   // prefilter tests (existing children)
-            c_cl_h += __popc(b) * __popc(exm & ~(ev | (ev << 1)));   // counted child tests not evaluated
-          }
+          if (PF == 1 || lane == 0) c_cl_h += __popc(b) * __popc(exm & ~(x | (x << 1)));   // counted, not evaluated
         }
         uint32_t m = 0;
 #pragma unroll
         for (int c = 0; c < (BT ? BT : 32); c += 2) {
           if (!BT && c >= B) break;
           if constexpr (PF > 0) {
-            if (((pfm >> c) & 3u) == 0u) continue;   // uniform
+            if (((pfm >> c) & 1u) == 0u) continue;   // uniform
           }
           bool p0, p1;
           if (SMALL) {

@@ -3,8 +3,10 @@ K8-PF), on the CPU: Eq 9 as the oracle evaluates it (float32, the paper's
 order: PAPER.md:179-181, reading R12/R13) is monotone in the target sphere,
 and the prefilter's margin covers float32 rounding. If the oracle's test
 passes for a sphere (P, R), then the prefilter passes for every sphere (C, Rb)
-with |P - C| + R <= Rb. The prefilter is transcribed here in numpy float32 in
-the kernel's operation order, because the claim is about that evaluation.
+with |P - C| + R <= Rb. Both prefilter forms (the scalar `cull_pf` of the top level and the packed,
+fused `cull2_pf_s` of the child pairs) are transcribed here in numpy float32
+in the kernel's operation order, because the claim is about those
+evaluations.
 The inputs are random nodes (narrow to wide cones, and the pass-all wide
 nodes) and spheres placed on the pass/fail boundary, where rounding matters
 most."""
@@ -40,6 +42,25 @@ def cull_pf(c, d, a, tn, sc, S):
     w2 = f32(f32(f32(wx * wx) + f32(wy * wy)) + f32(wz * wz))
     rhs = f32(f32(max(s, f32(0.0)) * tn) + f32(dr * sc))
     return bool(w2 <= f32(rhs * rhs))
+
+
+def fma(a, b, c):
+    """float32 fused multiply-add (the product of two float32 is exact in
+    float64; one rounding of the sum, then to float32)."""
+    return f32(np.float64(a) * np.float64(b) + np.float64(c))
+
+
+def cull2_pf_half(c, d, a, tn, sc, S):
+    """One half of k_traverse.cuh cull2_pf_s (the packed child prefilter),
+    float32 with its fused operations."""
+    vx, vy, vz = f32(S[0] - c[0]), f32(S[1] - c[1]), f32(S[2] - c[2])
+    mag = f32(f32(f32(f32(abs(vx) + abs(vy)) + abs(vz)) + abs(f32(d))) + f32(S[3]))
+    dr = fma(mag, f32(2.0 ** -12), f32(f32(d) + f32(S[3])))
+    s = fma(vx, a[0], fma(vy, a[1], f32(vz * a[2])))
+    wx, wy, wz = fma(s, -a[0], vx), fma(s, -a[1], vy), fma(s, -a[2], vz)
+    w2 = fma(wx, wx, fma(wy, wy, f32(wz * wz)))
+    rhs = fma(max(s, f32(0.0)), tn, f32(dr * sc))
+    return bool(s >= -dr) and bool(w2 <= f32(rhs * rhs))
 
 
 def random_node():
@@ -86,6 +107,7 @@ def test_prefilter_passes_whenever_a_contained_sphere_passes(orc, trial):
             C = (P.astype(np.float64) + off).astype(f32)
             Rb = np.nextafter(f32(np.linalg.norm(P.astype(np.float64) - C.astype(np.float64)) + float(R)), f32(np.inf))
             assert cull_pf(c, d, a_rec, tn, sc, (C[0], C[1], C[2], Rb)), (node8, P, R, C, Rb)
+            assert cull2_pf_half(c, d, a_rec, tn, sc, (C[0], C[1], C[2], Rb)), (node8, P, R, C, Rb)
     assert passes > 100
 
 
@@ -123,10 +145,12 @@ def test_prefilter_covers_spheres_on_the_float_boundary(orc):
         n += 1
         tn, sc = tansec(alpha)
         assert cull_pf(c, d, a, tn, sc, (P[0], P[1], P[2], Rs)), (node8, P, Rs)
+        assert cull2_pf_half(c, d, a, tn, sc, (P[0], P[1], P[2], Rs)), (node8, P, Rs)
         off = rng.normal(size=3) * 1e-3
         C = (P.astype(np.float64) + off).astype(f32)
         Rb = np.nextafter(f32(np.linalg.norm(P.astype(np.float64) - C.astype(np.float64)) + float(Rs)), f32(np.inf))
         assert cull_pf(c, d, a, tn, sc, (C[0], C[1], C[2], Rb)), (node8, P, Rs, C, Rb)
+        assert cull2_pf_half(c, d, a, tn, sc, (C[0], C[1], C[2], Rb)), (node8, P, Rs, C, Rb)
     assert n > 1000
 
 
@@ -137,5 +161,7 @@ def test_prefilter_rejects_far_spheres():
     assert not cull_pf(c, f32(0.1), a, tn, sc, (50.0, 0.0, 10.0, 1.0))
     assert not cull_pf(c, f32(0.1), a, tn, sc, (0.0, 0.0, -20.0, 1.0))   # behind the apex
     assert cull_pf(c, f32(0.1), a, tn, sc, (0.0, 0.0, 30.0, 1.0))
+    assert not cull2_pf_half(c, f32(0.1), a, tn, sc, (50.0, 0.0, 10.0, 1.0))
+    assert cull2_pf_half(c, f32(0.1), a, tn, sc, (0.0, 0.0, 30.0, 1.0))
     wtn, wsc = tansec(2.0)   # wide: pass-all
     assert cull_pf(c, f32(0.1), np.zeros(3, f32), wtn, wsc, (50.0, 0.0, -10.0, 1.0))
