@@ -1024,6 +1024,10 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
           // PF = 1: warp-uniform sums (lane 0's copy is flushed); PF = 2: sums
           // over the lanes (the top-level skips are per lane), lane 0 adds here
           if (PF == 1 || lane == 0) c_cl_h += __popc(b) * __popc(exm & ~(x | (x << 1)));   // counted, not evaluated
+          if (x == 0u) {   // uniform: no child pair of node j can pass -- counted, nothing evaluated
+            c_ch_t += __popc(b) * __popc(exm);
+            continue;
+          }
         }
         uint32_t m = 0;
 #pragma unroll
