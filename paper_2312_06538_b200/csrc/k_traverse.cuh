@@ -335,6 +335,9 @@ constexpr int LOWQ = 64;                     // capacity of a warp queue below l
 #ifndef CRSH_OBJ_LIST
 #define CRSH_OBJ_LIST 512     // entries of that list (8 bytes each)
 #endif
+#ifndef CRSH_PF_NODES
+#define CRSH_PF_NODES 1   // K8-PF: nodes without a child pair past the prefilter are not iterated
+#endif
 #ifndef CRSH_TRAV_PREFETCH
 #define CRSH_TRAV_PREFETCH 0
 #endif
@@ -987,7 +990,34 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
       c_top_t += __popc(nm);   // every (node, triangle) with a surviving mesh was tested (skipped pairs have none)
       c_top_h += __popc(pm);
       // then each top node that passed for some lane
-      for (uint32_t jm = __reduce_or_sync(CRSH_FULL, pm); jm; jm &= jm - 1) {
+      uint32_t jm0 = __reduce_or_sync(CRSH_FULL, pm);
+#if CRSH_PF_NODES
+      if constexpr (PF > 0 && SMALL && BT == 8 && KT == 8) {
+        if (jm0 != 0u && Lv >= 2) {
+          // the slice's child prefilter now (all 64 children, one packed test
+          // per lane), then only the nodes with a child pair that may pass
+          // are iterated; the others' child tests are counted (and reported
+          // as not evaluated) here
+          pa = __ballot_sync(CRSH_FULL, cull2_pf_s(pairs_s + 80u * lane, pfs) != 0u);
+          pa_done = true;
+          if (PF == 1 || lane == 0) c_cl_t += (uint32_t)(KT * BT);
+          uint32_t t = pa | (pa >> 1);
+          t = (t | (t >> 2)) & 0x11111111u;   // bit 4j: node j has a pair that may pass
+          t = (t | (t >> 3)) & 0x03030303u;
+          t = (t | (t >> 6)) & 0x000F000Fu;
+          t = (t | (t >> 12)) & 0xFFu;        // bit j
+          for (uint32_t sk = jm0 & ~t; sk; sk &= sk - 1) {
+            const int j = __ffs(sk) - 1;
+            const uint32_t bj = __ballot_sync(CRSH_FULL, (pm >> j) & 1u);
+            const uint32_t nt = __popc(bj) * __popc(s_exm[j]);
+            c_ch_t += nt;
+            if (PF == 1 || lane == 0) c_cl_h += nt;
+          }
+          jm0 &= t;
+        }
+      }
+#endif
+      for (uint32_t jm = jm0; jm; jm &= jm - 1) {
         const int j = __ffs(jm) - 1;
         const bool pass = (pm >> j) & 1u;
         const uint32_t b = __ballot_sync(CRSH_FULL, pass);
