@@ -338,6 +338,9 @@ constexpr int LOWQ = 64;                     // capacity of a warp queue below l
 #ifndef CRSH_PF_NODES
 #define CRSH_PF_NODES 1   // K8-PF: nodes without a child pair past the prefilter are not iterated
 #endif
+#ifndef CRSH_APPEND_BITS
+#define CRSH_APPEND_BITS 1   // K8-PF: child survivors appended child by child (ballot ranks)
+#endif
 #ifndef CRSH_TRAV_PREFETCH
 #define CRSH_TRAV_PREFETCH 0
 #endif
@@ -1091,6 +1094,30 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
         c_ch_t += __popc(b) * __popc(exm);
         const uint32_t cnt = __popc(m);
         c_ch_h += cnt;
+#if CRSH_APPEND_BITS
+        if constexpr (PF == 1) {   // (measured on R6; the Z-order instantiation keeps the scan)
+          // few children survive past the prefilter: append child by child
+          // (a ballot per child some lane kept, entries at popc ranks) instead
+          // of a warp scan of the per-lane counts
+          uint32_t om = __reduce_or_sync(CRSH_FULL, m);
+          if (om == 0u) continue;   // the common case: no child survived
+          uint32_t ql = qget(k1);
+          uint2* qb = q + s_qoff[k1];
+          for (; om; om &= om - 1) {
+            const uint32_t c = __ffs(om) - 1;
+            const bool has = (m >> c) & 1u;
+            const uint32_t bc = __ballot_sync(CRSH_FULL, has);
+            CRSH_CHECK(ql + __popc(bc) <= qcap(k1), 803);
+            if (has) qb[ql + __popc(bc & lt)] = make_uint2(cbase | c, tri);
+            ql += __popc(bc);
+          }
+          __syncwarp();
+          qset(k1, ql);
+          if (!QREG || k1 != 1) __syncwarp();
+          drain(false);
+          continue;
+        }
+#endif
         if (__ballot_sync(CRSH_FULL, m != 0u) == 0u) continue;   // the common case: no child survived
         uint32_t incl = cnt;
 #pragma unroll

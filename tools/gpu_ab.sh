@@ -1,0 +1,4 @@
+# A/B: child survivors appended child by child (CRSH_APPEND_BITS), parity on the variant; then the checked build's suite
+CRSH_LIB_PATH=$PWD/build/ab/libcrsh_ab1.so timeout 1500 python -m pytest tests/test_gpu_parity.py tests/test_gpu_headline.py -q -x -k "prefilter or cfg1 or micro or option or cfg2_full or edge or sharded or headline_full_frame_parity and 3-3" > gpurun_out/ab_par.log 2>&1; tail -3 gpurun_out/ab_par.log
+bash tools/ab_trav.sh "4 3 2" "--zorder, " ab0 ab1 2>/dev/null
+bash tools/gpu_checked.sh
