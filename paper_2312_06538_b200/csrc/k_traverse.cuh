@@ -341,6 +341,9 @@ constexpr int LOWQ = 64;                     // capacity of a warp queue below l
 #ifndef CRSH_APPEND_BITS
 #define CRSH_APPEND_BITS 1   // K8-PF: child survivors appended child by child (ballot ranks)
 #endif
+#ifndef CRSH_PF_BULK
+#define CRSH_PF_BULK 1   // K8-PF: skipped nodes' child tests counted with one warp sum when the group is full
+#endif
 #ifndef CRSH_TRAV_PREFETCH
 #define CRSH_TRAV_PREFETCH 0
 #endif
@@ -534,6 +537,7 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
   const uint32_t pairs_s = (uint32_t)__cvta_generic_to_shared(s_pairs);   // 32-bit shared address (CRSH_LDS32)
   const uint32_t tpairs_s = (uint32_t)__cvta_generic_to_shared(s_tpairs);
   __shared__ uint32_t s_item, s_cur_g, s_n_act, s_carry, s_carry_c, s_blk;
+  __shared__ uint32_t s_exm_full;   // every top node of the group has all B children
 #if CRSH_OBJ_TWOPHASE
   __shared__ uint32_t s_lcnt, s_lclaim, s_lexh;          // object tree: cluster list fill / claim, blocks exhausted
   __shared__ uint2 s_list[OBJ ? CRSH_OBJ_LIST : 1];      // object tree: (cluster, node mask) of passing clusters
@@ -689,7 +693,7 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
           rp[3 * RAY_PLANE] = make_float4(a1.z, b1.z, a1.w, b1.w);
         }
       }
-      if (tid == 0) { s_carry = 0u; s_carry_c = 0u; }
+      if (tid == 0) { s_carry = 0u; s_carry_c = 0u; s_exm_full = 1u; }
       __syncthreads();
       for (int jp = tid; jp < (K + 1) / 2; jp += TRAV_THREADS) {
         const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -714,6 +718,7 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
             m |= (r >= 0.0f ? 1u : 0u) << c;
           }
           s_exm[j] = m;
+          if (m != (B == 32 ? 0xFFFFFFFFu : ((1u << B) - 1u))) s_exm_full = 0u;   // benign race: all write 0
         }
         if (SMALL) {
           const uint32_t n_pairs = s_pg[k1] / 2u;
@@ -1009,12 +1014,21 @@ __global__ void __launch_bounds__(TRAV_THREADS, LVT == 2 ? CRSH_TRAV_MINB_LV2 : 
           t = (t | (t >> 3)) & 0x03030303u;
           t = (t | (t >> 6)) & 0x000F000Fu;
           t = (t | (t >> 12)) & 0xFFu;        // bit j
-          for (uint32_t sk = jm0 & ~t; sk; sk &= sk - 1) {
-            const int j = __ffs(sk) - 1;
-            const uint32_t bj = __ballot_sync(CRSH_FULL, (pm >> j) & 1u);
-            const uint32_t nt = __popc(bj) * __popc(s_exm[j]);
-            c_ch_t += nt;
-            if (PF == 1 || lane == 0) c_cl_h += nt;
+          const uint32_t skn = jm0 & ~t;
+          if (skn != 0u) {
+            if (CRSH_PF_BULK && s_exm_full) {   // uniform: every skipped node has B children -- one warp sum
+              const uint32_t nt = (uint32_t)BT * __reduce_add_sync(CRSH_FULL, (uint32_t)__popc(pm & skn));
+              c_ch_t += nt;
+              if (PF == 1 || lane == 0) c_cl_h += nt;
+            } else {
+              for (uint32_t sk = skn; sk; sk &= sk - 1) {
+                const int j = __ffs(sk) - 1;
+                const uint32_t bj = __ballot_sync(CRSH_FULL, (pm >> j) & 1u);
+                const uint32_t nt = __popc(bj) * __popc(s_exm[j]);
+                c_ch_t += nt;
+                if (PF == 1 || lane == 0) c_cl_h += nt;
+              }
+            }
           }
           jm0 &= t;
         }
