@@ -435,7 +435,7 @@ def run_crsh(args):
             "flops_convention": f"{EQ9_FLOPS} flops per Eq 9 test and {MT_FLOPS} per Moller-Trumbore test, the "
                                 f"operations of the evaluated formulas (DESIGN.md §5); with SURVEY §8(d)'s estimates "
                                 f"(28 / 55) frac = {tfl_s / peak_tflops:.4f}; Eq 9 tests counted as evaluated: the "
-                                f"paper's counts - child tests skipped by the child prefilter "
+                                f"paper's counts - tests skipped by the prefilter "
                                 f"({int(sum(st.get('skipped_tests', [0])))}) + prefilter tests "
                                 f"({int(sum(st.get('prefilter_tests', [0])))})",
             "frac_survey_convention": round(tfl_s / peak_tflops, 4),
