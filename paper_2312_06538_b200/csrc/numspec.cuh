@@ -312,10 +312,13 @@ __device__ __forceinline__ uint32_t cull2_bits(const float4* rec, f2 Px, f2 Py, 
 }
 // cull2_ns with the paired record read through a 32-bit shared-memory address
 // (ld.shared: no generic-to-shared window computation per record; the same
-// values, so the same decisions)
+// values, so the same decisions). Volatile with a memory clobber: the
+// compiler must not hoist these loads across the group setup that writes the
+// records (an address that does not change between groups would otherwise
+// look loop-invariant); the SASS of the K8 instantiations is unchanged.
 __device__ __forceinline__ float4 lds128(uint32_t addr) {
   float4 v;
-  asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr) : "memory");
   return v;
 }
 __device__ __forceinline__ void cull2_ns_s(uint32_t rec, f2 Px, f2 Py, f2 Pz, f2 R, bool& p0, bool& p1) {
